@@ -1,0 +1,131 @@
+/*
+ * bloch_b200.h — C-ABI of libbloch_b200.so, the sm_100a Bloch event-stream engine.
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference
+ * (pure Python, /root/reference/pkg/src/mrsim) has no FFI of its own; the seam
+ * it exposes — and that its tests monkeypatch (tests/test_engine.py:214-222) —
+ * is
+ *
+ *     engine.compute_block(tables: OperatorTables, block: SpinBlock)
+ *         -> (echoes complex128 (n_acq, max_ns), [snapshot (n,3) f64 | None])
+ *                                                   (engine.py:259-310)
+ *
+ * fed by the master precompute engine.precompute_sequence_tables
+ * (engine.py:83-164) and folded by engine.run / _run_pool (engine.py:465-595).
+ * The entry points below replace exactly that seam; the ctypes binding that
+ * the reference side would add is shown in INTEGRATION.md.
+ *
+ *   reference                                     this ABI
+ *   --------------------------------------------  --------------------------------
+ *   OperatorTables / EsTable (engine.py:51-80)    bloch_set_tables()
+ *   compute_block (engine.py:259-310)             bloch_compute_block()
+ *   worker exception -> WorkerPanic               status < 0 + bloch_last_error()
+ *     (engine.py:455-459, 575-577; errors.py:57)
+ *   InvalidParameter (engine.py:467-473)          BLOCH_E_INVALID
+ *
+ * Conventions: plain pointers and sizes only; every call returns an int
+ * status (0 = ok, < 0 = error) and leaves a thread-local message readable via
+ * bloch_last_error().  A context is bound to one CUDA device and is not
+ * re-entrant: serialise calls per context.  The caller owns every buffer it
+ * passes; the context owns only its scratch (compiled program, staged spins,
+ * partial k-space) and retains no caller pointer past a call.
+ */
+#ifndef BLOCH_B200_H
+#define BLOCH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BLOCH_ABI_VERSION 1
+
+/* status codes */
+#define BLOCH_OK 0
+#define BLOCH_E_INVALID -1 /* bad argument          -> mrsim InvalidParameter      */
+#define BLOCH_E_CUDA -2    /* CUDA error / no device -> mrsim WorkerPanic          */
+#define BLOCH_E_STATE -3   /* call out of order (e.g. compute before set_tables)  */
+#define BLOCH_E_NOMEM -4   /* device allocation failed                            */
+
+/* precision of the per-spin state inside the kernel */
+#define BLOCH_PREC_F32 32 /* fp32 state, fp64 phase / signal accumulation (default) */
+#define BLOCH_PREC_F64 64 /* fp64 everywhere (for the reference's 1e-12 unit tests) */
+
+/* bloch_compute_block flags */
+#define BLOCH_IN_DEVICE 1u  /* spin arrays are device pointers (else host)          */
+#define BLOCH_OUT_DEVICE 2u /* echoes/snapshot outputs are device pointers (else host) */
+#define BLOCH_NO_SYNC 4u    /* device outputs only: do not synchronise the stream   */
+
+typedef struct bloch_ctx bloch_ctx;
+
+/* Library / ABI identification. */
+const char* bloch_version(void);
+int bloch_abi_version(void);
+/* Message of the last failed call on this thread ("" if none). */
+const char* bloch_last_error(void);
+/* Number of visible CUDA devices (0 when none; status BLOCH_E_CUDA if the driver fails). */
+int bloch_device_count(int* out);
+
+/* pseudo-device of a compile-only context (no CUDA calls; set_tables / program_stats only) */
+#define BLOCH_HOST_ONLY -1
+
+/* Create a context on `device` (or BLOCH_HOST_ONLY) with state precision BLOCH_PREC_F32 / _F64. */
+int bloch_create(int device, int precision, bloch_ctx** out);
+int bloch_destroy(bloch_ctx* ctx);
+/* Stream used for all work of this context (a cudaStream_t; NULL = context-owned). */
+int bloch_set_stream(bloch_ctx* ctx, void* stream);
+
+/*
+ * Upload the event tables of one sequence — the flattened OperatorTables.
+ * For elementary sequence i (0 <= i < n_es) its events are
+ * [es_ev_offset[i], es_ev_offset[i+1]) of the ev_* arrays (EsTable.ev_*,
+ * engine.py:51-70); es_has_pulse[i] != 0 means EsTable.pulse_mat is the 3x3
+ * row-major matrix at es_pulse_mat + 9*i; es_acq[i] is EsTable.acq (-1 when
+ * the ES does not acquire).  The library compiles the stream into its device
+ * program (rotations, generic intervals, uniform ADC windows).
+ */
+int bloch_set_tables(bloch_ctx* ctx, int32_t n_es, const int64_t* es_ev_offset,
+                     const uint8_t* es_has_pulse, const double* es_pulse_mat,
+                     const int32_t* es_acq, const double* ev_dt, const double* ev_dmom,
+                     const uint8_t* ev_sample, const int32_t* ev_snap, int32_t n_acq,
+                     int32_t max_samples, int32_t n_snap);
+
+/* Statistics of the compiled program: events E (reference table size incl.
+ * pulses), ADC samples, and op counts of each kind. */
+int bloch_program_stats(const bloch_ctx* ctx, int64_t* n_events, int64_t* n_samples,
+                        int64_t* n_rot, int64_t* n_interval, int64_t* n_window_ops,
+                        int64_t* n_window_samples);
+
+/*
+ * Evolve one spin block through the uploaded tables — compute_block.
+ *
+ *   n        spins in the block (SpinBlock.n, engine.py:187-189); n >= 0
+ *   pos      n*3 float64, row-major (SpinBlock.pos)
+ *   mx,my,mz,t1,t2,m0,domega   n float64 each (SpinBlock fields)
+ *   weight   complex128 interleaved (re, im): n_coils*n*2 doubles laid out
+ *            [coil][spin]; NULL means the uniform weight 1+0j (n_coils = 1)
+ *   echoes_out  n_coils * n_acq * max_samples complex128 (interleaved),
+ *            un-normalised partial sums exactly as compute_block returns them
+ *            (the caller divides by the global spin count, engine.py:507)
+ *   snaps_out   n_snap * n * 3 float64, or NULL
+ *   snap_present n_snap bytes set to 1 where the snapshot was taken, or NULL
+ *   flags    BLOCH_IN_DEVICE / BLOCH_OUT_DEVICE / BLOCH_NO_SYNC
+ */
+int bloch_compute_block(bloch_ctx* ctx, int64_t n, const double* pos, const double* mx,
+                        const double* my, const double* mz, const double* t1,
+                        const double* t2, const double* m0, const double* domega,
+                        const double* weight, int32_t n_coils, double* echoes_out,
+                        double* snaps_out, uint8_t* snap_present, uint32_t flags);
+
+/* Device time (ms, CUDA events on the context stream) of the last
+ * bloch_compute_block: the integrator kernel alone, and all device work of the
+ * call (staging kernels + integrator + reduction). */
+int bloch_last_timing(const bloch_ctx* ctx, float* kernel_ms, float* device_ms,
+                      int32_t* kernel_launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BLOCH_B200_H */

@@ -1,0 +1,453 @@
+// C-ABI of libbloch_b200.so — see include/bloch_b200.h for the contract and the
+// reference interfaces each entry point replaces.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/bloch_b200.h"
+#include "kernels.h"
+#include "program_host.h"
+
+#ifndef BLOCH_VERSION_STRING
+#define BLOCH_VERSION_STRING "bloch_b200 0.1.0 (sm_100a)"
+#endif
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+struct CudaError : std::runtime_error {
+  explicit CudaError(const std::string& m) : std::runtime_error(m) {}
+};
+struct InvalidArg : std::runtime_error {
+  explicit InvalidArg(const std::string& m) : std::runtime_error(m) {}
+};
+
+inline void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* ensure(size_t bytes) {
+    if (bytes <= cap) return p;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    if (bytes == 0) return nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      throw CudaError(std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+    }
+    cap = bytes;
+    return p;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+}  // namespace
+
+struct bloch_ctx {
+  int device = 0;
+  int precision = BLOCH_PREC_F32;
+  int n_sm = 148;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  bloch::Program prog;
+  bool has_prog = false;
+  std::vector<uint8_t> snap_present;
+  DevBuf d_ops, d_gev, d_sample_g;
+  DevBuf in_pos, in_mx, in_my, in_mz, in_t1, in_t2, in_m0, in_dw, in_w;
+  DevBuf x, y, z, r1, r2, wpad;
+  DevBuf partial, echo, snaps;
+  float kernel_ms = 0.f, device_ms = 0.f;
+  int launches = 0;
+};
+
+namespace {
+
+struct Variant {
+  int prec, S, NC;
+};
+
+// pick (S, NC) for a block of n spins with ncp (power-of-two) coils
+Variant pick_variant(int prec, int64_t n, int ncp, int n_sm) {
+  if (prec == BLOCH_PREC_F32) {
+    switch (ncp) {
+      case 1: return {32, n >= int64_t(n_sm) * 8 * 64 ? 8 : 1, 1};
+      case 2: return {32, 4, 2};
+      case 4: return {32, 4, 4};
+      default: return {32, 2, 8};
+    }
+  }
+  switch (ncp) {
+    case 1: return {64, n >= int64_t(n_sm) * 4 * 64 ? 4 : 1, 1};
+    case 2: return {64, 2, 2};
+    case 4: return {64, 2, 4};
+    default: return {64, 1, 8};
+  }
+}
+
+template <typename R, int S, int NC>
+cudaError_t dispatch_one(const Variant& v, const bloch::KParams& kp, int grid, int threads,
+                         cudaStream_t st, bool* matched) {
+  if (v.prec == int(8 * sizeof(R)) && v.S == S && v.NC == NC) {
+    *matched = true;
+    return bloch::launch_integrate<R, S, NC>(kp, grid, threads, st);
+  }
+  return cudaSuccess;
+}
+
+cudaError_t dispatch(const Variant& v, const bloch::KParams& kp, int grid, int threads,
+                     cudaStream_t st) {
+  bool matched = false;
+  cudaError_t e = cudaSuccess;
+#define BLOCH_DISPATCH(R, S, NC) \
+  if (!matched && e == cudaSuccess) e = dispatch_one<R, S, NC>(v, kp, grid, threads, st, &matched);
+  BLOCH_FOR_EACH_VARIANT(BLOCH_DISPATCH)
+#undef BLOCH_DISPATCH
+  if (!matched) throw InvalidArg("no kernel variant for the requested precision/coils");
+  return e;
+}
+
+void upload(DevBuf& b, const void* src, size_t bytes, cudaStream_t st) {
+  b.ensure(bytes);
+  if (bytes) ck(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, st), "H2D");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bloch_version(void) { return BLOCH_VERSION_STRING; }
+int bloch_abi_version(void) { return BLOCH_ABI_VERSION; }
+const char* bloch_last_error(void) { return g_err.c_str(); }
+
+int bloch_device_count(int* out) {
+  if (!out) return fail(BLOCH_E_INVALID, "out is NULL");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) {
+    cudaGetLastError();
+    *out = 0;
+    return BLOCH_OK;
+  }
+  if (e != cudaSuccess) return fail(BLOCH_E_CUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+  *out = n;
+  return BLOCH_OK;
+}
+
+int bloch_create(int device, int precision, bloch_ctx** out) {
+  if (!out) return fail(BLOCH_E_INVALID, "out is NULL");
+  *out = nullptr;
+  if (precision != BLOCH_PREC_F32 && precision != BLOCH_PREC_F64)
+    return fail(BLOCH_E_INVALID, "precision must be 32 or 64");
+  if (device == BLOCH_HOST_ONLY) {  // compile-only context: no CUDA calls at all
+    bloch_ctx* c = new bloch_ctx();
+    c->device = BLOCH_HOST_ONLY;
+    c->precision = precision;
+    *out = c;
+    return BLOCH_OK;
+  }
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return fail(BLOCH_E_CUDA, "no CUDA device available (the Bloch engine has no CPU fallback)");
+  }
+  if (device < 0 || device >= n) return fail(BLOCH_E_INVALID, "device index out of range");
+  bloch_ctx* c = new bloch_ctx();
+  try {
+    c->device = device;
+    c->precision = precision;
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop;
+    ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major < 10)
+      throw CudaError("device is sm_" + std::to_string(prop.major) + std::to_string(prop.minor) +
+                      "; this library is built for sm_100a only");
+    c->n_sm = prop.multiProcessorCount;
+    ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    c->own_stream = true;
+    for (auto& ev : c->ev) ck(cudaEventCreate(&ev), "cudaEventCreate");
+  } catch (const std::exception& ex) {
+    bloch_destroy(c);
+    return fail(BLOCH_E_CUDA, ex.what());
+  }
+  *out = c;
+  return BLOCH_OK;
+}
+
+int bloch_destroy(bloch_ctx* c) {
+  if (!c) return BLOCH_OK;
+  if (c->device == BLOCH_HOST_ONLY) {
+    delete c;
+    return BLOCH_OK;
+  }
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (DevBuf* b : {&c->d_ops, &c->d_gev, &c->d_sample_g, &c->in_pos, &c->in_mx, &c->in_my, &c->in_mz,
+                    &c->in_t1, &c->in_t2, &c->in_m0, &c->in_dw, &c->in_w, &c->x, &c->y, &c->z, &c->r1,
+                    &c->r2, &c->wpad, &c->partial, &c->echo, &c->snaps})
+    b->release();
+  for (auto& ev : c->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return BLOCH_OK;
+}
+
+int bloch_set_stream(bloch_ctx* c, void* stream) {
+  if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
+  if (c->device == BLOCH_HOST_ONLY) return fail(BLOCH_E_STATE, "host-only context has no stream");
+  cudaSetDevice(c->device);
+  if (c->own_stream && c->stream) {
+    cudaStreamSynchronize(c->stream);
+    cudaStreamDestroy(c->stream);
+  }
+  if (stream) {
+    c->stream = static_cast<cudaStream_t>(stream);
+    c->own_stream = false;
+  } else {
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return fail(BLOCH_E_CUDA, cudaGetErrorString(e));
+    c->own_stream = true;
+  }
+  return BLOCH_OK;
+}
+
+int bloch_set_tables(bloch_ctx* c, int32_t n_es, const int64_t* es_ev_offset,
+                     const uint8_t* es_has_pulse, const double* es_pulse_mat, const int32_t* es_acq,
+                     const double* ev_dt, const double* ev_dmom, const uint8_t* ev_sample,
+                     const int32_t* ev_snap, int32_t n_acq, int32_t max_samples, int32_t n_snap) {
+  if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
+  if (n_es < 0) return fail(BLOCH_E_INVALID, "n_es < 0");
+  if (n_es > 0 && (!es_ev_offset || !es_has_pulse || !es_pulse_mat || !es_acq))
+    return fail(BLOCH_E_INVALID, "NULL elementary-sequence array");
+  const int64_t E = n_es > 0 ? es_ev_offset[n_es] : 0;
+  if (E > 0 && (!ev_dt || !ev_dmom || !ev_sample || !ev_snap))
+    return fail(BLOCH_E_INVALID, "NULL event array");
+  bloch::TablesView tv{n_es, es_ev_offset, es_has_pulse, es_pulse_mat, es_acq, ev_dt,
+                       ev_dmom, ev_sample, ev_snap, n_acq, max_samples, n_snap};
+  try {
+    bloch::Program prog;
+    bloch::compile_program(tv, prog);
+    if (c->device != BLOCH_HOST_ONLY) {
+      ck(cudaSetDevice(c->device), "cudaSetDevice");
+      upload(c->d_ops, prog.ops.data(), prog.ops.size() * sizeof(bloch::DevOp), c->stream);
+      upload(c->d_gev, prog.gev.data(), prog.gev.size() * sizeof(bloch::GEv), c->stream);
+      upload(c->d_sample_g, prog.sample_g.data(), prog.sample_g.size() * sizeof(int64_t), c->stream);
+      ck(cudaStreamSynchronize(c->stream), "set_tables sync");
+    }
+    c->snap_present.assign(static_cast<size_t>(n_snap), 0);
+    for (const auto& op : prog.ops)
+      if (op.kind == bloch::OP_EVENT && op.aux >= 0) c->snap_present[op.aux] = 1;
+    c->prog = std::move(prog);
+    c->has_prog = true;
+  } catch (const std::invalid_argument& ex) {
+    c->has_prog = false;
+    return fail(BLOCH_E_INVALID, std::string("invalid tables: ") + ex.what());
+  } catch (const std::exception& ex) {
+    c->has_prog = false;
+    return fail(BLOCH_E_CUDA, ex.what());
+  }
+  return BLOCH_OK;
+}
+
+int bloch_program_stats(const bloch_ctx* c, int64_t* n_events, int64_t* n_samples, int64_t* n_rot,
+                        int64_t* n_interval, int64_t* n_window_ops, int64_t* n_window_samples) {
+  if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
+  if (!c->has_prog) return fail(BLOCH_E_STATE, "no tables uploaded");
+  if (n_events) *n_events = c->prog.n_events;
+  if (n_samples) *n_samples = c->prog.n_samples;
+  if (n_rot) *n_rot = c->prog.n_rot;
+  if (n_interval) *n_interval = c->prog.n_interval + c->prog.n_gsamp_events;
+  if (n_window_ops) *n_window_ops = c->prog.n_window_ops;
+  if (n_window_samples) *n_window_samples = c->prog.n_window_samples;
+  return BLOCH_OK;
+}
+
+int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double* mx,
+                        const double* my, const double* mz, const double* t1, const double* t2,
+                        const double* m0, const double* domega, const double* weight,
+                        int32_t n_coils, double* echoes_out, double* snaps_out,
+                        uint8_t* snap_present, uint32_t flags) {
+  if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
+  if (!c->has_prog) return fail(BLOCH_E_STATE, "bloch_set_tables must be called first");
+  if (c->device == BLOCH_HOST_ONLY) return fail(BLOCH_E_STATE, "host-only context cannot compute");
+  if (n < 0) return fail(BLOCH_E_INVALID, "n < 0");
+  if (n_coils < 1 || n_coils > 8) return fail(BLOCH_E_INVALID, "n_coils must be in [1, 8]");
+  if (n_coils > 1 && !weight) return fail(BLOCH_E_INVALID, "n_coils > 1 requires a weight array");
+  if (n > 0 && (!pos || !mx || !my || !mz || !t1 || !t2 || !m0 || !domega))
+    return fail(BLOCH_E_INVALID, "NULL spin array");
+  const bloch::Program& P = c->prog;
+  const int64_t G = static_cast<int64_t>(P.n_acq) * P.max_samples;
+  if (G > 0 && !echoes_out) return fail(BLOCH_E_INVALID, "echoes_out is NULL");
+  const bool in_dev = flags & BLOCH_IN_DEVICE, out_dev = flags & BLOCH_OUT_DEVICE;
+  try {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    cudaStream_t st = c->stream;
+    c->launches = 0;
+    ck(cudaEventRecord(c->ev[0], st), "event");
+    const int ncp = n_coils <= 1 ? 1 : n_coils <= 2 ? 2 : n_coils <= 4 ? 4 : 8;
+    const size_t nd = static_cast<size_t>(n) * sizeof(double);
+
+    // 1. inputs on the device
+    const double *d_pos = pos, *d_mx = mx, *d_my = my, *d_mz = mz, *d_t1 = t1, *d_t2 = t2,
+                 *d_m0 = m0, *d_dw = domega, *d_w = weight;
+    if (!in_dev && n > 0) {
+      upload(c->in_pos, pos, 3 * nd, st);
+      upload(c->in_mx, mx, nd, st);
+      upload(c->in_my, my, nd, st);
+      upload(c->in_mz, mz, nd, st);
+      upload(c->in_t1, t1, nd, st);
+      upload(c->in_t2, t2, nd, st);
+      upload(c->in_m0, m0, nd, st);
+      upload(c->in_dw, domega, nd, st);
+      d_pos = c->in_pos.as<double>();
+      d_mx = c->in_mx.as<double>();
+      d_my = c->in_my.as<double>();
+      d_mz = c->in_mz.as<double>();
+      d_t1 = c->in_t1.as<double>();
+      d_t2 = c->in_t2.as<double>();
+      d_m0 = c->in_m0.as<double>();
+      d_dw = c->in_dw.as<double>();
+      if (weight) {
+        upload(c->in_w, weight, 2 * nd * n_coils, st);
+        d_w = c->in_w.as<double>();
+      }
+    }
+    // 2. staging: SoA positions, 1/T1, 1/T2, padded weights
+    if (n > 0) {
+      c->x.ensure(nd);
+      c->y.ensure(nd);
+      c->z.ensure(nd);
+      c->r1.ensure(nd);
+      c->r2.ensure(nd);
+      ck(bloch::launch_prep(n, d_pos, d_t1, d_t2, c->x.as<double>(), c->y.as<double>(),
+                            c->z.as<double>(), c->r1.as<double>(), c->r2.as<double>(), st),
+         "prep kernel");
+      c->launches++;
+      if (d_w && ncp != n_coils) {
+        c->wpad.ensure(2 * nd * ncp);
+        ck(bloch::launch_pad_weights(n, n_coils, ncp, d_w, c->wpad.as<double>(), st), "pad kernel");
+        c->launches++;
+        d_w = c->wpad.as<double>();
+      }
+    }
+    // 3. outputs
+    const size_t echo_bytes = static_cast<size_t>(G) * n_coils * 2 * sizeof(double);
+    double* d_echo = out_dev ? echoes_out : static_cast<double*>(c->echo.ensure(echo_bytes));
+    if (echo_bytes) ck(cudaMemsetAsync(d_echo, 0, echo_bytes, st), "memset echoes");
+    const size_t snap_bytes = static_cast<size_t>(P.n_snap) * n * 3 * sizeof(double);
+    double* d_snap = nullptr;
+    if (snaps_out && snap_bytes) {
+      d_snap = out_dev ? snaps_out : static_cast<double*>(c->snaps.ensure(snap_bytes));
+      ck(cudaMemsetAsync(d_snap, 0, snap_bytes, st), "memset snapshots");
+    }
+    // 4. integrator + ordered fold
+    float kms = 0.f;
+    if (n > 0) {
+      const Variant v = pick_variant(c->precision, n, ncp, c->n_sm);
+      const int max_t = 512;
+      const int64_t per_wave = int64_t(c->n_sm) * v.S * max_t;
+      const int64_t waves = (n + per_wave - 1) / per_wave;
+      int64_t threads = (n + int64_t(c->n_sm) * waves * v.S - 1) / (int64_t(c->n_sm) * waves * v.S);
+      threads = ((threads + 31) / 32) * 32;
+      threads = std::max<int64_t>(32, std::min<int64_t>(max_t, threads));
+      const int64_t spc = threads * v.S;
+      const int64_t grid = (n + spc - 1) / spc;
+      const int64_t n_slots = P.n_samples * ncp;
+      const size_t rsz = v.prec == 32 ? sizeof(float) : sizeof(double);
+      c->partial.ensure(static_cast<size_t>(std::max<int64_t>(1, grid * n_slots * 2)) * rsz);
+      bloch::KParams kp{};
+      kp.ops = c->d_ops.as<bloch::DevOp>();
+      kp.n_ops = static_cast<int32_t>(P.ops.size());
+      kp.spins_per_cta = static_cast<int32_t>(spc);
+      kp.gev = c->d_gev.as<bloch::GEv>();
+      kp.n = n;
+      kp.x = c->x.as<double>();
+      kp.y = c->y.as<double>();
+      kp.z = c->z.as<double>();
+      kp.dw = d_dw;
+      kp.r1 = c->r1.as<double>();
+      kp.r2 = c->r2.as<double>();
+      kp.m0 = d_m0;
+      kp.mx0 = d_mx;
+      kp.my0 = d_my;
+      kp.mz0 = d_mz;
+      kp.w = d_w;
+      kp.partial = c->partial.p;
+      kp.part_stride = n_slots * 2;
+      kp.snaps = d_snap;
+      ck(cudaEventRecord(c->ev[1], st), "event");
+      ck(dispatch(v, kp, static_cast<int>(grid), static_cast<int>(threads), st), "integrate kernel");
+      ck(cudaEventRecord(c->ev[2], st), "event");
+      c->launches++;
+      if (n_slots > 0) {
+        if (v.prec == 32)
+          ck(bloch::launch_reduce<float>(c->partial.as<float>(), static_cast<int>(grid), n_slots,
+                                         n_coils, ncp, c->d_sample_g.as<int64_t>(), G, d_echo, st),
+             "reduce kernel");
+        else
+          ck(bloch::launch_reduce<double>(c->partial.as<double>(), static_cast<int>(grid), n_slots,
+                                          n_coils, ncp, c->d_sample_g.as<int64_t>(), G, d_echo, st),
+             "reduce kernel");
+        c->launches++;
+      }
+    } else {
+      ck(cudaEventRecord(c->ev[1], st), "event");
+      ck(cudaEventRecord(c->ev[2], st), "event");
+    }
+    // 5. outputs to the host
+    if (!out_dev) {
+      if (echo_bytes) ck(cudaMemcpyAsync(echoes_out, d_echo, echo_bytes, cudaMemcpyDeviceToHost, st), "D2H echoes");
+      if (d_snap) ck(cudaMemcpyAsync(snaps_out, d_snap, snap_bytes, cudaMemcpyDeviceToHost, st), "D2H snapshots");
+    }
+    ck(cudaEventRecord(c->ev[3], st), "event");
+    if (!out_dev || !(flags & BLOCH_NO_SYNC)) {
+      ck(cudaStreamSynchronize(st), "stream sync");
+      ck(cudaEventElapsedTime(&kms, c->ev[1], c->ev[2]), "elapsed");
+      c->kernel_ms = kms;
+      ck(cudaEventElapsedTime(&c->device_ms, c->ev[0], c->ev[3]), "elapsed");
+    }
+    if (snap_present)
+      for (int32_t i = 0; i < P.n_snap; ++i) snap_present[i] = c->snap_present[i];
+  } catch (const InvalidArg& ex) {
+    return fail(BLOCH_E_INVALID, ex.what());
+  } catch (const std::exception& ex) {
+    return fail(BLOCH_E_CUDA, ex.what());
+  }
+  return BLOCH_OK;
+}
+
+int bloch_last_timing(const bloch_ctx* c, float* kernel_ms, float* device_ms, int32_t* launches) {
+  if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
+  if (kernel_ms) *kernel_ms = c->kernel_ms;
+  if (device_ms) *device_ms = c->device_ms;
+  if (launches) *launches = c->launches;
+  return BLOCH_OK;
+}
+
+}  // extern "C"

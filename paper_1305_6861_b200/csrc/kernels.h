@@ -1,0 +1,56 @@
+// Kernel parameter block, compile-time variants and host launchers.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "program.h"
+
+namespace bloch {
+
+struct KParams {
+  const DevOp* ops;
+  int32_t n_ops;
+  int32_t spins_per_cta;  // S * blockDim.x
+  const GEv* gev;
+  int64_t n;  // spins
+  const double *x, *y, *z, *dw;  // positions (m), off-resonance (rad/s)
+  const double *r1, *r2, *m0;    // 1/T1, 1/T2, equilibrium magnetisation
+  const double *mx0, *my0, *mz0; // initial state (SpinBlock.mx/my/mz)
+  const double* w;               // [NC][n][2] complex weights, or nullptr = 1+0j
+  void* partial;                 // [grid][part_stride] of R
+  int64_t part_stride;           // n_samples * NC * 2
+  double* snaps;                 // [n_snap][n][3] or nullptr
+};
+
+template <typename R, int S, int NC>
+struct KernelTraits {
+  static constexpr int kMaxThreads = 512;
+};
+
+// (real type, spins per thread, coils) instantiated in bloch_kernels.cu
+#define BLOCH_FOR_EACH_VARIANT(X) \
+  X(float, 8, 1)                  \
+  X(float, 1, 1)                  \
+  X(float, 4, 2)                  \
+  X(float, 4, 4)                  \
+  X(float, 2, 8)                  \
+  X(double, 4, 1)                 \
+  X(double, 1, 1)                 \
+  X(double, 2, 2)                 \
+  X(double, 2, 4)                 \
+  X(double, 1, 8)
+
+template <typename R, int S, int NC>
+cudaError_t launch_integrate(const KParams& kp, int grid, int threads, cudaStream_t stream);
+template <typename R, int S, int NC>
+cudaError_t kernel_attrs(int* max_threads, int* regs);
+
+cudaError_t launch_prep(int64_t n, const double* pos, const double* t1, const double* t2, double* x,
+                        double* y, double* z, double* r1, double* r2, cudaStream_t stream);
+cudaError_t launch_pad_weights(int64_t n, int nc, int ncp, const double* w, double* out,
+                               cudaStream_t stream);
+template <typename R>
+cudaError_t launch_reduce(const R* part, int grid, int64_t n_slots, int nc, int ncp,
+                          const int64_t* sample_g, int64_t G, double* out, cudaStream_t stream);
+
+}  // namespace bloch

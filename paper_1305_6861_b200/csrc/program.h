@@ -1,0 +1,51 @@
+// Device program of the Bloch event-stream engine (shared by the host
+// compiler, program.cpp, and the kernels, bloch_kernels.cu).
+//
+// The reference walks OperatorTables.entries in Python (engine.py:276-308):
+// per elementary sequence an optional 3x3 pulse (277-283), then per event an
+// optional precession+relaxation (288-302), an optional ADC sample (303-305)
+// and an optional snapshot (306-308).  The compiler flattens that walk into a
+// linear op stream whose control flow is uniform across a CTA:
+//
+//   OP_ROT     hard pulse, 3x3 rotation                    (engine.py:277-283)
+//   OP_EVENT   one interval: precession (+ relaxation when dt != 0), then an
+//              optional snapshot                            (engine.py:286-302, 306-308)
+//   OP_GSAMP   1..8 consecutive intervals each followed by an ADC sample, with
+//              per-event (dt, dmom) from the side table     (engine.py:286-305)
+//   OP_WINDOW  a uniform ADC window: an optional leading no-op sample followed
+//              by `count - lead` identical (dt, dmom) intervals each followed
+//              by a sample — the ES-level hoisting the reference's relax cache
+//              (engine.py:292-299) only does for the exponentials
+#pragma once
+#include <stdint.h>
+
+namespace bloch {
+
+enum OpKind : int32_t { OP_ROT = 1, OP_EVENT = 2, OP_GSAMP = 3, OP_WINDOW = 4 };
+
+// flags of an interval (OP_EVENT.count, GEv.flags)
+enum : int32_t { EV_MOVE = 1, EV_RELAX = 2 };
+
+struct alignas(16) DevOp {
+  int32_t kind;
+  int32_t count;  // WINDOW: samples recorded; GSAMP: events (1..8); EVENT: EV_* flags
+  int32_t s0;     // WINDOW/GSAMP: compact index of the first recorded sample
+  int32_t aux;    // WINDOW: lead flag; GSAMP: first side-table entry; EVENT: snapshot or -1
+  double p[9];    // ROT: row-major fp64 matrix; EVENT/WINDOW: dt, dmx, dmy, dmz
+  float f[9];     // ROT: fp32 copy of the matrix
+  int32_t pad;
+};
+static_assert(sizeof(DevOp) == 128, "DevOp must be 128 bytes");
+
+struct alignas(16) GEv {  // one generic sampled interval
+  double dt, dmx, dmy, dmz;
+  int32_t flags;
+  int32_t pad[3];
+};
+static_assert(sizeof(GEv) == 48, "GEv must be 48 bytes");
+
+constexpr int kChunkSlots = 8;   // ADC slots reduced per warp transpose (samples x coils)
+constexpr int kStripSlots = 64;  // slots buffered per warp in shared memory before a CTA flush
+constexpr int kMinWindow = 4;    // shortest uniform run compiled as OP_WINDOW
+
+}  // namespace bloch

@@ -1,0 +1,37 @@
+// Host-side view of the flattened tables and the compiled program.
+#pragma once
+#include <stdint.h>
+
+#include <vector>
+
+#include "program.h"
+
+namespace bloch {
+
+struct TablesView {  // borrowed pointers, see bloch_set_tables() in include/bloch_b200.h
+  int32_t n_es;
+  const int64_t* es_ev_offset;
+  const uint8_t* es_has_pulse;
+  const double* es_pulse_mat;
+  const int32_t* es_acq;
+  const double* ev_dt;
+  const double* ev_dmom;
+  const uint8_t* ev_sample;
+  const int32_t* ev_snap;
+  int32_t n_acq, max_samples, n_snap;
+};
+
+struct Program {
+  std::vector<DevOp> ops;
+  std::vector<GEv> gev;
+  std::vector<int64_t> sample_g;  // compact sample -> acq * max_samples + index
+  int32_t n_acq = 0, max_samples = 0, n_snap = 0;
+  int64_t n_events = 0;  // reference table size incl. pulses
+  int64_t n_samples = 0;
+  int64_t n_rot = 0, n_interval = 0, n_window_ops = 0, n_window_samples = 0, n_gsamp_events = 0;
+};
+
+// Throws std::invalid_argument on malformed tables.
+void compile_program(const TablesView& t, Program& prog);
+
+}  // namespace bloch

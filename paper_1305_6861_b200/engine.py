@@ -1,0 +1,570 @@
+"""Host layer of the Bloch engine — the reference's ``mrsim.engine`` API over the GPU.
+
+The seam is the reference's own: ``compute_block(tables, block)``
+(engine.py:259-310) with identical argument meaning and return types, fed by
+``precompute_sequence_tables`` (engine.py:83-164) and ``build_spin_arrays``
+(engine.py:192-226) and folded by ``run`` (engine.py:465-537).  The per-event
+arithmetic runs in ``libbloch_b200.so`` (sm_100a) through the C-ABI in
+``include/bloch_b200.h``; there is no CPU fallback — without the library or a
+device every compute call raises.
+
+Because the function is a drop-in, the reference package itself can be driven
+by the GPU: ``mrsim.engine.compute_block = paper_1305_6861_b200.compute_block``
+ — ``compute_block`` accepts the reference's own
+``OperatorTables`` / ``SpinBlock`` objects (duck-typed) as well as the mirror
+classes defined here.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import platform
+import time
+import weakref
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Tuple
+
+import numpy as np
+
+from . import _capi
+from .bloch import GAMMA_PROTON, hard_pulse_matrix
+from .errors import InvalidParameter
+from .phantom import DEFAULT_SPIN_CAP, Phantom, rasterize_arrays
+from .sequence import Sequence
+from .system import SystemModel, default_system, receive_weights, spin_off_resonance
+
+# ---------------------------------------------------------------------------
+# event tables (master side) — engine.py:51-164
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class EsTable:
+    """Operator data of one elementary sequence (engine.py:51-70)."""
+
+    pulse_mat: Optional[np.ndarray]
+    duration: float
+    moments: np.ndarray
+    ev_dt: np.ndarray
+    ev_dmom: np.ndarray
+    ev_sample: np.ndarray
+    ev_snap: np.ndarray
+    acq: int = -1
+    n_samples: int = 0
+
+
+@dataclass(eq=False)
+class OperatorTables:
+    entries: List[EsTable]
+    n_acq: int
+    acq_times: List[np.ndarray]
+    snapshot_times: Tuple[float, ...]
+    pulse_memo_hits: int
+    gamma: float
+
+
+def precompute_sequence_tables(
+    sequence: Sequence, gamma: float = GAMMA_PROTON, snapshot_times=(), memoize: bool = True
+) -> OperatorTables:
+    """Per-ES operator tables, event for event those of engine.py:83-164.
+
+    Events partition each ES at its ADC and snapshot instants (a snapshot sorts
+    before a sample at the same instant, engine.py:119); event i carries the
+    interval ``ev_dt[i]`` and moment increment ``ev_dmom[i]`` leading up to it;
+    a tail event closes the ES when the last instant misses the end or the
+    accumulated moment differs from the total in any bit (engine.py:135-140).
+    The increments are formed with ``np.diff`` — the same subtractions as the
+    reference loop, so the tables are bit-identical.
+    """
+    snapshot_times = tuple(sorted(snapshot_times))
+    entries: List[EsTable] = []
+    acq_times: List[np.ndarray] = []
+    memo: Dict[Tuple[float, float], np.ndarray] = {}
+    hits = 0
+    t0 = 0.0
+    acq = 0
+    zero3 = np.zeros((1, 3))
+    for es in sequence.elements:
+        mat = None
+        if es.pulse is not None and es.pulse.alpha != 0.0:
+            key = (es.pulse.alpha, es.pulse.phi)
+            if memoize and key in memo:
+                mat = memo[key]
+                hits += 1
+            else:
+                mat = hard_pulse_matrix(es.pulse.alpha, es.pulse.phi)
+                if memoize:
+                    memo[key] = mat
+        t1 = t0 + es.duration
+        s_ts = es.acquisition.sample_times(es.duration)
+        snaps = [
+            (float(t_abs - t0), si)
+            for si, t_abs in enumerate(snapshot_times)
+            if t0 < t_abs <= t1 or (t_abs == 0.0 == t0)
+        ]
+        if not snaps and s_ts.size == 0:  # no instants: the tail event alone (engine.py:135-140)
+            total = es.gradient.moments(es.duration, gamma)
+            if 0.0 < es.duration or np.any(total != 0.0):
+                ev_dt, ev_dmom = np.array([es.duration - 0.0]), (total - np.zeros(3)).reshape(1, 3)
+            else:
+                ev_dt, ev_dmom = np.zeros(0), np.zeros((0, 3))
+            entries.append(EsTable(pulse_mat=mat, duration=es.duration, moments=np.asarray(total, dtype=float),
+                                   ev_dt=ev_dt, ev_dmom=ev_dmom, ev_sample=np.zeros(ev_dt.size, dtype=bool),
+                                   ev_snap=np.full(ev_dt.size, -1, dtype=int)))
+            t0 = t1
+            continue
+        if snaps:
+            events = [(float(t), True, -1) for t in s_ts] + [(t, False, si) for t, si in snaps]
+            events.sort(key=lambda e: (e[0], e[1]))
+            ts = np.array([e[0] for e in events])
+            is_sample = np.array([e[1] for e in events], dtype=bool)
+            snap_idx = np.array([e[2] for e in events], dtype=int)
+        else:
+            ts = np.asarray(s_ts, dtype=float)
+            is_sample = np.ones(ts.size, dtype=bool)
+            snap_idx = np.full(ts.size, -1, dtype=int)
+        partial = es.gradient.partial_moments(ts, es.duration, gamma) if ts.size else np.zeros((0, 3))
+        total = es.gradient.moments(es.duration, gamma)
+        ev_dt = np.diff(ts, prepend=0.0)
+        ev_dmom = np.diff(partial, axis=0, prepend=zero3) if ts.size else np.zeros((0, 3))
+        prev_t = float(ts[-1]) if ts.size else 0.0
+        prev_m = partial[-1] if ts.size else np.zeros(3)
+        if prev_t < es.duration or np.any(prev_m != total):
+            ev_dt = np.append(ev_dt, es.duration - prev_t)
+            ev_dmom = np.vstack([ev_dmom, (total - prev_m)[None, :]])
+            is_sample = np.append(is_sample, False)
+            snap_idx = np.append(snap_idx, -1)
+        entry = EsTable(
+            pulse_mat=mat,
+            duration=es.duration,
+            moments=np.asarray(total, dtype=float),
+            ev_dt=np.asarray(ev_dt, dtype=float),
+            ev_dmom=np.asarray(ev_dmom, dtype=float).reshape(-1, 3),
+            ev_sample=np.asarray(is_sample, dtype=bool),
+            ev_snap=np.asarray(snap_idx, dtype=int),
+        )
+        if es.acquisition.enabled:
+            entry.acq = acq
+            entry.n_samples = es.acquisition.n_samples
+            acq_times.append(t0 + s_ts)
+            acq += 1
+        entries.append(entry)
+        t0 = t1
+    return OperatorTables(
+        entries=entries, n_acq=acq, acq_times=acq_times, snapshot_times=snapshot_times,
+        pulse_memo_hits=hits, gamma=gamma,
+    )
+
+
+def flatten_tables(tables) -> Dict[str, np.ndarray]:
+    """Flatten OperatorTables (product or reference object) into the C-ABI arrays."""
+    entries = tables.entries
+    n_es = len(entries)
+    counts = np.fromiter((e.ev_dt.size for e in entries), dtype=np.int64, count=n_es)
+    offset = np.zeros(n_es + 1, dtype=np.int64)
+    np.cumsum(counts, out=offset[1:])
+    has_pulse = np.fromiter((e.pulse_mat is not None for e in entries), dtype=np.uint8, count=n_es)
+    mats = np.zeros((n_es, 9))
+    for i, e in enumerate(entries):
+        if e.pulse_mat is not None:
+            mats[i] = np.asarray(e.pulse_mat, dtype=float).reshape(9)
+    acq = np.fromiter((e.acq for e in entries), dtype=np.int32, count=n_es)
+    E = int(offset[-1])
+    if E:
+        ev_dt = np.ascontiguousarray(np.concatenate([e.ev_dt for e in entries]), dtype=np.float64)
+        ev_dmom = np.ascontiguousarray(
+            np.concatenate([np.asarray(e.ev_dmom, dtype=float).reshape(-1, 3) for e in entries]), dtype=np.float64
+        )
+        ev_sample = np.ascontiguousarray(np.concatenate([e.ev_sample for e in entries]), dtype=np.uint8)
+        ev_snap = np.ascontiguousarray(np.concatenate([e.ev_snap for e in entries]), dtype=np.int32)
+    else:
+        ev_dt, ev_dmom = np.zeros(0), np.zeros((0, 3))
+        ev_sample, ev_snap = np.zeros(0, np.uint8), np.zeros(0, np.int32)
+    max_ns = max((e.n_samples for e in entries), default=0)
+    return dict(
+        n_es=n_es, offset=offset, has_pulse=has_pulse, mats=np.ascontiguousarray(mats), acq=acq,
+        ev_dt=ev_dt, ev_dmom=ev_dmom, ev_sample=ev_sample, ev_snap=ev_snap,
+        n_acq=int(tables.n_acq), max_ns=int(max_ns), n_snap=len(tables.snapshot_times),
+    )
+
+
+# ---------------------------------------------------------------------------
+# spin blocks — engine.py:172-251
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class SpinBlock:
+    """Contiguous slice of the spin set (engine.py:172-189).
+
+    ``weight`` is complex (n,) — or (C, n) for C receive coils (extension)."""
+
+    index: int
+    pos: np.ndarray
+    mx: np.ndarray
+    my: np.ndarray
+    mz: np.ndarray
+    t1: np.ndarray
+    t2: np.ndarray
+    m0: np.ndarray
+    domega: np.ndarray
+    weight: np.ndarray
+
+    @property
+    def n(self) -> int:
+        return self.mx.size
+
+
+def build_spin_arrays(spins, system: SystemModel) -> SpinBlock:
+    """Pack spins into SoA arrays, folding in off-resonance and receive weight (engine.py:192-226).
+
+    ``spins`` is the dict returned by :func:`~.phantom.rasterize_arrays` or a
+    list of ``SpinSample`` (the reference's form).
+    """
+    if isinstance(spins, dict):
+        pos = np.asarray(spins["pos"], dtype=float).reshape(-1, 3)
+        m0 = np.asarray(spins["m0"], dtype=float)
+        t1 = np.asarray(spins["t1"], dtype=float)
+        t2 = np.asarray(spins["t2"], dtype=float)
+        obj_dw = np.asarray(spins["delta_omega"], dtype=float)
+        mx, my, mz = np.zeros_like(m0), np.zeros_like(m0), m0.copy()
+    else:
+        n = len(spins)
+        pos = np.array([s.position for s in spins], dtype=float).reshape(n, 3)
+        m0 = np.array([s.relax.m0 for s in spins], dtype=float)
+        t1 = np.array([s.relax.t1 for s in spins], dtype=float)
+        t2 = np.array([s.relax.t2 for s in spins], dtype=float)
+        obj_dw = np.array([s.delta_omega for s in spins], dtype=float)
+        mx = np.array([s.m.mx for s in spins], dtype=float)
+        my = np.array([s.m.my for s in spins], dtype=float)
+        mz = np.array([s.m.mz for s in spins], dtype=float)
+    return SpinBlock(
+        index=0, pos=pos, mx=mx, my=my, mz=mz, t1=t1, t2=t2, m0=m0,
+        domega=spin_off_resonance(system, pos, obj_dw), weight=receive_weights(system, pos),
+    )
+
+
+def partition_blocks(arrays: SpinBlock, n_blocks: int) -> List[SpinBlock]:
+    """At most n_blocks contiguous disjoint blocks, np.linspace bounds (engine.py:229-251)."""
+    n = arrays.n
+    n_blocks = max(1, min(n_blocks, n)) if n else 1
+    bounds = np.linspace(0, n, n_blocks + 1).astype(int)
+    w = np.asarray(arrays.weight)
+    out = []
+    for b in range(n_blocks):
+        lo, hi = bounds[b], bounds[b + 1]
+        out.append(
+            SpinBlock(
+                index=b, pos=arrays.pos[lo:hi].copy(), mx=arrays.mx[lo:hi].copy(), my=arrays.my[lo:hi].copy(),
+                mz=arrays.mz[lo:hi].copy(), t1=arrays.t1[lo:hi].copy(), t2=arrays.t2[lo:hi].copy(),
+                m0=arrays.m0[lo:hi].copy(), domega=arrays.domega[lo:hi].copy(),
+                weight=(w[..., lo:hi].copy()),
+            )
+        )
+    return out
+
+
+# ---------------------------------------------------------------------------
+# the device engine (C-ABI context)
+# ---------------------------------------------------------------------------
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class BlochEngine:
+    """One libbloch_b200 context: a CUDA device, a state precision, the uploaded tables."""
+
+    def __init__(self, device: int = 0, precision: int = 32):
+        lib = _capi.load()
+        self._lib = lib
+        self.device = int(device)
+        self.precision = int(precision)
+        h = ctypes.c_void_p()
+        _capi.check(lib.bloch_create(self.device, self.precision, ctypes.byref(h)), "bloch_create")
+        self._h = h
+        self._tables_ref = None
+        self._flat = None
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.bloch_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- tables --------------------------------------------------------------
+    def set_tables(self, tables) -> Dict[str, np.ndarray]:
+        if self._tables_ref is not None and self._tables_ref() is tables:
+            return self._flat
+        f = flatten_tables(tables)
+        i32 = ctypes.POINTER(ctypes.c_int32)
+        u8 = ctypes.POINTER(ctypes.c_uint8)
+        _capi.check(
+            self._lib.bloch_set_tables(
+                self._h, f["n_es"], f["offset"].ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                f["has_pulse"].ctypes.data_as(u8), _capi.dptr(f["mats"]), f["acq"].ctypes.data_as(i32),
+                _capi.dptr(f["ev_dt"]), _capi.dptr(f["ev_dmom"]), f["ev_sample"].ctypes.data_as(u8),
+                f["ev_snap"].ctypes.data_as(i32), f["n_acq"], f["max_ns"], f["n_snap"],
+            ),
+            "bloch_set_tables",
+        )
+        try:
+            self._tables_ref = weakref.ref(tables)
+        except TypeError:
+            self._tables_ref = None
+        self._flat = f
+        return f
+
+    def program_stats(self) -> Dict[str, int]:
+        vals = [ctypes.c_int64() for _ in range(6)]
+        _capi.check(self._lib.bloch_program_stats(self._h, *[ctypes.byref(v) for v in vals]), "bloch_program_stats")
+        keys = ("events", "samples", "rot", "interval", "window_ops", "window_samples")
+        return {k: v.value for k, v in zip(keys, vals)}
+
+    def last_timing(self) -> Dict[str, float]:
+        k, d, n = ctypes.c_float(), ctypes.c_float(), ctypes.c_int32()
+        _capi.check(self._lib.bloch_last_timing(self._h, ctypes.byref(k), ctypes.byref(d), ctypes.byref(n)), "timing")
+        return {"kernel_ms": k.value, "device_ms": d.value, "launches": n.value}
+
+    # -- compute -------------------------------------------------------------
+    def compute(self, tables, pos, mx, my, mz, t1, t2, m0, domega, weight, block_index=0):
+        """compute_block on host numpy arrays; returns (echoes, snapshots)."""
+        f = self.set_tables(tables)
+        n = int(np.asarray(mx).size)
+        pos = _f64(np.asarray(pos, dtype=float).reshape(n, 3))
+        arrs = [_f64(a) for a in (mx, my, mz, t1, t2, m0, domega)]
+        w = np.asarray(weight)
+        multi = w.ndim == 2
+        n_coils = w.shape[0] if multi else 1
+        if w.shape[-1] != n:
+            raise InvalidParameter(f"weight has {w.shape[-1]} spins, block has {n}")
+        wc = np.ascontiguousarray(w, dtype=np.complex128).reshape(n_coils, n)
+        echoes = np.zeros((n_coils, f["n_acq"], f["max_ns"]), dtype=np.complex128)
+        n_snap = f["n_snap"]
+        snaps = np.zeros((n_snap, n, 3)) if n_snap else None
+        present = np.zeros(max(n_snap, 1), dtype=np.uint8)
+        st = self._lib.bloch_compute_block(
+            self._h, n, _capi.dptr(pos), *[_capi.dptr(a) for a in arrs],
+            _capi.dptr(wc.view(np.float64)), n_coils, _capi.dptr(echoes.view(np.float64)),
+            _capi.dptr(snaps) if snaps is not None else None,
+            present.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), 0,
+        )
+        _capi.check(st, "bloch_compute_block", block_index)
+        snap_list = [snaps[i] if present[i] else None for i in range(n_snap)]
+        return (echoes if multi else echoes[0]), snap_list
+
+
+_ENGINES: Dict[Tuple[int, int], BlochEngine] = {}
+
+
+def default_device() -> int:
+    return int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def get_engine(device: Optional[int] = None, precision: Optional[int] = None) -> BlochEngine:
+    """Process-wide engine per (device, precision); precision from BLOCH_PRECISION (32)."""
+    dev = default_device() if device is None else int(device)
+    prec = int(os.environ.get("BLOCH_PRECISION", "32")) if precision is None else int(precision)
+    key = (dev, prec)
+    eng = _ENGINES.get(key)
+    if eng is None:
+        eng = BlochEngine(dev, prec)
+        _ENGINES[key] = eng
+    return eng
+
+
+# ---------------------------------------------------------------------------
+# the kernel seam — engine.py:259-335
+# ---------------------------------------------------------------------------
+
+
+def compute_block(tables, block, *, device: Optional[int] = None, precision: Optional[int] = None):
+    """Evolve one block through the whole sequence on the GPU (engine.py:259-310).
+
+    Returns ``(echo_partials, snapshots)``: complex128 (n_acq, max_ns) — or
+    (C, n_acq, max_ns) for a (C, n) weight — of receive-weighted transverse
+    sums over the block, and one (n, 3) array (or None) per snapshot time.
+    The block is not mutated.
+    """
+    eng = get_engine(device, precision)
+    return eng.compute(
+        tables, block.pos, block.mx, block.my, block.mz, block.t1, block.t2, block.m0, block.domega,
+        block.weight, block_index=getattr(block, "index", 0),
+    )
+
+
+def simulate_spin(spin, tables, domega: float = 0.0, weight: complex = 1.0 + 0.0j, **kw):
+    """Single-spin wrapper (engine.py:313-335)."""
+    block = SpinBlock(
+        index=0, pos=np.array([spin.position], dtype=float), mx=np.array([spin.m.mx]),
+        my=np.array([spin.m.my]), mz=np.array([spin.m.mz]), t1=np.array([spin.relax.t1]),
+        t2=np.array([spin.relax.t2]), m0=np.array([spin.relax.m0]), domega=np.array([float(domega)]),
+        weight=np.array([complex(weight)]),
+    )
+    return compute_block(tables, block, **kw)
+
+
+# ---------------------------------------------------------------------------
+# run orchestration — engine.py:343-537
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class EchoRecord:
+    acq_index: int
+    values: np.ndarray
+    timestamps: np.ndarray
+
+
+@dataclass
+class RunMetrics:
+    wall_time_s: float
+    spin_count: int
+    throughput: float  # spins per second of wall time
+    workers: int
+    blocks: int
+    busy_fraction: Dict[int, float]
+    hardware: str
+    kernel_ms: float = 0.0
+    events_per_spin: int = 0
+
+
+@dataclass
+class RunResult:
+    echoes: List[EchoRecord]
+    metrics: RunMetrics
+    snapshots: List[Tuple[float, np.ndarray]]
+    spin_count: int
+    spacing: Tuple[float, float, float]
+    spacing_report: Optional[object] = None
+
+    def echo_matrix(self) -> np.ndarray:
+        return np.array([rec.values for rec in self.echoes])
+
+
+@dataclass
+class Experiment:
+    sequence: Sequence
+    phantom: Phantom
+    system: SystemModel = field(default_factory=default_system)
+    spacing: Optional[Tuple[float, float, float]] = None
+    workers: int = 1  # accepted for API parity; one host process drives the device
+    deterministic: bool = True  # the device fold is always in a fixed order
+    blocks: Optional[int] = None
+    snapshot_times: Tuple[float, ...] = ()
+    spin_cap: int = DEFAULT_SPIN_CAP
+    precision: int = 32
+    device: Optional[int] = None
+
+
+def run(exp: Experiment) -> RunResult:
+    """Execute one experiment on the GPU (engine.py:465-537).
+
+    Differences from the reference, all outside the hot path: ``spacing`` must
+    be given (the spin-spacing analysis of mrsim.discretize is out of scope,
+    SURVEY §2), and the spin set runs as one device block — the device result
+    does not depend on the block partition (fixed per-CTA tiling, ordered fold).
+    """
+    if exp.workers < 1:
+        raise InvalidParameter(f"workers must be >= 1, got {exp.workers}")
+    if exp.spacing is None:
+        raise InvalidParameter(
+            "Experiment.spacing is required: the spacing analysis (mrsim.discretize) is out of "
+            "scope for the GPU engine"
+        )
+    wall_start = time.perf_counter()
+    spacing = tuple(float(s) for s in exp.spacing)
+    spins = rasterize_arrays(exp.phantom, spacing, cap=exp.spin_cap)
+    if spins["m0"].size == 0:
+        raise InvalidParameter("the phantom rasterized to zero spins")
+    arrays = build_spin_arrays(spins, exp.system)
+    tables = precompute_sequence_tables(exp.sequence, gamma=exp.system.gamma, snapshot_times=exp.snapshot_times)
+    eng = get_engine(exp.device, exp.precision)
+    t_k = time.perf_counter()
+    echo_sum, snaps = eng.compute(
+        tables, arrays.pos, arrays.mx, arrays.my, arrays.mz, arrays.t1, arrays.t2, arrays.m0, arrays.domega,
+        arrays.weight,
+    )
+    busy = time.perf_counter() - t_k
+    n_spins = arrays.n
+    records = []
+    if tables.n_acq:
+        echo_sum = echo_sum / n_spins  # engine.py:507
+        for i in range(tables.n_acq):
+            records.append(
+                EchoRecord(acq_index=i, values=echo_sum[..., i, : tables.acq_times[i].size],
+                           timestamps=tables.acq_times[i])
+            )
+    wall = time.perf_counter() - wall_start
+    timing = eng.last_timing()
+    metrics = RunMetrics(
+        wall_time_s=wall, spin_count=n_spins, throughput=n_spins / wall if wall > 0 else math.inf,
+        workers=1, blocks=1, busy_fraction={0: busy / wall} if wall > 0 else {},
+        hardware=f"{platform.machine()} cuda:{eng.device} sm_100a", kernel_ms=timing["kernel_ms"],
+        events_per_spin=eng.program_stats()["events"],
+    )
+    snapshots = [
+        (t, snaps[i] if snaps[i] is not None else np.zeros((0, 3))) for i, t in enumerate(tables.snapshot_times)
+    ]
+    return RunResult(echoes=records, metrics=metrics, snapshots=snapshots, spin_count=n_spins, spacing=spacing)
+
+
+# ---------------------------------------------------------------------------
+# result comparison — engine.py:603-656
+# ---------------------------------------------------------------------------
+
+
+def delta_e_stoer(ref, test) -> float:
+    """10*log10(sum|ref-test|^2 / sum|ref|^2); -inf when identical (engine.py:603-616)."""
+    ref = np.asarray(ref).ravel()
+    test = np.asarray(test).ravel()
+    if ref.shape != test.shape:
+        raise InvalidParameter(f"shape mismatch: {ref.shape} vs {test.shape}")
+    num = float(np.sum(np.abs(ref - test) ** 2))
+    den = float(np.sum(np.abs(ref) ** 2))
+    if den == 0.0:
+        return -math.inf if num == 0.0 else math.inf
+    if num == 0.0:
+        return -math.inf
+    return 10.0 * math.log10(num / den)
+
+
+@dataclass(frozen=True)
+class ComparisonResult:
+    delta_e_db: float
+    exceedances: int
+    compared: int
+    rel_threshold: float
+
+
+def compare_results(ref, test, rel_threshold: float = 1e-6) -> ComparisonResult:
+    """ΔE_stör plus per-component relative exceedances, eps-scale pairs unrated (engine.py:627-656)."""
+    ref = np.asarray(ref)
+    test = np.asarray(test)
+    if ref.shape != test.shape:
+        raise InvalidParameter(f"shape mismatch: {ref.shape} vs {test.shape}")
+    if np.iscomplexobj(ref) or np.iscomplexobj(test):
+        ref = np.concatenate([np.real(ref).ravel(), np.imag(ref).ravel()])
+        test = np.concatenate([np.real(test).ravel(), np.imag(test).ravel()])
+    else:
+        ref = ref.ravel().astype(float)
+        test = test.ravel().astype(float)
+    scale = float(np.max(np.abs(ref))) if ref.size else 0.0
+    eps_scale = np.finfo(float).eps * max(scale, 1e-300)
+    rated = ~((np.abs(ref) < eps_scale) & (np.abs(test) < eps_scale))
+    rel = np.zeros_like(ref)
+    denom = np.abs(ref[rated])
+    denom = np.where(denom > 0.0, denom, eps_scale)
+    rel[rated] = np.abs(ref[rated] - test[rated]) / denom
+    return ComparisonResult(
+        delta_e_db=delta_e_stoer(ref, test), exceedances=int(np.sum(rel > rel_threshold)),
+        compared=int(np.sum(rated)), rel_threshold=rel_threshold,
+    )

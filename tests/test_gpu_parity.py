@@ -1,0 +1,162 @@
+"""GPU parity: libbloch_b200 through the C-ABI vs the reference's own outputs.
+
+Every case replays a golden record produced by the reference itself
+(tests/golden/make_golden.py): the same spin arrays and the same sequence go
+through ``paper_1305_6861_b200.compute_block`` (ctypes -> bloch_compute_block
+-> sm_100a kernels) and the echoes / snapshots are compared with the
+BASELINE.json tolerances:
+
+* fp32 state (default engine): k-space rel L2 <= 1e-4, final magnetisation
+  rel L2 <= 1e-5;
+* fp64 state engine: rel L2 <= 1e-11 (the reference unit tests' regime).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import cases
+from conftest import load_golden
+from oracle.bloch_oracle import rel_l2
+from paper_1305_6861_b200 import SpinBlock, compute_block, precompute_sequence_tables
+
+pytestmark = pytest.mark.gpu
+
+SMALL = ["fid", "pair", "se16_box", "tse16", "epi16", "cpmg8", "mixed", "mixed_coils"]
+CONFIGS = ["cfg0", "cfg1", "cfg2", "cfg3", "cfg4"]
+
+KSPACE_TOL = {32: 1e-4, 64: 1e-11}
+STATE_TOL = {32: 1e-5, 64: 1e-11}
+
+
+def _sequence_of(name):
+    if name.startswith("cfg"):
+        from paper_1305_6861_b200 import configs
+
+        return configs.make(int(name[3:])).sequence
+    return cases.small_cases()[name]["sequence"]
+
+
+_SEQ_CACHE = {}
+
+
+def _tables(name, rec):
+    if name not in _SEQ_CACHE:
+        _SEQ_CACHE[name] = precompute_sequence_tables(
+            _sequence_of(name), snapshot_times=tuple(rec["snapshot_times"].tolist())
+        )
+    return _SEQ_CACHE[name]
+
+
+def _block(rec):
+    return SpinBlock(index=0, pos=rec["spin_pos"], mx=rec["spin_mx"], my=rec["spin_my"], mz=rec["spin_mz"],
+                     t1=rec["spin_t1"], t2=rec["spin_t2"], m0=rec["spin_m0"], domega=rec["spin_domega"],
+                     weight=rec["spin_weight"])
+
+
+def echo_error(rec, echoes):
+    """rel L2 of the GPU echoes vs the golden (full array, or head/tail + per-acq checksums)."""
+    if "echo_full" in rec:
+        return rel_l2(rec["echo_full"], echoes)
+    shape = tuple(rec["echo_shape"])
+    ek = np.asarray(echoes).reshape((-1,) + shape[-2:])
+    errs = [rel_l2(rec["echo_head"], ek[:, :4]), rel_l2(rec["echo_tail"], ek[:, -4:]),
+            rel_l2(rec["echo_sum"], ek.sum(axis=-1))]
+    return max(errs)
+
+
+def snapshot_errors(rec, snaps):
+    out = []
+    for i in range(int(rec["n_snap"])):
+        present = bool(rec[f"snap_{i}_present"])
+        assert (snaps[i] is not None) == present, f"snapshot {i} presence"
+        if present:
+            out.append(rel_l2(rec[f"snap_{i}"], snaps[i]))
+    return out
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+@pytest.mark.parametrize("name", SMALL + CONFIGS)
+def test_gpu_matches_reference_golden(name, precision):
+    rec = load_golden(name)
+    tables = _tables(name, rec)
+    echoes, snaps = compute_block(tables, _block(rec), precision=precision)
+    assert echoes.shape == tuple(rec["echo_shape"])
+    err = echo_error(rec, echoes)
+    assert err <= KSPACE_TOL[precision], f"{name} fp{precision} k-space rel L2 {err:.3e}"
+    for i, e in enumerate(snapshot_errors(rec, snaps)):
+        assert e <= STATE_TOL[precision], f"{name} fp{precision} snapshot {i} rel L2 {e:.3e}"
+
+
+# --- reference engine tests restated against the GPU path (tests/test_engine.py) ---
+
+
+def test_fid_amplitude():  # test_engine.py:115-122
+    rec = load_golden("fid")
+    echoes, _ = compute_block(_tables("fid", rec), _block(rec), precision=64)
+    assert abs(echoes[0, 0]) == pytest.approx(0.5 * math.exp(-0.05 / 0.2), rel=1e-12)
+    echoes32, _ = compute_block(_tables("fid", rec), _block(rec), precision=32)
+    assert abs(echoes32[0, 0]) == pytest.approx(0.5 * math.exp(-0.05 / 0.2), rel=1e-6)
+
+
+def test_zero_m0_contributes_nothing():  # test_engine.py:125-131
+    rec = load_golden("fid")
+    blk = _block(rec)
+    blk.mz = np.zeros(1)
+    blk.m0 = np.zeros(1)
+    for prec in (32, 64):
+        echoes, _ = compute_block(_tables("fid", rec), blk, precision=prec)
+        assert np.all(echoes == 0)
+
+
+def test_opposite_positions_sum_to_real_signal():  # test_engine.py:134-155
+    rec = load_golden("pair")
+    echoes, _ = compute_block(_tables("pair", rec), _block(rec), precision=64)
+    np.testing.assert_allclose(echoes.imag, 0.0, atol=1e-14)
+    assert np.max(np.abs(echoes.real)) > 0.1
+
+
+def test_empty_block():
+    rec = load_golden("tse16")
+    blk = _block(rec)
+    empty = SpinBlock(index=0, pos=np.zeros((0, 3)), mx=np.zeros(0), my=np.zeros(0), mz=np.zeros(0),
+                      t1=np.zeros(0), t2=np.zeros(0), m0=np.zeros(0), domega=np.zeros(0),
+                      weight=np.zeros(0, complex))
+    echoes, snaps = compute_block(_tables("tse16", rec), empty)
+    assert echoes.shape == tuple(rec["echo_shape"]) and np.all(echoes == 0)
+    assert all(s is None or s.shape == (0, 3) for s in snaps)
+    del blk
+
+
+def test_scaling_m0_by_two_is_exact():  # test_engine.py:203-206 (power-of-two scaling commutes with rounding)
+    rec = load_golden("se16_box")
+    t = _tables("se16_box", rec)
+    a, _ = compute_block(t, _block(rec))
+    blk = _block(rec)
+    blk.m0 = blk.m0 * 2.0
+    blk.mz = blk.mz * 2.0
+    b, _ = compute_block(t, blk)
+    assert np.array_equal(a * 2.0, b)
+
+
+def test_deterministic_repeat_bit_identical():  # test_engine.py:181-184
+    rec = load_golden("cfg1")
+    t = _tables("cfg1", rec)
+    a, sa = compute_block(t, _block(rec))
+    b, sb = compute_block(t, _block(rec))
+    assert np.array_equal(a, b) and np.array_equal(sa[0], sb[0])
+
+
+def test_block_partition_linearity():  # test_engine.py:175-179, 191-200
+    rec = load_golden("tse16")
+    t = _tables("tse16", rec)
+    full, _ = compute_block(t, _block(rec))
+    blk = _block(rec)
+    parts = []
+    for lo, hi in ((0, 77), (77, 300)):
+        sub = SpinBlock(index=0, pos=blk.pos[lo:hi], mx=blk.mx[lo:hi], my=blk.my[lo:hi], mz=blk.mz[lo:hi],
+                        t1=blk.t1[lo:hi], t2=blk.t2[lo:hi], m0=blk.m0[lo:hi], domega=blk.domega[lo:hi],
+                        weight=blk.weight[lo:hi])
+        parts.append(compute_block(t, sub)[0])
+    assert rel_l2(full, parts[0] + parts[1]) <= 1e-6
