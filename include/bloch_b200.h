@@ -92,10 +92,14 @@ int bloch_set_tables(bloch_ctx* ctx, int32_t n_es, const int64_t* es_ev_offset,
                      int32_t max_samples, int32_t n_snap);
 
 /* Statistics of the compiled program: events E (reference table size incl.
- * pulses), ADC samples, and op counts of each kind. */
+ * pulses), ADC samples, pulses, generic intervals (evaluated one by one),
+ * uniform ADC windows and the samples they cover, samples covered by
+ * linear-increment (chirp) runs, and pulse+interval pairs folded into RF
+ * trains.  Any pointer may be NULL. */
 int bloch_program_stats(const bloch_ctx* ctx, int64_t* n_events, int64_t* n_samples,
                         int64_t* n_rot, int64_t* n_interval, int64_t* n_window_ops,
-                        int64_t* n_window_samples);
+                        int64_t* n_window_samples, int64_t* n_chirp_samples,
+                        int64_t* n_train_pairs);
 
 /*
  * Evolve one spin block through the uploaded tables — compute_block.

@@ -42,7 +42,7 @@ SIGNATURES = {
     "bloch_program_stats": (
         c_int,
         [c_void_p, POINTER(c_int64), POINTER(c_int64), POINTER(c_int64), POINTER(c_int64),
-         POINTER(c_int64), POINTER(c_int64)],
+         POINTER(c_int64), POINTER(c_int64), POINTER(c_int64), POINTER(c_int64)],
     ),
     "bloch_compute_block": (
         c_int,

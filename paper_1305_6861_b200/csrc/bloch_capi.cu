@@ -77,7 +77,7 @@ struct bloch_ctx {
   bloch::Program prog;
   bool has_prog = false;
   std::vector<uint8_t> snap_present;
-  DevBuf d_ops, d_gev, d_sample_g;
+  DevBuf d_ops, d_gev, d_mats, d_sample_g;
   DevBuf in_pos, in_mx, in_my, in_mz, in_t1, in_t2, in_m0, in_dw, in_w;
   DevBuf x, y, z, r1, r2, wpad;
   DevBuf partial, echo, snaps;
@@ -95,14 +95,14 @@ struct Variant {
 Variant pick_variant(int prec, int64_t n, int ncp, int n_sm) {
   if (prec == BLOCH_PREC_F32) {
     switch (ncp) {
-      case 1: return {32, n >= int64_t(n_sm) * 8 * 64 ? 8 : 1, 1};
+      case 1: return {32, n >= int64_t(n_sm) * 4 * 64 ? 4 : 1, 1};
       case 2: return {32, 4, 2};
       case 4: return {32, 4, 4};
       default: return {32, 2, 8};
     }
   }
   switch (ncp) {
-    case 1: return {64, n >= int64_t(n_sm) * 4 * 64 ? 4 : 1, 1};
+    case 1: return {64, n >= int64_t(n_sm) * 2 * 64 ? 2 : 1, 1};
     case 2: return {64, 2, 2};
     case 4: return {64, 2, 4};
     default: return {64, 1, 8};
@@ -207,7 +207,7 @@ int bloch_destroy(bloch_ctx* c) {
   }
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  for (DevBuf* b : {&c->d_ops, &c->d_gev, &c->d_sample_g, &c->in_pos, &c->in_mx, &c->in_my, &c->in_mz,
+  for (DevBuf* b : {&c->d_ops, &c->d_gev, &c->d_mats, &c->d_sample_g, &c->in_pos, &c->in_mx, &c->in_my, &c->in_mz,
                     &c->in_t1, &c->in_t2, &c->in_m0, &c->in_dw, &c->in_w, &c->x, &c->y, &c->z, &c->r1,
                     &c->r2, &c->wpad, &c->partial, &c->echo, &c->snaps})
     b->release();
@@ -257,6 +257,7 @@ int bloch_set_tables(bloch_ctx* c, int32_t n_es, const int64_t* es_ev_offset,
       ck(cudaSetDevice(c->device), "cudaSetDevice");
       upload(c->d_ops, prog.ops.data(), prog.ops.size() * sizeof(bloch::DevOp), c->stream);
       upload(c->d_gev, prog.gev.data(), prog.gev.size() * sizeof(bloch::GEv), c->stream);
+      upload(c->d_mats, prog.mats.data(), prog.mats.size() * sizeof(double), c->stream);
       upload(c->d_sample_g, prog.sample_g.data(), prog.sample_g.size() * sizeof(int64_t), c->stream);
       ck(cudaStreamSynchronize(c->stream), "set_tables sync");
     }
@@ -276,15 +277,18 @@ int bloch_set_tables(bloch_ctx* c, int32_t n_es, const int64_t* es_ev_offset,
 }
 
 int bloch_program_stats(const bloch_ctx* c, int64_t* n_events, int64_t* n_samples, int64_t* n_rot,
-                        int64_t* n_interval, int64_t* n_window_ops, int64_t* n_window_samples) {
+                        int64_t* n_interval, int64_t* n_window_ops, int64_t* n_window_samples,
+                        int64_t* n_chirp_samples, int64_t* n_train_pairs) {
   if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
   if (!c->has_prog) return fail(BLOCH_E_STATE, "no tables uploaded");
   if (n_events) *n_events = c->prog.n_events;
   if (n_samples) *n_samples = c->prog.n_samples;
   if (n_rot) *n_rot = c->prog.n_rot;
-  if (n_interval) *n_interval = c->prog.n_interval + c->prog.n_gsamp_events;
+  if (n_interval) *n_interval = c->prog.n_interval + c->prog.n_gsamp_events;  // generic intervals
   if (n_window_ops) *n_window_ops = c->prog.n_window_ops;
   if (n_window_samples) *n_window_samples = c->prog.n_window_samples;
+  if (n_chirp_samples) *n_chirp_samples = c->prog.n_chirp_samples;
+  if (n_train_pairs) *n_train_pairs = c->prog.n_train_pairs;
   return BLOCH_OK;
 }
 
@@ -386,6 +390,7 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       kp.n_ops = static_cast<int32_t>(P.ops.size());
       kp.spins_per_cta = static_cast<int32_t>(spc);
       kp.gev = c->d_gev.as<bloch::GEv>();
+      kp.mats = c->d_mats.as<double>();
       kp.n = n;
       kp.x = c->x.as<double>();
       kp.y = c->y.as<double>();
@@ -444,6 +449,15 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
 
 int bloch_last_timing(const bloch_ctx* c, float* kernel_ms, float* device_ms, int32_t* launches) {
   if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
+  if (c->device != BLOCH_HOST_ONLY && c->ev[3]) {  // asynchronous calls: wait for the call's last event
+    cudaSetDevice(c->device);
+    if (cudaEventSynchronize(c->ev[3]) == cudaSuccess) {
+      float k = 0.f, d = 0.f;
+      if (cudaEventElapsedTime(&k, c->ev[1], c->ev[2]) == cudaSuccess) const_cast<bloch_ctx*>(c)->kernel_ms = k;
+      if (cudaEventElapsedTime(&d, c->ev[0], c->ev[3]) == cudaSuccess) const_cast<bloch_ctx*>(c)->device_ms = d;
+    }
+    cudaGetLastError();
+  }
   if (kernel_ms) *kernel_ms = c->kernel_ms;
   if (device_ms) *device_ms = c->device_ms;
   if (launches) *launches = c->launches;

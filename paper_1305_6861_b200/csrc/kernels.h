@@ -12,6 +12,7 @@ struct KParams {
   int32_t n_ops;
   int32_t spins_per_cta;  // S * blockDim.x
   const GEv* gev;
+  const double* mats;  // OP_RFTRAIN matrices, 9 per pair
   int64_t n;  // spins
   const double *x, *y, *z, *dw;  // positions (m), off-resonance (rad/s)
   const double *r1, *r2, *m0;    // 1/T1, 1/T2, equilibrium magnetisation
@@ -29,12 +30,12 @@ struct KernelTraits {
 
 // (real type, spins per thread, coils) instantiated in bloch_kernels.cu
 #define BLOCH_FOR_EACH_VARIANT(X) \
-  X(float, 8, 1)                  \
+  X(float, 4, 1)                  \
   X(float, 1, 1)                  \
   X(float, 4, 2)                  \
   X(float, 4, 4)                  \
   X(float, 2, 8)                  \
-  X(double, 4, 1)                 \
+  X(double, 2, 1)                 \
   X(double, 1, 1)                 \
   X(double, 2, 2)                 \
   X(double, 2, 4)                 \

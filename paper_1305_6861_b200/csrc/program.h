@@ -16,24 +16,36 @@
 //              by `count - lead` identical (dt, dmom) intervals each followed
 //              by a sample — the ES-level hoisting the reference's relax cache
 //              (engine.py:292-299) only does for the exponentials
+//   OP_CHIRP   `count` sampled intervals of equal dt whose moment increments
+//              grow linearly (dmom_k = dmom_0 + k*dd): trapezoid ramps under
+//              the ADC (sequence.py:106-116); the per-event rotation factors
+//              form a geometric progression
+//   OP_RFTRAIN `count` consecutive elementary sequences each made of a hard
+//              pulse (or none) and one identical interval: a discretised
+//              shaped pulse under a constant gradient (sequence.py:650-674);
+//              matrices in the side table at `aux`
+//
+// The per-spin state is fp64 in every precision mode; in the fp32 mode only
+// the ADC sample recurrence of OP_WINDOW runs in fp32.
 #pragma once
 #include <stdint.h>
 
 namespace bloch {
 
-enum OpKind : int32_t { OP_ROT = 1, OP_EVENT = 2, OP_GSAMP = 3, OP_WINDOW = 4 };
+enum OpKind : int32_t { OP_ROT = 1, OP_EVENT = 2, OP_GSAMP = 3, OP_WINDOW = 4, OP_CHIRP = 5, OP_RFTRAIN = 6 };
 
 // flags of an interval (OP_EVENT.count, GEv.flags)
 enum : int32_t { EV_MOVE = 1, EV_RELAX = 2 };
 
 struct alignas(16) DevOp {
   int32_t kind;
-  int32_t count;  // WINDOW: samples recorded; GSAMP: events (1..8); EVENT: EV_* flags
-  int32_t s0;     // WINDOW/GSAMP: compact index of the first recorded sample
-  int32_t aux;    // WINDOW: lead flag; GSAMP: first side-table entry; EVENT: snapshot or -1
-  double p[9];    // ROT: row-major fp64 matrix; EVENT/WINDOW: dt, dmx, dmy, dmz
-  float f[9];     // ROT: fp32 copy of the matrix
-  int32_t pad;
+  int32_t count;  // WINDOW/CHIRP: samples; GSAMP: events (1..8); RFTRAIN: pairs; EVENT: EV_* flags
+  int32_t s0;     // WINDOW/GSAMP/CHIRP: compact index of the first recorded sample
+  int32_t aux;    // WINDOW: lead flag; GSAMP: first GEv; RFTRAIN: first matrix; EVENT: snapshot or -1
+  double p[9];    // ROT: row-major matrix; EVENT/WINDOW/RFTRAIN: dt, dmx, dmy, dmz;
+                  // CHIRP: dt, dmom_0 (3), dd (3)
+  int32_t flags;  // RFTRAIN: EV_* flags of the shared interval
+  int32_t pad[9];
 };
 static_assert(sizeof(DevOp) == 128, "DevOp must be 128 bytes");
 
@@ -47,5 +59,7 @@ static_assert(sizeof(GEv) == 48, "GEv must be 48 bytes");
 constexpr int kChunkSlots = 8;   // ADC slots reduced per warp transpose (samples x coils)
 constexpr int kStripSlots = 64;  // slots buffered per warp in shared memory before a CTA flush
 constexpr int kMinWindow = 4;    // shortest uniform run compiled as OP_WINDOW
+constexpr int kMinChirp = 3;     // shortest linear-increment run compiled as OP_CHIRP
+constexpr int kMinTrain = 4;     // shortest pulse+interval run compiled as OP_RFTRAIN
 
 }  // namespace bloch

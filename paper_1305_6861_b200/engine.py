@@ -158,6 +158,25 @@ def precompute_sequence_tables(
     )
 
 
+def event_counts(tables) -> Dict[str, int]:
+    """Reference table size E and per-class counts.
+
+    E = #ES with a pulse matrix + #events; classes: rot, prec_relax (dt != 0),
+    prec (dt == 0, moment != 0), noop, adc (sampled events)."""
+    out = {"rot": 0, "prec_relax": 0, "prec": 0, "noop": 0, "adc": 0}
+    for e in tables.entries:
+        out["rot"] += int(e.pulse_mat is not None)
+        if e.ev_dt.size:
+            dt = np.asarray(e.ev_dt)
+            moving = np.any(np.asarray(e.ev_dmom) != 0.0, axis=1)
+            out["prec_relax"] += int(np.sum(dt != 0.0))
+            out["prec"] += int(np.sum((dt == 0.0) & moving))
+            out["noop"] += int(np.sum((dt == 0.0) & ~moving))
+            out["adc"] += int(np.sum(e.ev_sample))
+    out["events"] = out["rot"] + out["prec_relax"] + out["prec"] + out["noop"]
+    return out
+
+
 def flatten_tables(tables) -> Dict[str, np.ndarray]:
     """Flatten OperatorTables (product or reference object) into the C-ABI arrays."""
     entries = tables.entries
@@ -324,9 +343,10 @@ class BlochEngine:
         return f
 
     def program_stats(self) -> Dict[str, int]:
-        vals = [ctypes.c_int64() for _ in range(6)]
+        vals = [ctypes.c_int64() for _ in range(8)]
         _capi.check(self._lib.bloch_program_stats(self._h, *[ctypes.byref(v) for v in vals]), "bloch_program_stats")
-        keys = ("events", "samples", "rot", "interval", "window_ops", "window_samples")
+        keys = ("events", "samples", "rot", "interval", "window_ops", "window_samples", "chirp_samples",
+                "train_pairs")
         return {k: v.value for k, v in zip(keys, vals)}
 
     def last_timing(self) -> Dict[str, float]:
@@ -334,9 +354,39 @@ class BlochEngine:
         _capi.check(self._lib.bloch_last_timing(self._h, ctypes.byref(k), ctypes.byref(d), ctypes.byref(n)), "timing")
         return {"kernel_ms": k.value, "device_ms": d.value, "launches": n.value}
 
+    def set_stream(self, stream_ptr: int) -> None:
+        """Run on an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream); 0 = own stream."""
+        _capi.check(self._lib.bloch_set_stream(self._h, ctypes.c_void_p(int(stream_ptr) or None)), "bloch_set_stream")
+
     # -- compute -------------------------------------------------------------
-    def compute(self, tables, pos, mx, my, mz, t1, t2, m0, domega, weight, block_index=0):
-        """compute_block on host numpy arrays; returns (echoes, snapshots)."""
+    def compute_device(self, tables, spins: Dict[str, int], n: int, n_coils: int, out_echoes: int,
+                       out_snaps: int = 0, sync: bool = False) -> None:
+        """compute_block on device-resident float64 arrays (raw CUDA pointers).
+
+        ``spins`` maps pos/mx/my/mz/t1/t2/m0/domega/weight to device pointers
+        (weight 0 = uniform 1+0j); outputs are device pointers.  Asynchronous on
+        the engine's stream unless ``sync``.
+        """
+        f = self.set_tables(tables)
+        ptr = lambda key: ctypes.cast(ctypes.c_void_p(int(spins[key])), ctypes.POINTER(ctypes.c_double)) \
+            if spins.get(key) else None
+        flags = _capi.BLOCH_IN_DEVICE | _capi.BLOCH_OUT_DEVICE | (0 if sync else _capi.BLOCH_NO_SYNC)
+        st = self._lib.bloch_compute_block(
+            self._h, int(n), ptr("pos"), ptr("mx"), ptr("my"), ptr("mz"), ptr("t1"), ptr("t2"), ptr("m0"),
+            ptr("domega"), ptr("weight"), int(n_coils),
+            ctypes.cast(ctypes.c_void_p(int(out_echoes)), ctypes.POINTER(ctypes.c_double)) if out_echoes else None,
+            ctypes.cast(ctypes.c_void_p(int(out_snaps)), ctypes.POINTER(ctypes.c_double)) if out_snaps else None,
+            None, flags,
+        )
+        _capi.check(st, "bloch_compute_block")
+        del f
+
+    def compute(self, tables, pos, mx, my, mz, t1, t2, m0, domega, weight, block_index=0,
+                out_echoes: Optional[np.ndarray] = None, out_snaps: Optional[np.ndarray] = None):
+        """compute_block on host numpy arrays; returns (echoes, snapshots).
+
+        ``out_echoes`` (complex128 (C, n_acq, max_ns)) and ``out_snaps`` (float64
+        (n_snap, n, 3)) may be preallocated (e.g. pinned) buffers."""
         f = self.set_tables(tables)
         n = int(np.asarray(mx).size)
         pos = _f64(np.asarray(pos, dtype=float).reshape(n, 3))
@@ -347,9 +397,20 @@ class BlochEngine:
         if w.shape[-1] != n:
             raise InvalidParameter(f"weight has {w.shape[-1]} spins, block has {n}")
         wc = np.ascontiguousarray(w, dtype=np.complex128).reshape(n_coils, n)
-        echoes = np.zeros((n_coils, f["n_acq"], f["max_ns"]), dtype=np.complex128)
+        eshape = (n_coils, f["n_acq"], f["max_ns"])
+        if out_echoes is not None:
+            if out_echoes.shape != eshape or out_echoes.dtype != np.complex128 or not out_echoes.flags.c_contiguous:
+                raise InvalidParameter(f"out_echoes must be C-contiguous complex128 {eshape}")
+            echoes = out_echoes
+        else:
+            echoes = np.zeros(eshape, dtype=np.complex128)
         n_snap = f["n_snap"]
-        snaps = np.zeros((n_snap, n, 3)) if n_snap else None
+        if n_snap and out_snaps is not None:
+            if out_snaps.shape != (n_snap, n, 3) or out_snaps.dtype != np.float64:
+                raise InvalidParameter(f"out_snaps must be float64 {(n_snap, n, 3)}")
+            snaps = out_snaps
+        else:
+            snaps = np.zeros((n_snap, n, 3)) if n_snap else None
         present = np.zeros(max(n_snap, 1), dtype=np.uint8)
         st = self._lib.bloch_compute_block(
             self._h, n, _capi.dptr(pos), *[_capi.dptr(a) for a in arrs],

@@ -36,6 +36,12 @@ from paper_1305_6861_b200.engine import flatten_tables  # noqa: E402
 FULL_ACQ_LIMIT = 4096  # store every acquisition when the k-space has at most this many samples x coils
 
 
+def projection_vector(n):
+    """Seeded complex projection: a per-acquisition checksum without cancellation bias."""
+    rng = np.random.default_rng(12345)
+    return rng.normal(size=n) + 1j * rng.normal(size=n)
+
+
 def to_ref_sequence(seq, ref):
     els = []
     for es in seq.elements:
@@ -89,6 +95,7 @@ def run_case(name, case, ref, out_dir):
     n_acq = ek.shape[1]
     rec["echo_shape"] = np.array(echoes.shape)
     rec["echo_sum"] = ek.sum(axis=-1)
+    rec["echo_proj"] = ek @ projection_vector(ek.shape[-1])
     rec["echo_energy"] = (np.abs(ek) ** 2).sum(axis=-1)
     if ek.size <= FULL_ACQ_LIMIT * 4 or n_acq <= 8:
         rec["echo_full"] = echoes

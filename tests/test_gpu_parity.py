@@ -18,6 +18,7 @@ import pytest
 
 import cases
 from conftest import load_golden
+from make_golden import projection_vector
 from oracle.bloch_oracle import rel_l2
 from paper_1305_6861_b200 import SpinBlock, compute_block, precompute_sequence_tables
 
@@ -62,7 +63,7 @@ def echo_error(rec, echoes):
     shape = tuple(rec["echo_shape"])
     ek = np.asarray(echoes).reshape((-1,) + shape[-2:])
     errs = [rel_l2(rec["echo_head"], ek[:, :4]), rel_l2(rec["echo_tail"], ek[:, -4:]),
-            rel_l2(rec["echo_sum"], ek.sum(axis=-1))]
+            rel_l2(rec["echo_proj"], ek @ projection_vector(ek.shape[-1]))]
     return max(errs)
 
 
