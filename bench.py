@@ -210,7 +210,9 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    stream = torch.cuda.current_stream()
+    # one explicit stream shared by torch (flush, events, NCCL ordering) and the library
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
 
     t_setup = time.perf_counter()
     w = configs.make(args.config)

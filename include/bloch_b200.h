@@ -101,6 +101,12 @@ int bloch_program_stats(const bloch_ctx* ctx, int64_t* n_events, int64_t* n_samp
                         int64_t* n_window_samples, int64_t* n_chirp_samples,
                         int64_t* n_train_pairs);
 
+/* Layout of the compiled program: ops in the device stream, rotation classes
+ * (tabulated per-spin propagators), relax classes (tabulated exponentials), and
+ * intervals evaluated on the fly (unique intervals after fusion). */
+int bloch_program_layout(const bloch_ctx* ctx, int64_t* n_ops, int64_t* n_rot_classes,
+                         int64_t* n_relax_classes, int64_t* n_onthefly_intervals);
+
 /*
  * Evolve one spin block through the uploaded tables — compute_block.
  *

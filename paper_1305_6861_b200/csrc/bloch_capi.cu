@@ -77,10 +77,10 @@ struct bloch_ctx {
   bloch::Program prog;
   bool has_prog = false;
   std::vector<uint8_t> snap_present;
-  DevBuf d_ops, d_gev, d_mats, d_sample_g;
+  DevBuf d_ops, d_gev, d_mats, d_sample_g, d_relax_t, d_rot_cls;
   DevBuf in_pos, in_mx, in_my, in_mz, in_t1, in_t2, in_m0, in_dw, in_w;
   DevBuf x, y, z, r1, r2, wpad;
-  DevBuf partial, echo, snaps;
+  DevBuf partial, echo, snaps, relax, rot;
   float kernel_ms = 0.f, device_ms = 0.f;
   int launches = 0;
 };
@@ -95,14 +95,14 @@ struct Variant {
 Variant pick_variant(int prec, int64_t n, int ncp, int n_sm) {
   if (prec == BLOCH_PREC_F32) {
     switch (ncp) {
-      case 1: return {32, n >= int64_t(n_sm) * 4 * 64 ? 4 : 1, 1};
+      case 1: return {32, n >= int64_t(n_sm) * 8 * 64 ? 8 : 2, 1};
       case 2: return {32, 4, 2};
-      case 4: return {32, 4, 4};
+      case 4: return {32, 2, 4};
       default: return {32, 2, 8};
     }
   }
   switch (ncp) {
-    case 1: return {64, n >= int64_t(n_sm) * 2 * 64 ? 2 : 1, 1};
+    case 1: return {64, n >= int64_t(n_sm) * 4 * 64 ? 4 : 1, 1};
     case 2: return {64, 2, 2};
     case 4: return {64, 2, 4};
     default: return {64, 1, 8};
@@ -207,7 +207,7 @@ int bloch_destroy(bloch_ctx* c) {
   }
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  for (DevBuf* b : {&c->d_ops, &c->d_gev, &c->d_mats, &c->d_sample_g, &c->in_pos, &c->in_mx, &c->in_my, &c->in_mz,
+  for (DevBuf* b : {&c->d_ops, &c->d_gev, &c->d_mats, &c->d_sample_g, &c->d_relax_t, &c->relax, &c->d_rot_cls, &c->rot, &c->in_pos, &c->in_mx, &c->in_my, &c->in_mz,
                     &c->in_t1, &c->in_t2, &c->in_m0, &c->in_dw, &c->in_w, &c->x, &c->y, &c->z, &c->r1,
                     &c->r2, &c->wpad, &c->partial, &c->echo, &c->snaps})
     b->release();
@@ -258,6 +258,8 @@ int bloch_set_tables(bloch_ctx* c, int32_t n_es, const int64_t* es_ev_offset,
       upload(c->d_ops, prog.ops.data(), prog.ops.size() * sizeof(bloch::DevOp), c->stream);
       upload(c->d_gev, prog.gev.data(), prog.gev.size() * sizeof(bloch::GEv), c->stream);
       upload(c->d_mats, prog.mats.data(), prog.mats.size() * sizeof(double), c->stream);
+      upload(c->d_relax_t, prog.relax_t.data(), prog.relax_t.size() * sizeof(double), c->stream);
+      upload(c->d_rot_cls, prog.rot_classes.data(), prog.rot_classes.size() * sizeof(bloch::RotClass), c->stream);
       upload(c->d_sample_g, prog.sample_g.data(), prog.sample_g.size() * sizeof(int64_t), c->stream);
       ck(cudaStreamSynchronize(c->stream), "set_tables sync");
     }
@@ -289,6 +291,20 @@ int bloch_program_stats(const bloch_ctx* c, int64_t* n_events, int64_t* n_sample
   if (n_window_samples) *n_window_samples = c->prog.n_window_samples;
   if (n_chirp_samples) *n_chirp_samples = c->prog.n_chirp_samples;
   if (n_train_pairs) *n_train_pairs = c->prog.n_train_pairs;
+  return BLOCH_OK;
+}
+
+int bloch_program_layout(const bloch_ctx* c, int64_t* n_ops, int64_t* n_rot_classes, int64_t* n_relax_classes,
+                         int64_t* n_onthefly_intervals) {
+  if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
+  if (!c->has_prog) return fail(BLOCH_E_STATE, "no tables uploaded");
+  int64_t otf = 0;
+  for (const auto& op : c->prog.ops)
+    if (op.kind == bloch::OP_EVENT && op.rot < 0 && (op.count & bloch::EV_MOVE)) otf++;
+  if (n_ops) *n_ops = static_cast<int64_t>(c->prog.ops.size());
+  if (n_rot_classes) *n_rot_classes = static_cast<int64_t>(c->prog.rot_classes.size());
+  if (n_relax_classes) *n_relax_classes = static_cast<int64_t>(c->prog.relax_t.size());
+  if (n_onthefly_intervals) *n_onthefly_intervals = otf;
   return BLOCH_OK;
 }
 
@@ -353,6 +369,23 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
                             c->z.as<double>(), c->r1.as<double>(), c->r2.as<double>(), st),
          "prep kernel");
       c->launches++;
+      const int n_cls = static_cast<int>(P.relax_t.size());
+      if (n_cls > 0) {
+        c->relax.ensure(2 * nd * n_cls);
+        ck(bloch::launch_relax_table(n, n_cls, c->d_relax_t.as<double>(), c->r1.as<double>(), c->r2.as<double>(),
+                                     c->relax.as<double>(), st),
+           "relax table kernel");
+        c->launches++;
+      }
+      const int n_rot = static_cast<int>(P.rot_classes.size());
+      if (n_rot > 0) {
+        c->rot.ensure(8 * nd * n_rot);
+        ck(bloch::launch_rot_table(n, n_rot, c->d_rot_cls.as<bloch::RotClass>(), c->x.as<double>(), c->y.as<double>(),
+                                   c->z.as<double>(), d_dw, c->r1.as<double>(), c->r2.as<double>(), d_m0,
+                                   c->rot.as<double>(), st),
+           "rotation table kernel");
+        c->launches++;
+      }
       if (d_w && ncp != n_coils) {
         c->wpad.ensure(2 * nd * ncp);
         ck(bloch::launch_pad_weights(n, n_coils, ncp, d_w, c->wpad.as<double>(), st), "pad kernel");
@@ -406,6 +439,8 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       kp.partial = c->partial.p;
       kp.part_stride = n_slots * 2;
       kp.snaps = d_snap;
+      kp.relax = c->relax.as<double>();
+      kp.rot = c->rot.as<double>();
       ck(cudaEventRecord(c->ev[1], st), "event");
       ck(dispatch(v, kp, static_cast<int>(grid), static_cast<int>(threads), st), "integrate kernel");
       ck(cudaEventRecord(c->ev[2], st), "event");

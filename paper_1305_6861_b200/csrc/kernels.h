@@ -21,6 +21,8 @@ struct KParams {
   void* partial;                 // [grid][part_stride] of R
   int64_t part_stride;           // n_samples * NC * 2
   double* snaps;                 // [n_snap][n][3] or nullptr
+  const double* relax;           // [n_cls][2][n]: exp(-T_c/T1_i), exp(-T_c/T2_i)
+  const double* rot;             // [n_rot][8][n]: rotation-class propagators (rot_table_kernel)
 };
 
 template <typename R, int S, int NC>
@@ -30,12 +32,12 @@ struct KernelTraits {
 
 // (real type, spins per thread, coils) instantiated in bloch_kernels.cu
 #define BLOCH_FOR_EACH_VARIANT(X) \
-  X(float, 4, 1)                  \
-  X(float, 1, 1)                  \
+  X(float, 8, 1)                  \
+  X(float, 2, 1)                  \
   X(float, 4, 2)                  \
-  X(float, 4, 4)                  \
+  X(float, 2, 4)                  \
   X(float, 2, 8)                  \
-  X(double, 2, 1)                 \
+  X(double, 4, 1)                 \
   X(double, 1, 1)                 \
   X(double, 2, 2)                 \
   X(double, 2, 4)                 \
@@ -45,6 +47,13 @@ template <typename R, int S, int NC>
 cudaError_t launch_integrate(const KParams& kp, int grid, int threads, cudaStream_t stream);
 template <typename R, int S, int NC>
 cudaError_t kernel_attrs(int* max_threads, int* regs);
+template <typename R, int S, int NC>
+size_t integrate_smem_bytes(int threads);
+cudaError_t launch_rot_table(int64_t n, int n_cls, const RotClass* rc, const double* x, const double* y,
+                             const double* z, const double* dw, const double* r1, const double* r2, const double* m0,
+                             double* out, cudaStream_t stream);
+cudaError_t launch_relax_table(int64_t n, int n_cls, const double* T, const double* r1, const double* r2, double* out,
+                               cudaStream_t stream);
 
 cudaError_t launch_prep(int64_t n, const double* pos, const double* t1, const double* t2, double* x,
                         double* y, double* z, double* r1, double* r2, cudaStream_t stream);

@@ -9,6 +9,9 @@
 #include "program_host.h"
 
 #include <algorithm>
+#include <array>
+#include <functional>
+#include <map>
 #include <cmath>
 #include <stdexcept>
 #include <string>
@@ -46,6 +49,8 @@ inline bool same_interval(double dt_a, const double* a, double dt_b, const doubl
 
 }  // namespace
 
+void fuse_intervals(Program& prog, const std::function<int32_t(double)>& relax_class);
+
 void compile_program(const TablesView& t, Program& prog) {
   prog = Program();
   prog.n_acq = t.n_acq;
@@ -67,6 +72,16 @@ void compile_program(const TablesView& t, Program& prog) {
   }
 
   auto dm = [&](int64_t i) { return t.ev_dmom + 3 * i; };
+  std::map<double, int32_t> classes;  // exact interval length -> relax class (engine.py:293)
+  auto relax_class = [&](double T) -> int32_t {
+    if (T == 0.0) return -1;
+    auto it = classes.find(T);
+    if (it != classes.end()) return it->second;
+    const int32_t c = static_cast<int32_t>(prog.relax_t.size());
+    classes.emplace(T, c);
+    prog.relax_t.push_back(T);
+    return c;
+  };
   auto n_ev = [&](int32_t es) { return t.es_ev_offset[es + 1] - t.es_ev_offset[es]; };
 
   // an ES that can join an RF train: exactly one event, no ADC, no snapshot
@@ -107,6 +122,8 @@ void compile_program(const TablesView& t, Program& prog) {
         op.p[0] = t.ev_dt[e0] == 0.0 ? 0.0 : sdt / n;
         for (int a = 0; a < 3; ++a) op.p[1 + a] = dm(e0)[a] == 0.0 ? 0.0 : sm[a] / n;
         op.flags = (moving(op.p[0], op.p + 1) ? EV_MOVE : 0) | (op.p[0] != 0.0 ? EV_RELAX : 0);
+        op.cls = relax_class(op.p[0]);
+        op.rot = -1;
         prog.ops.push_back(op);
         prog.n_events += k - es;
         prog.n_train_ops++;
@@ -194,6 +211,8 @@ void compile_program(const TablesView& t, Program& prog) {
         op.aux = t.ev_snap[i];
         op.p[0] = dt;
         for (int k = 0; k < 3; ++k) op.p[1 + k] = dm(i)[k];
+        op.cls = -1;  // classes are assigned by fuse_intervals()
+        op.rot = -1;
         prog.ops.push_back(op);
         prog.n_interval++;
         ++i;
@@ -214,6 +233,8 @@ void compile_program(const TablesView& t, Program& prog) {
         op.aux = lead;
         op.p[0] = t.ev_dt[j0] == 0.0 ? 0.0 : sdt / static_cast<double>(rot);
         for (int a = 0; a < 3; ++a) op.p[1 + a] = dm(j0)[a] == 0.0 ? 0.0 : sm[a] / static_cast<double>(rot);
+        op.cls = -1;
+        op.rot = -1;  // assigned by fuse_intervals()
         op.s0 = record_sample();
         for (int64_t k = 1; k < rot + lead; ++k) record_sample();
         prog.ops.push_back(op);
@@ -234,6 +255,8 @@ void compile_program(const TablesView& t, Program& prog) {
           // slope from the run's end points keeps the accumulated moment exact
           op.p[4 + a] = (dm(i + ch - 1)[a] - dm(i)[a]) / m;
         }
+        op.cls = relax_class(dt);
+        op.rot = -1;
         op.s0 = record_sample();
         for (int64_t k = 1; k < ch; ++k) record_sample();
         prog.ops.push_back(op);
@@ -256,6 +279,7 @@ void compile_program(const TablesView& t, Program& prog) {
         g.dmy = dm(i)[1];
         g.dmz = dm(i)[2];
         g.flags = (moving(g.dt, dm(i)) ? EV_MOVE : 0) | (g.dt != 0.0 ? EV_RELAX : 0);
+        g.cls = relax_class(g.dt);
         prog.gev.push_back(g);
         const int32_t s = record_sample();
         if (op.count == 0) op.s0 = s;
@@ -269,6 +293,156 @@ void compile_program(const TablesView& t, Program& prog) {
   }
   prog.n_events += prog.n_rot;
   prog.n_samples = static_cast<int64_t>(prog.sample_g.size());
+  fuse_intervals(prog, relax_class);
+}
+
+// Interval fusion and class assignment.
+//
+// Consecutive intervals with no pulse, ADC sample or snapshot between them
+// compose exactly into one interval: the transverse factors multiply
+// (e2_a e^{-i th_a}) (e2_b e^{-i th_b}) = e^{-(dt_a+dt_b)/T2} e^{-i (th_a+th_b)}
+// with th linear in (dmom, dt), and the longitudinal affine maps compose to
+// mz -> e1_a e1_b mz + m0 (1 - e1_a e1_b) — so (dt, dmom) simply add
+// (engine.py:288-302 applied back to back).
+//
+// Rotation classes (tabulated per-spin propagators, program.h) pay off only
+// when reused: a window absorbs the merged interval right before it (pre) and
+// right after it (post) when the resulting (pre, window, post) class occurs at
+// least kMinReuse times; other intervals get a class when they occur at least
+// kMinReuse times.  At most kMaxRotClasses classes are made (table memory is
+// classes x spins x 64 B); everything else is evaluated on the fly.
+void fuse_intervals(Program& prog, const std::function<int32_t(double)>& relax_class) {
+  constexpr int64_t kMinReuse = 4;
+  constexpr size_t kMaxRotClasses = 64;
+  struct Item {
+    DevOp op;
+    bool interval;  // merged EVENT
+  };
+  std::vector<Item> items;
+  for (const DevOp& op : prog.ops) {
+    if (op.kind == OP_EVENT) {
+      if (!items.empty() && items.back().interval && items.back().op.aux < 0) {
+        DevOp& m = items.back().op;  // extend the open interval
+        m.p[0] += op.p[0];
+        for (int a = 0; a < 3; ++a) m.p[1 + a] += op.p[1 + a];
+        m.aux = op.aux;  // a snapshot closes the merged interval
+      } else {
+        items.push_back({op, true});
+      }
+      continue;
+    }
+    items.push_back({op, false});
+  }
+  const size_t n_items = items.size();
+  using Key = std::array<double, 4>;
+  auto key_of = [](const DevOp& op) { return Key{op.p[0], op.p[1], op.p[2], op.p[3]}; };
+  const double none[4] = {0.0, 0.0, 0.0, 0.0};
+  using RotKey = std::array<double, 13>;
+  auto rot_key = [](const double* pre, const double* main, double mult, const double* post) {
+    RotKey key;
+    for (int a = 0; a < 4; ++a) {
+      key[a] = pre[a];
+      key[4 + a] = main[a];
+      key[9 + a] = post[a];
+    }
+    key[8] = mult;
+    return key;
+  };
+  auto free_interval = [&](size_t k) { return k < n_items && items[k].interval && items[k].op.aux < 0; };
+
+  // 1. windows: candidate absorption, kept when the absorbed class is reused
+  std::vector<int> pre_of(n_items, 0), post_of(n_items, 0);  // 1 = absorbs neighbour
+  std::map<RotKey, int64_t> win_uses;
+  auto win_key = [&](size_t k, int pre, int post) {
+    const DevOp& w = items[k].op;
+    return rot_key(pre ? items[k - 1].op.p : none, w.p, static_cast<double>(w.count - w.aux),
+                   post ? items[k + 1].op.p : none);
+  };
+  for (size_t k = 0; k < n_items; ++k)
+    if (items[k].op.kind == OP_WINDOW && !items[k].interval) {
+      pre_of[k] = k > 0 && free_interval(k - 1);
+      post_of[k] = free_interval(k + 1);
+    }
+  for (size_t k = 0; k + 1 < n_items; ++k)  // an interval between two windows goes to the earlier one
+    if (items[k].op.kind == OP_WINDOW && post_of[k] && k + 2 < n_items && pre_of[k + 2]) pre_of[k + 2] = 0;
+  for (size_t k = 0; k < n_items; ++k)
+    if (items[k].op.kind == OP_WINDOW && !items[k].interval) win_uses[win_key(k, pre_of[k], post_of[k])]++;
+  for (size_t k = 0; k < n_items; ++k)
+    if (items[k].op.kind == OP_WINDOW && !items[k].interval && win_uses[win_key(k, pre_of[k], post_of[k])] < kMinReuse)
+      pre_of[k] = post_of[k] = 0;
+  std::vector<bool> absorbed(n_items, false);
+  for (size_t k = 0; k < n_items; ++k) {
+    if (pre_of[k]) absorbed[k - 1] = true;
+    if (post_of[k]) absorbed[k + 1] = true;
+  }
+  // 2. reuse counts of the intervals that stay separate
+  std::map<Key, int64_t> iv_uses;
+  std::map<RotKey, int64_t> plain_win_uses;
+  for (size_t k = 0; k < n_items; ++k) {
+    if (items[k].interval && !absorbed[k]) iv_uses[key_of(items[k].op)]++;
+    if (items[k].op.kind == OP_WINDOW && !items[k].interval) plain_win_uses[win_key(k, pre_of[k], post_of[k])]++;
+  }
+
+  std::map<RotKey, int32_t> rot_ids;
+  auto rot_class = [&](const RotKey& key) -> int32_t {
+    auto f = rot_ids.find(key);
+    if (f != rot_ids.end()) return f->second;
+    if (prog.rot_classes.size() >= kMaxRotClasses) return -1;
+    const int32_t c = static_cast<int32_t>(prog.rot_classes.size());
+    rot_ids.emplace(key, c);
+    RotClass rc{};
+    for (int a = 0; a < 4; ++a) {
+      rc.pre[a] = key[a];
+      rc.main[a] = key[4 + a];
+      rc.post[a] = key[9 + a];
+    }
+    rc.mult = key[8];
+    prog.rot_classes.push_back(rc);
+    return c;
+  };
+
+  // 3. emit; windows first claim classes in order of reuse (most reused first)
+  std::vector<std::pair<int64_t, RotKey>> order;
+  for (const auto& kv : plain_win_uses) order.push_back({-kv.second, kv.first});
+  for (const auto& kv : iv_uses)
+    if (kv.second >= kMinReuse && moving(kv.first[0], kv.first.data() + 1))
+      order.push_back({-kv.second, rot_key(none, kv.first.data(), 1.0, none)});
+  std::sort(order.begin(), order.end());
+  for (const auto& o : order) rot_class(o.second);
+
+  std::vector<DevOp> out;
+  for (size_t k = 0; k < n_items; ++k) {
+    if (absorbed[k]) continue;
+    DevOp op = items[k].op;
+    if (op.kind == OP_WINDOW && !items[k].interval) {
+      const RotKey key = win_key(k, pre_of[k], post_of[k]);
+      auto f = rot_ids.find(key);
+      op.rot = f != rot_ids.end() ? f->second : -1;
+      if (op.rot < 0) {  // on-the-fly window: no absorbed neighbours (kept separate above only if classed)
+        if (pre_of[k] || post_of[k]) throw std::logic_error("absorbing window without a class");
+        op.cls = relax_class(op.p[0]);
+        op.flags = relax_class(op.p[0] * static_cast<double>(op.count - op.aux));  // whole-window class
+      }
+      prog.n_fused_windows += pre_of[k] + post_of[k];
+      out.push_back(op);
+      continue;
+    }
+    if (items[k].interval) {
+      const bool mv = moving(op.p[0], op.p + 1);
+      op.count = (mv ? EV_MOVE : 0) | (op.p[0] != 0.0 ? EV_RELAX : 0);
+      op.rot = -1;
+      op.cls = -1;
+      if (mv) {
+        auto f = rot_ids.find(rot_key(none, op.p, 1.0, none));
+        if (f != rot_ids.end()) op.rot = f->second;
+        else op.cls = relax_class(op.p[0]);
+      }
+      if (!mv && op.aux < 0) continue;  // a no-op interval (dt = 0, dmom = 0) without snapshot
+      prog.n_fused_intervals++;
+    }
+    out.push_back(op);
+  }
+  prog.ops.swap(out);
 }
 
 }  // namespace bloch

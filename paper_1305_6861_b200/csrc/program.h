@@ -27,6 +27,11 @@
 //
 // The per-spin state is fp64 in every precision mode; in the fp32 mode only
 // the ADC sample recurrence of OP_WINDOW runs in fp32.
+//
+// Relaxation factors are looked up, not evaluated: every distinct interval
+// length T (an event's dt, or a whole window's nrot*dt) is a "relax class";
+// a prep kernel tabulates exp(-T/T1), exp(-T/T2) per (class, spin) once per
+// call — the reference's relax_cache keyed on dt (engine.py:272, 292-299).
 #pragma once
 #include <stdint.h>
 
@@ -45,19 +50,37 @@ struct alignas(16) DevOp {
   double p[9];    // ROT: row-major matrix; EVENT/WINDOW/RFTRAIN: dt, dmx, dmy, dmz;
                   // CHIRP: dt, dmom_0 (3), dd (3)
   int32_t flags;  // RFTRAIN: EV_* flags of the shared interval
-  int32_t pad[9];
+  int32_t cls;    // relax class of dt (EVENT/CHIRP/RFTRAIN on-the-fly path), -1 = no relaxation
+  int32_t rot;    // rotation class (EVENT: repeated interval; WINDOW: always), -1 = none
+  int32_t pad[7];
 };
+
+// A rotation class: pre, then `mult` times main, then post (intervals (dt,
+// dmom)).  The prep kernel tabulates per spin the closed-form propagators
+//   Cpre = e2(pre) exp(-i theta_pre)                 (state at the first sample)
+//   C    = exp(-T/T2) exp(-i (theta_pre + mult theta + theta_post)),
+//   mz -> A mz + B, A = exp(-T/T1), B = m0 (1 - A),  T = total duration
+//   z    = e2(main) exp(-i theta)                    (per-sample factor)
+struct alignas(16) RotClass {
+  double pre[4];   // (dt, dmx, dmy, dmz) applied once before the run (WINDOW: before the samples)
+  double main[4];  // the repeated interval
+  double mult;     // repetitions of `main`
+  double post[4];  // applied once after the run
+  double pad[3];
+};
+static_assert(sizeof(RotClass) == 128, "RotClass must be 128 bytes");
 static_assert(sizeof(DevOp) == 128, "DevOp must be 128 bytes");
 
 struct alignas(16) GEv {  // one generic sampled interval
   double dt, dmx, dmy, dmz;
   int32_t flags;
-  int32_t pad[3];
+  int32_t cls;  // relax class of dt, -1 = none
+  int32_t pad[2];
 };
 static_assert(sizeof(GEv) == 48, "GEv must be 48 bytes");
 
 constexpr int kChunkSlots = 8;   // ADC slots reduced per warp transpose (samples x coils)
-constexpr int kStripSlots = 64;  // slots buffered per warp in shared memory before a CTA flush
+constexpr int kStripSlots = 256; // slots buffered per warp in shared memory before a CTA flush
 constexpr int kMinWindow = 4;    // shortest uniform run compiled as OP_WINDOW
 constexpr int kMinChirp = 3;     // shortest linear-increment run compiled as OP_CHIRP
 constexpr int kMinTrain = 4;     // shortest pulse+interval run compiled as OP_RFTRAIN

@@ -347,7 +347,11 @@ class BlochEngine:
         _capi.check(self._lib.bloch_program_stats(self._h, *[ctypes.byref(v) for v in vals]), "bloch_program_stats")
         keys = ("events", "samples", "rot", "interval", "window_ops", "window_samples", "chirp_samples",
                 "train_pairs")
-        return {k: v.value for k, v in zip(keys, vals)}
+        out = {k: v.value for k, v in zip(keys, vals)}
+        lay = [ctypes.c_int64() for _ in range(4)]
+        _capi.check(self._lib.bloch_program_layout(self._h, *[ctypes.byref(v) for v in lay]), "bloch_program_layout")
+        out.update(zip(("ops", "rot_classes", "relax_classes", "onthefly_intervals"), (v.value for v in lay)))
+        return out
 
     def last_timing(self) -> Dict[str, float]:
         k, d, n = ctypes.c_float(), ctypes.c_float(), ctypes.c_int32()
