@@ -1,0 +1,67 @@
+"""CPU, world_size 2 (gloo): the multi-GPU decomposition over spins.
+
+Each rank takes its contiguous shard (parallel.shard_block, the reference's
+np.linspace partition, engine.py:229-251), evolves it (here with the float64
+oracle standing in for the device, since this container has no GPU), and the
+partial k-space is summed with the single collective of the path
+(parallel.reduce_kspace -> dist.reduce); the final magnetisation shards are
+concatenated in rank order (parallel.gather_final_state).  Rank 0's result
+must equal the single-process result on the whole block — the reference's
+linearity / block-partition invariance (test_engine.py:175-200).
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, out_path):
+    import torch
+    import torch.distributed as dist
+
+    from oracle import bloch_oracle as O
+    from paper_1305_6861_b200 import configs
+    from paper_1305_6861_b200.parallel import gather_final_state, reduce_kspace, shard_block
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    w = configs.make(0).subset(4)
+    seq = w.sequence
+    tables = O.precompute_tables(seq, snapshot_times=(seq.end_time,))
+    shard = shard_block(w.block, world, rank)
+    echoes, snaps = O.compute_block(tables, shard.pos, shard.mx, shard.my, shard.mz, shard.t1, shard.t2, shard.m0,
+                                    shard.domega, shard.weight)
+    t = torch.from_numpy(np.ascontiguousarray(echoes).view(np.float64).copy())
+    reduce_kspace(t, dst=0)
+    final = gather_final_state(snaps[0], dst=0)
+    if rank == 0:
+        np.savez(out_path, echoes=t.numpy().view(np.complex128).reshape(echoes.shape), final=final)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_reduce_matches_single_process(tmp_path):
+    import torch.multiprocessing as mp
+
+    from oracle import bloch_oracle as O
+    from paper_1305_6861_b200 import configs
+
+    out = str(tmp_path / "r0.npz")
+    mp.start_processes(_worker, args=(2, _free_port(), out), nprocs=2, join=True, start_method="spawn")
+    got = np.load(out)
+    w = configs.make(0).subset(4)
+    seq = w.sequence
+    b = w.block
+    ref_e, ref_s = O.compute_block(O.precompute_tables(seq, snapshot_times=(seq.end_time,)), b.pos, b.mx, b.my, b.mz,
+                                   b.t1, b.t2, b.m0, b.domega, b.weight)
+    assert O.rel_l2(ref_e, got["echoes"]) <= 1e-13
+    assert np.array_equal(ref_s[0], got["final"])

@@ -1,0 +1,121 @@
+"""CPU: pin the oracle (and the product's host-side table builder) to the reference's own outputs.
+
+Golden records were produced by running the reference package itself
+(tests/golden/make_golden.py).  Here, without importing the reference:
+
+* the oracle's table restatement equals the reference tables bit for bit;
+* the product's ``precompute_sequence_tables`` equals them bit for bit;
+* the product's vectorised ``rasterize_arrays`` equals the reference's
+  ``rasterize`` + ``build_spin_arrays`` output bit for bit;
+* the oracle's ``compute_block`` reproduces the reference echoes and
+  snapshots (same numpy arithmetic, rel 1e-12 to allow a different BLAS
+  kernel for ``pos @ dmom`` on another CPU).
+"""
+
+import numpy as np
+import pytest
+
+import cases
+from conftest import load_golden
+from make_golden import projection_vector
+from oracle import bloch_oracle as O
+from paper_1305_6861_b200 import configs, flatten_tables, precompute_sequence_tables
+from paper_1305_6861_b200.phantom import rasterize_arrays
+
+SMALL = ["fid", "pair", "se16_box", "tse16", "epi16", "cpmg8", "mixed", "mixed_coils"]
+CONFIGS = ["cfg0", "cfg1", "cfg2", "cfg3", "cfg4"]
+
+
+def _sequence(name):
+    if name.startswith("cfg"):
+        return configs.make(int(name[3:])).sequence
+    return cases.small_cases()[name]["sequence"]
+
+
+def _assert_tables_equal(rec, tables):
+    flat = flatten_tables(tables)
+    for k, v in flat.items():
+        ref = rec["tab_" + k]
+        assert np.array_equal(np.asarray(v), ref), f"table field {k} differs"
+
+
+@pytest.mark.parametrize("name", SMALL + CONFIGS)
+def test_oracle_tables_match_reference(name):
+    rec = load_golden(name)
+    seq = _sequence(name)
+    snaps = tuple(rec["snapshot_times"].tolist())
+    _assert_tables_equal(rec, O.precompute_tables(seq, snapshot_times=snaps))
+    tabs = O.precompute_tables(seq, snapshot_times=snaps)
+    assert tabs.pulse_memo_hits == int(rec["pulse_memo_hits"])
+
+
+@pytest.mark.parametrize("name", SMALL + CONFIGS)
+def test_product_tables_match_reference(name):
+    rec = load_golden(name)
+    tables = precompute_sequence_tables(_sequence(name), snapshot_times=tuple(rec["snapshot_times"].tolist()))
+    _assert_tables_equal(rec, tables)
+    assert tables.pulse_memo_hits == int(rec["pulse_memo_hits"])
+
+
+def test_rasterize_matches_reference():  # phantom.py:98-142 + engine.py:192-226
+    rec = load_golden("se16_box")
+    case = cases.small_cases()["se16_box"]
+    a = rasterize_arrays(case["phantom"], case["spacing"])
+    assert np.array_equal(a["pos"], rec["spin_pos"])
+    assert np.array_equal(a["m0"], rec["spin_m0"])
+    assert np.array_equal(a["t1"], rec["spin_t1"])
+    assert np.array_equal(a["t2"], rec["spin_t2"])
+
+
+def _oracle_run(name, rec):
+    tables = O.precompute_tables(_sequence(name), snapshot_times=tuple(rec["snapshot_times"].tolist()))
+    return O.compute_block(tables, rec["spin_pos"], rec["spin_mx"], rec["spin_my"], rec["spin_mz"], rec["spin_t1"],
+                           rec["spin_t2"], rec["spin_m0"], rec["spin_domega"], rec["spin_weight"])
+
+
+def _check_echoes(rec, echoes, tol):
+    assert echoes.shape == tuple(rec["echo_shape"])
+    if "echo_full" in rec:
+        assert O.rel_l2(rec["echo_full"], echoes) <= tol
+        return
+    ek = echoes.reshape((-1,) + echoes.shape[-2:])
+    assert O.rel_l2(rec["echo_head"], ek[:, :4]) <= tol
+    assert O.rel_l2(rec["echo_tail"], ek[:, -4:]) <= tol
+    assert O.rel_l2(rec["echo_proj"], ek @ projection_vector(ek.shape[-1])) <= tol
+    assert O.rel_l2(rec["echo_energy"], (np.abs(ek) ** 2).sum(axis=-1)) <= tol
+
+
+@pytest.mark.parametrize("name", SMALL + ["cfg0", "cfg1", "cfg3"])
+def test_oracle_compute_block_matches_reference(name):
+    rec = load_golden(name)
+    echoes, snaps = _oracle_run(name, rec)
+    _check_echoes(rec, echoes, 1e-12)
+    for i in range(int(rec["n_snap"])):
+        if bool(rec[f"snap_{i}_present"]):
+            assert O.rel_l2(rec[f"snap_{i}"], snaps[i]) <= 1e-12
+        else:
+            assert snaps[i] is None
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["cfg2", "cfg4"])
+def test_oracle_compute_block_matches_reference_long(name):
+    rec = load_golden(name)
+    echoes, snaps = _oracle_run(name, rec)
+    _check_echoes(rec, echoes, 1e-12)
+    assert O.rel_l2(rec["snap_0"], snaps[0]) <= 1e-12
+
+
+def test_event_counts_match_survey():  # E = 4,480 / 67,072 / 264,768
+    want = {0: 4480, 1: 67072, 2: 264768}
+    for i, e in want.items():
+        assert O.event_count(O.precompute_tables(configs.make(i).sequence)) == e
+
+
+def test_delta_e_stoer_and_rel_l2():  # engine.py:603-616; test_engine.py:277-291
+    rng = np.random.default_rng(0)
+    ref = rng.normal(size=256) + 1j * rng.normal(size=256)
+    assert O.delta_e_stoer(ref, ref) == -np.inf
+    assert O.delta_e_stoer(ref, ref * (1 + 1e-6)) == pytest.approx(-120.0, abs=0.5)
+    assert O.delta_e_stoer(np.array([1.0, 2.0, 3.0]), np.zeros(3)) == pytest.approx(0.0, abs=1e-12)
+    assert O.rel_l2(ref, ref * (1 + 1e-4)) == pytest.approx(1e-4, rel=1e-6)
