@@ -110,6 +110,23 @@ Variant pick_variant(int prec, int64_t n, int ncp, int n_sm) {
 }
 
 template <typename R, int S, int NC>
+void shape_one(const Variant& v, int* max_t, int* min_b) {
+  if (v.prec == int(8 * sizeof(R)) && v.S == S && v.NC == NC) {
+    *max_t = bloch::KernelTraits<R, S, NC>::kMaxThreads;
+    *min_b = bloch::KernelTraits<R, S, NC>::kMinBlocks;
+  }
+}
+
+// max threads per CTA and resident CTAs per SM of a variant
+void variant_shape(const Variant& v, int* max_t, int* min_b) {
+  *max_t = 512;
+  *min_b = 1;
+#define BLOCH_SHAPE(R, S, NC) shape_one<R, S, NC>(v, max_t, min_b);
+  BLOCH_FOR_EACH_VARIANT(BLOCH_SHAPE)
+#undef BLOCH_SHAPE
+}
+
+template <typename R, int S, int NC>
 cudaError_t dispatch_one(const Variant& v, const bloch::KParams& kp, int grid, int threads,
                          cudaStream_t st, bool* matched) {
   if (v.prec == int(8 * sizeof(R)) && v.S == S && v.NC == NC) {
@@ -407,17 +424,20 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
     float kms = 0.f;
     if (n > 0) {
       const Variant v = pick_variant(c->precision, n, ncp, c->n_sm);
-      const int max_t = 512;
-      const int64_t per_wave = int64_t(c->n_sm) * v.S * max_t;
+      int max_t = 512, min_b = 1;
+      variant_shape(v, &max_t, &min_b);
+      const int64_t slots = int64_t(c->n_sm) * min_b;  // resident CTAs per wave
+      const int64_t per_wave = slots * v.S * max_t;
       const int64_t waves = (n + per_wave - 1) / per_wave;
-      int64_t threads = (n + int64_t(c->n_sm) * waves * v.S - 1) / (int64_t(c->n_sm) * waves * v.S);
+      int64_t threads = (n + slots * waves * v.S - 1) / (slots * waves * v.S);
       threads = ((threads + 31) / 32) * 32;
       threads = std::max<int64_t>(32, std::min<int64_t>(max_t, threads));
       const int64_t spc = threads * v.S;
       const int64_t grid = (n + spc - 1) / spc;
       const int64_t n_slots = P.n_samples * ncp;
       const size_t rsz = v.prec == 32 ? sizeof(float) : sizeof(double);
-      c->partial.ensure(static_cast<size_t>(std::max<int64_t>(1, grid * n_slots * 2)) * rsz);
+      const int64_t rows = grid * (threads / 32);  // one partial row per warp
+      c->partial.ensure(static_cast<size_t>(std::max<int64_t>(1, rows * n_slots * 2)) * rsz);
       bloch::KParams kp{};
       kp.ops = c->d_ops.as<bloch::DevOp>();
       kp.n_ops = static_cast<int32_t>(P.ops.size());
@@ -447,11 +467,11 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       c->launches++;
       if (n_slots > 0) {
         if (v.prec == 32)
-          ck(bloch::launch_reduce<float>(c->partial.as<float>(), static_cast<int>(grid), n_slots,
+          ck(bloch::launch_reduce<float>(c->partial.as<float>(), static_cast<int>(rows), n_slots,
                                          n_coils, ncp, c->d_sample_g.as<int64_t>(), G, d_echo, st),
              "reduce kernel");
         else
-          ck(bloch::launch_reduce<double>(c->partial.as<double>(), static_cast<int>(grid), n_slots,
+          ck(bloch::launch_reduce<double>(c->partial.as<double>(), static_cast<int>(rows), n_slots,
                                           n_coils, ncp, c->d_sample_g.as<int64_t>(), G, d_echo, st),
              "reduce kernel");
         c->launches++;

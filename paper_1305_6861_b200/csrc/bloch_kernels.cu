@@ -99,47 +99,28 @@ __device__ __forceinline__ void transpose_reduce8(R (&v)[kChunkSlots], int lane)
 // per-CTA ADC strip (shared memory) and its flush to the partial buffer
 // ---------------------------------------------------------------------------
 
+// Each warp owns one row of the partial buffer: after the transpose-reduction
+// the 8 lanes holding a slot total write it straight to global memory (64 B per
+// chunk, coalesced).  No shared-memory staging, no CTA barrier: warps never wait
+// for each other.  reduce_partials_kernel folds the warp rows in a fixed order
+// in fp64, so results stay bit-reproducible (engine.py:594-595).
 template <typename R>
 struct Strip {
-  R* val;        // [2][nw][kStripSlots][2]
-  int32_t* idx;  // [2][kStripSlots] compact slot id of each strip position
-  int nw, warp, lane, slots, buf;
+  R* row;  // this warp's partial row: [n_slots][2]
+  int lane;
 
-  __device__ __forceinline__ R& at(int b, int w, int s, int comp) {
-    return val[((b * nw + w) * kStripSlots + s) * 2 + comp];
-  }
-
-  // Reduce one chunk (cnt <= 8 slots) across the warp and append it.
+  // Reduce one chunk (cnt <= 8 slots) across the warp and store it.
   __device__ __forceinline__ void push(R (&re)[kChunkSlots], R (&im)[kChunkSlots], int cnt, int32_t first_id) {
     transpose_reduce8(re, lane);
     transpose_reduce8(im, lane);
     const int j = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
     if ((lane & 3) == 0 && j < cnt) {
-      at(buf, warp, slots + j, 0) = re[0];
-      at(buf, warp, slots + j, 1) = im[0];
+      R* p = row + static_cast<int64_t>(first_id + j) * 2;
+      p[0] = re[0];
+      p[1] = im[0];
     }
-    // every warp writes the same ids: no per-warp predicate to keep live
-    if (lane < cnt) idx[buf * kStripSlots + slots + lane] = first_id + lane;
-    slots += cnt;
   }
-
-  // CTA-wide: sum the warps' strips and write this CTA's partial row.
-  // Must be reached by every thread of the CTA (uniform control flow).
-  __device__ __forceinline__ void flush(R* part_row) {
-    __syncthreads();
-    const int total = slots * 2;
-    for (int t = threadIdx.x; t < total; t += blockDim.x) {
-      const int s = t >> 1, comp = t & 1;
-      R acc = R(0);
-      for (int w = 0; w < nw; ++w) acc += at(buf, w, s, comp);
-      part_row[static_cast<int64_t>(idx[buf * kStripSlots + s]) * 2 + comp] = acc;
-    }
-    buf ^= 1;
-    slots = 0;
-  }
-  __device__ __forceinline__ void reserve(int cnt, R* part_row) {
-    if (slots + cnt > kStripSlots) flush(part_row);
-  }
+  __device__ __forceinline__ void reserve(int, R*) {}
 };
 
 // ---------------------------------------------------------------------------
@@ -327,7 +308,8 @@ __device__ __forceinline__ void window_chunk_f2(float2 (&U)[P], float2 (&V)[P], 
 // ---------------------------------------------------------------------------
 
 template <typename R, int S, int NC>
-__global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, 1) integrate_kernel(const KParams kp) {
+__global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTraits<R, S, NC>::kMinBlocks)
+    integrate_kernel(const KParams kp) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int kSampPerChunk = kChunkSlots / NC;
   constexpr bool kPacked = sizeof(R) == 4 && NC == 1 && (S % 2 == 0);
@@ -338,15 +320,11 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, 1) integr
   sp.base = static_cast<int64_t>(blockIdx.x) * kp.spins_per_cta + threadIdx.x;
   sp.bd = bd;
   sp.n = kp.n;
-  Strip<R> strip;
-  strip.val = reinterpret_cast<R*>(sp.sm + 3 * S * bd);
-  strip.idx = reinterpret_cast<int32_t*>(strip.val + 2 * nw * kStripSlots * 2);
-  strip.nw = nw;
-  strip.warp = threadIdx.x >> 5;
+  Strip<R> strip;  // one partial row per warp of the grid
   strip.lane = threadIdx.x & 31;
-  strip.slots = 0;
-  strip.buf = 0;
-  R* part_row = reinterpret_cast<R*>(kp.partial) + static_cast<int64_t>(blockIdx.x) * kp.part_stride;
+  strip.row = reinterpret_cast<R*>(kp.partial) +
+              (static_cast<int64_t>(blockIdx.x) * nw + (threadIdx.x >> 5)) * kp.part_stride;
+  R* part_row = strip.row;
 
 #pragma unroll
   for (int s = 0; s < S; ++s) {
@@ -688,7 +666,6 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, 1) integr
       }
     }
   }
-  if (strip.slots > 0) strip.flush(part_row);
 }
 
 // ---------------------------------------------------------------------------
@@ -792,8 +769,8 @@ __global__ void reduce_partials_kernel(const R* __restrict__ part, int grid, int
 template <typename R, int S, int NC>
 size_t integrate_smem_bytes(int threads) {
   const int nw = threads / 32;
-  return static_cast<size_t>(3 * S * threads) * sizeof(double) +
-         static_cast<size_t>(2 * nw * kStripSlots * 2) * sizeof(R) + static_cast<size_t>(2 * kStripSlots) * sizeof(int32_t);
+  (void)nw;
+  return static_cast<size_t>(3 * S * threads) * sizeof(double);
 }
 
 template <typename R, int S, int NC>

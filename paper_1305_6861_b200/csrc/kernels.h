@@ -25,9 +25,17 @@ struct KParams {
   const double* rot;             // [n_rot][8][n]: rotation-class propagators (rot_table_kernel)
 };
 
+// Launch shape per variant: max threads per CTA and min resident CTAs per SM
+// (registers per thread <= 64K / (kMaxThreads * kMinBlocks)).
 template <typename R, int S, int NC>
 struct KernelTraits {
   static constexpr int kMaxThreads = 512;
+  static constexpr int kMinBlocks = 1;
+};
+template <>
+struct KernelTraits<float, 8, 1> {  // the fp32 single-coil workhorse: 2 CTAs x 10 warps per SM
+  static constexpr int kMaxThreads = 320;
+  static constexpr int kMinBlocks = 2;
 };
 
 // (real type, spins per thread, coils) instantiated in bloch_kernels.cu
