@@ -77,10 +77,10 @@ struct bloch_ctx {
   bloch::Program prog;
   bool has_prog = false;
   std::vector<uint8_t> snap_present;
-  DevBuf d_ops, d_gev, d_mats, d_sample_g, d_relax_t, d_rot_cls;
+  DevBuf d_ops, d_gev, d_mats, d_sample_g, d_relax_t, d_rot_cls, d_prog_cls;
   DevBuf in_pos, in_mx, in_my, in_mz, in_t1, in_t2, in_m0, in_dw, in_w;
-  DevBuf x, y, z, r1, r2, wpad;
-  DevBuf partial, echo, snaps, relax, rot;
+  DevBuf sc, wpad;
+  DevBuf partial, echo, snaps, relax, rot, progtab;
   float kernel_ms = 0.f, device_ms = 0.f;
   int launches = 0;
 };
@@ -225,8 +225,8 @@ int bloch_destroy(bloch_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (DevBuf* b : {&c->d_ops, &c->d_gev, &c->d_mats, &c->d_sample_g, &c->d_relax_t, &c->relax, &c->d_rot_cls, &c->rot, &c->in_pos, &c->in_mx, &c->in_my, &c->in_mz,
-                    &c->in_t1, &c->in_t2, &c->in_m0, &c->in_dw, &c->in_w, &c->x, &c->y, &c->z, &c->r1,
-                    &c->r2, &c->wpad, &c->partial, &c->echo, &c->snaps})
+                    &c->in_t1, &c->in_t2, &c->in_m0, &c->in_dw, &c->in_w, &c->sc, &c->wpad, &c->partial,
+                    &c->echo, &c->snaps, &c->d_prog_cls, &c->progtab})
     b->release();
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
@@ -277,6 +277,8 @@ int bloch_set_tables(bloch_ctx* c, int32_t n_es, const int64_t* es_ev_offset,
       upload(c->d_mats, prog.mats.data(), prog.mats.size() * sizeof(double), c->stream);
       upload(c->d_relax_t, prog.relax_t.data(), prog.relax_t.size() * sizeof(double), c->stream);
       upload(c->d_rot_cls, prog.rot_classes.data(), prog.rot_classes.size() * sizeof(bloch::RotClass), c->stream);
+      upload(c->d_prog_cls, prog.prog_classes.data(), prog.prog_classes.size() * sizeof(bloch::ProgClass),
+             c->stream);
       upload(c->d_sample_g, prog.sample_g.data(), prog.sample_g.size() * sizeof(int64_t), c->stream);
       ck(cudaStreamSynchronize(c->stream), "set_tables sync");
     }
@@ -317,7 +319,7 @@ int bloch_program_layout(const bloch_ctx* c, int64_t* n_ops, int64_t* n_rot_clas
   if (!c->has_prog) return fail(BLOCH_E_STATE, "no tables uploaded");
   int64_t otf = 0;
   for (const auto& op : c->prog.ops)
-    if (op.kind == bloch::OP_EVENT && op.rot < 0 && (op.count & bloch::EV_MOVE)) otf++;
+    if (op.kind == bloch::OP_EVENT && op.rot < 0 && op.prg < 0 && (op.count & bloch::EV_MOVE)) otf++;
   if (n_ops) *n_ops = static_cast<int64_t>(c->prog.ops.size());
   if (n_rot_classes) *n_rot_classes = static_cast<int64_t>(c->prog.rot_classes.size());
   if (n_relax_classes) *n_relax_classes = static_cast<int64_t>(c->prog.relax_t.size());
@@ -375,32 +377,32 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
         d_w = c->in_w.as<double>();
       }
     }
-    // 2. staging: SoA positions, 1/T1, 1/T2, padded weights
+    // 2. staging: per-spin constant records, relax / rotation / progression class tables
     if (n > 0) {
-      c->x.ensure(nd);
-      c->y.ensure(nd);
-      c->z.ensure(nd);
-      c->r1.ensure(nd);
-      c->r2.ensure(nd);
-      ck(bloch::launch_prep(n, d_pos, d_t1, d_t2, c->x.as<double>(), c->y.as<double>(),
-                            c->z.as<double>(), c->r1.as<double>(), c->r2.as<double>(), st),
-         "prep kernel");
+      c->sc.ensure(static_cast<size_t>(n) * sizeof(bloch::SpinConst));
+      bloch::SpinConst* d_sc = c->sc.as<bloch::SpinConst>();
+      ck(bloch::launch_prep(n, d_pos, d_dw, d_m0, d_t1, d_t2, d_sc, st), "prep kernel");
       c->launches++;
       const int n_cls = static_cast<int>(P.relax_t.size());
       if (n_cls > 0) {
         c->relax.ensure(2 * nd * n_cls);
-        ck(bloch::launch_relax_table(n, n_cls, c->d_relax_t.as<double>(), c->r1.as<double>(), c->r2.as<double>(),
-                                     c->relax.as<double>(), st),
+        ck(bloch::launch_relax_table(n, n_cls, c->d_relax_t.as<double>(), d_sc, c->relax.as<double>(), st),
            "relax table kernel");
         c->launches++;
       }
       const int n_rot = static_cast<int>(P.rot_classes.size());
       if (n_rot > 0) {
         c->rot.ensure(8 * nd * n_rot);
-        ck(bloch::launch_rot_table(n, n_rot, c->d_rot_cls.as<bloch::RotClass>(), c->x.as<double>(), c->y.as<double>(),
-                                   c->z.as<double>(), d_dw, c->r1.as<double>(), c->r2.as<double>(), d_m0,
-                                   c->rot.as<double>(), st),
+        ck(bloch::launch_rot_table(n, n_rot, c->d_rot_cls.as<bloch::RotClass>(), d_sc, c->rot.as<double>(), st),
            "rotation table kernel");
+        c->launches++;
+      }
+      const int n_prog = static_cast<int>(P.prog_classes.size());
+      if (n_prog > 0) {
+        c->progtab.ensure(8 * nd * n_prog);
+        ck(bloch::launch_prog_table(n, n_prog, c->d_prog_cls.as<bloch::ProgClass>(), d_sc, c->progtab.as<double>(),
+                                    st),
+           "progression table kernel");
         c->launches++;
       }
       if (d_w && ncp != n_coils) {
@@ -445,13 +447,7 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       kp.gev = c->d_gev.as<bloch::GEv>();
       kp.mats = c->d_mats.as<double>();
       kp.n = n;
-      kp.x = c->x.as<double>();
-      kp.y = c->y.as<double>();
-      kp.z = c->z.as<double>();
-      kp.dw = d_dw;
-      kp.r1 = c->r1.as<double>();
-      kp.r2 = c->r2.as<double>();
-      kp.m0 = d_m0;
+      kp.sc = c->sc.as<bloch::SpinConst>();
       kp.mx0 = d_mx;
       kp.my0 = d_my;
       kp.mz0 = d_mz;
@@ -461,6 +457,7 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       kp.snaps = d_snap;
       kp.relax = c->relax.as<double>();
       kp.rot = c->rot.as<double>();
+      kp.prog = c->progtab.as<double>();
       ck(cudaEventRecord(c->ev[1], st), "event");
       ck(dispatch(v, kp, static_cast<int>(grid), static_cast<int>(threads), st), "integrate kernel");
       ck(cudaEventRecord(c->ev[2], st), "event");

@@ -3,28 +3,26 @@
 // integrate_kernel<R, S, NC>  — the hot path: restates engine.compute_block
 //   (engine.py:259-310) for S spins per thread.  The op stream (program.h) is
 //   identical for every thread, so all control flow is CTA-uniform and op
-//   fields are broadcast loads.  ADC samples are reduced without atomics:
-//   per-thread sum over its S spins -> warp transpose-reduction of 8 slots
-//   (sample x coil) -> per-warp strip in shared memory -> CTA sum written to
-//   this CTA's row of the partial buffer; reduce_partials() then folds the rows
-//   in a fixed order in fp64 (deterministic, like the reference's ordered fold,
-//   engine.py:594-595).
+//   fields are broadcast loads.  ADC samples are reduced without atomics and
+//   without CTA barriers: per-thread sum over its S spins -> warp
+//   transpose-reduction of 8 slots (sample x coil) -> the warp's own row of the
+//   partial buffer; reduce_partials_kernel folds the rows in a fixed order in
+//   fp64 (deterministic, like the reference's ordered fold, engine.py:594-595).
 //
 // Precision: the per-spin state (mx, my, mz) is fp64 in every mode and lives in
-// shared memory between ops (it only changes at pulses, generic intervals, RF
-// trains, chirps and window exits).  R is the type of the ADC sample
-// recurrence inside uniform windows, the dominant work: fp32
-// (BLOCH_PREC_F32, packed FFMA2/FMUL2/FADD2 over spin pairs) or fp64.
+// shared memory between ops (it only changes at pulses, intervals, RF trains,
+// chirps and window exits).  R is the type of the ADC sample recurrence inside
+// uniform windows, the dominant work: fp32 (BLOCH_PREC_F32, packed
+// FFMA2/FMUL2/FADD2 over spin pairs) or fp64.
 //
-// Uniform ADC windows (OP_WINDOW): per spin the window rotation
-// z = e2 * exp(-i*theta) is formed once (fp64 phase, reduced mod 2pi) and the
-// receive-weighted transverse magnetisation u = w * (mx + i*my) is advanced by
-// one complex multiply per sample (engine.py:289-305 for every sample of the
-// window: same theta, same e2 from the relax cache).  The state that leaves the
-// window comes from the closed form m * E2^n * exp(-i*n*theta),
-// mz -> m0 + (mz - m0) * E1^n in fp64, so per-sample rounding never feeds back
-// into the spin state.  Relaxation factors come from the per-(class, spin)
-// table built by relax_table_kernel (the reference's relax_cache).
+// Uniform ADC windows (OP_WINDOW): per spin the sample factor
+// z = e2 * exp(-i*theta) and the closed-form propagators of the whole
+// (pre, samples, post) run come from the rotation-class table (built once per
+// call by rot_table_kernel, fp64); the receive-weighted transverse
+// magnetisation u = w * (Cpre m) is advanced by one complex multiply per sample
+// (engine.py:289-305 for every sample of the window: same theta, same e2 from
+// the relax cache).  The state leaving the window is C m, mz -> A mz + B in
+// fp64, so per-sample rounding never feeds back into the spin state.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -45,15 +43,11 @@ __device__ __forceinline__ double reduce_2pi(double th) {
   return fma(-k, kLo, fma(-k, kHi, th));
 }
 
-template <typename R>
-__device__ __forceinline__ void phase_sincos(double th, R& s, R& c);
-template <>
-__device__ __forceinline__ void phase_sincos<float>(double th, float& s, float& c) {
-  sincosf(static_cast<float>(reduce_2pi(th)), &s, &c);
-}
-template <>
-__device__ __forceinline__ void phase_sincos<double>(double th, double& s, double& c) {
+// exp(-i*theta) = (c, -s), fp64
+__device__ __forceinline__ void phase_factor(double th, double& c, double& ms) {
+  double s;
   sincos(reduce_2pi(th), &s, &c);
+  ms = -s;
 }
 
 template <typename R>
@@ -95,21 +89,14 @@ __device__ __forceinline__ void transpose_reduce8(R (&v)[kChunkSlots], int lane)
   v[0] += shfl_x(v[0], 1);
 }
 
-// ---------------------------------------------------------------------------
-// per-CTA ADC strip (shared memory) and its flush to the partial buffer
-// ---------------------------------------------------------------------------
-
 // Each warp owns one row of the partial buffer: after the transpose-reduction
 // the 8 lanes holding a slot total write it straight to global memory (64 B per
-// chunk, coalesced).  No shared-memory staging, no CTA barrier: warps never wait
-// for each other.  reduce_partials_kernel folds the warp rows in a fixed order
-// in fp64, so results stay bit-reproducible (engine.py:594-595).
+// chunk, coalesced).  No shared-memory staging, no CTA barrier.
 template <typename R>
 struct Strip {
   R* row;  // this warp's partial row: [n_slots][2]
   int lane;
 
-  // Reduce one chunk (cnt <= 8 slots) across the warp and store it.
   __device__ __forceinline__ void push(R (&re)[kChunkSlots], R (&im)[kChunkSlots], int cnt, int32_t first_id) {
     transpose_reduce8(re, lane);
     transpose_reduce8(im, lane);
@@ -120,11 +107,10 @@ struct Strip {
       p[1] = im[0];
     }
   }
-  __device__ __forceinline__ void reserve(int, R*) {}
 };
 
 // ---------------------------------------------------------------------------
-// spin state in shared memory: [3][S][blockDim] doubles (mx, my, mz)
+// spin state (shared memory, [3][S][blockDim] fp64) and per-spin constants
 // ---------------------------------------------------------------------------
 
 template <int S>
@@ -140,58 +126,47 @@ struct Spins {
   __device__ __forceinline__ double& mz(int s) { return sm[(2 * S + s) * bd + threadIdx.x]; }
 };
 
-__device__ __forceinline__ double spin_theta(const KParams& kp, int64_t i, double dt, double dmx, double dmy,
-                                             double dmz) {
-  // engine.py:289 — theta = pos @ dmom + domega * dt
-  return fma(kp.z[i], dmz, fma(kp.y[i], dmy, kp.x[i] * dmx)) + kp.dw[i] * dt;
-}
-
-// relax-class table: e1 = exp(-T_c/T1_i) at [2c][i], e2 = exp(-T_c/T2_i) at [2c+1][i]
-__device__ __forceinline__ double rt_e1(const KParams& kp, int c, int64_t i) {
-  return kp.relax[(2 * static_cast<int64_t>(c)) * kp.n + i];
-}
-__device__ __forceinline__ double rt_e2(const KParams& kp, int c, int64_t i) {
-  return kp.relax[(2 * static_cast<int64_t>(c) + 1) * kp.n + i];
-}
-
-// rotation-class table (program.h RotClass), SoA [class][field][spin], fp64:
-//   0,1 = Cpre; 2,3 = C (whole run); 4,5 = A, B (mz affine map); 6,7 = z (per sample)
-struct RotCoef {
-  double cr, ci, a, b;
+// SpinConst (kernels.h): one 64-byte record per spin, 4 x 16-byte loads
+struct SC {
+  double x, y, z, dw, m0;
 };
-constexpr int kRotFields = 8;
-__device__ __forceinline__ const double* rot_ptr(const KParams& kp, int c, int64_t i) {
-  return kp.rot + static_cast<int64_t>(c) * kRotFields * kp.n + i;
+__device__ __forceinline__ SC load_sc(const KParams& kp, int64_t i) {
+  const double2* p = reinterpret_cast<const double2*>(kp.sc + i);
+  const double2 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+  return SC{a.x, a.y, b.x, b.y, c.x};
 }
-__device__ __forceinline__ RotCoef rot_coef(const KParams& kp, int c, int64_t i) {
-  const double* t = rot_ptr(kp, c, i);
-  RotCoef k;  // read-only path: lets the loads of all spins issue ahead of the shared-memory state stores
-  k.cr = __ldg(t + 2 * kp.n);
-  k.ci = __ldg(t + 3 * kp.n);
-  k.a = __ldg(t + 4 * kp.n);
-  k.b = __ldg(t + 5 * kp.n);
-  return k;
+// engine.py:289 — theta = pos @ dmom + domega * dt
+__device__ __forceinline__ double theta_of(const SC& c, double dt, double dmx, double dmy, double dmz) {
+  return fma(c.z, dmz, fma(c.y, dmy, c.x * dmx)) + c.dw * dt;
+}
+// relax-class table: (e1, e2) = (exp(-T_c/T1_i), exp(-T_c/T2_i)) at [c][i]
+__device__ __forceinline__ double2 relax_pair(const KParams& kp, int c, int64_t i) {
+  return __ldg(reinterpret_cast<const double2*>(kp.relax) + static_cast<int64_t>(c) * kp.n + i);
+}
+// rotation-class table, AoS [c][i][8]: Cpre (2), C (2), A, B, z (2)
+struct RotCoef {
+  double pr, pi, cr, ci, a, b, zr, zi;
+};
+__device__ __forceinline__ RotCoef load_rot(const KParams& kp, int c, int64_t i) {
+  const double2* p = reinterpret_cast<const double2*>(kp.rot) + (static_cast<int64_t>(c) * kp.n + i) * 4;
+  const double2 a = __ldg(p), b = __ldg(p + 1), d = __ldg(p + 2), e = __ldg(p + 3);
+  return RotCoef{a.x, a.y, b.x, b.y, d.x, d.y, e.x, e.y};
 }
 
-// one interval on spin s: precession (+ relaxation), fp64 — engine.py:288-302
+// one interval on spin s (on the fly): precession (+ relaxation), fp64 — engine.py:288-302
 template <int S>
 __device__ __forceinline__ void interval(const KParams& kp, Spins<S>& sp, int s, int flags, int cls, double dt,
                                          double dmx, double dmy, double dmz) {
   if (!(flags & EV_MOVE) || !sp.act(s)) return;
   const int64_t i = sp.idx(s);
-  double sn, cs;
-  phase_sincos<double>(spin_theta(kp, i, dt, dmx, dmy, dmz), sn, cs);
+  const SC c = load_sc(kp, i);
+  const double2 e = cls >= 0 ? relax_pair(kp, cls, i) : make_double2(1.0, 1.0);
+  double cs, ms;
+  phase_factor(theta_of(c, dt, dmx, dmy, dmz), cs, ms);
   const double x = sp.mx(s), y = sp.my(s);
-  double nx = cs * x + sn * y;  // clockwise, bloch.py:10-17
-  double ny = cs * y - sn * x;
-  if (cls >= 0) {
-    const double e1 = rt_e1(kp, cls, i), e2 = rt_e2(kp, cls, i);
-    nx *= e2;
-    ny *= e2;
-    sp.mz(s) = sp.mz(s) * e1 + kp.m0[i] * (1.0 - e1);
-  }
-  sp.mx(s) = nx;
-  sp.my(s) = ny;
+  sp.mx(s) = e.y * (cs * x - ms * y);  // clockwise: (c - i s)(x + i y), bloch.py:10-17
+  sp.my(s) = e.y * (cs * y + ms * x);
+  if (cls >= 0) sp.mz(s) = fma(sp.mz(s), e.x, c.m0 * (1.0 - e.x));
 }
 
 // receive-weighted transverse magnetisation of the (fp64) state summed over the
@@ -205,15 +180,11 @@ __device__ __forceinline__ void record_state(const KParams& kp, Spins<S>& sp, R 
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       if (!sp.act(s)) continue;
-      double wr = 1.0, wi = 0.0;
-      if (kp.w != nullptr) {
-        const double* p = kp.w + (static_cast<int64_t>(c) * kp.n + sp.idx(s)) * 2;
-        wr = p[0];
-        wi = p[1];
-      }
+      double2 w = make_double2(1.0, 0.0);
+      if (kp.w != nullptr) w = __ldg(reinterpret_cast<const double2*>(kp.w) + static_cast<int64_t>(c) * kp.n + sp.idx(s));
       const double x = sp.mx(s), y = sp.my(s);
-      re += wr * x - wi * y;
-      im += wr * y + wi * x;
+      re += w.x * x - w.y * y;
+      im += w.x * y + w.y * x;
     }
     ar[base + c] = static_cast<R>(re);
     ai[base + c] = static_cast<R>(im);
@@ -274,8 +245,8 @@ __device__ __forceinline__ void window_chunk(R (&ur)[S], R (&ui)[S], const R (&z
 // pair-sample (sm_100 f32x2 datapath), FADD2 for the per-thread spin sum.
 template <int P, bool FULL, bool LEAD>
 __device__ __forceinline__ void window_chunk_f2(float2 (&U)[P], float2 (&V)[P], const float2 (&ZR)[P],
-                                                const float2 (&ZI)[P], const float2 (&NZI)[P],
-                                                float (&ar)[kChunkSlots], float (&ai)[kChunkSlots], int ck) {
+                                                const float2 (&ZI)[P], float (&ar)[kChunkSlots],
+                                                float (&ai)[kChunkSlots], int ck) {
 #pragma unroll
   for (int j = 0; j < kChunkSlots; ++j) {
     if (!FULL && j >= ck) {
@@ -286,10 +257,11 @@ __device__ __forceinline__ void window_chunk_f2(float2 (&U)[P], float2 (&V)[P], 
 #pragma unroll
       for (int p = 0; p < P; ++p) {
         const float2 a = U[p];
-        const float2 t1 = __fmul2_rn(V[p], NZI[p]);  // -v*zi
-        const float2 t2 = __fmul2_rn(V[p], ZR[p]);   //  v*zr
-        U[p] = __ffma2_rn(a, ZR[p], t1);             // u*zr - v*zi
-        V[p] = __ffma2_rn(a, ZI[p], t2);             // u*zi + v*zr
+        const float2 nzi = make_float2(-ZI[p].x, -ZI[p].y);  // folded into FMUL2's negate modifier
+        const float2 t1 = __fmul2_rn(V[p], nzi);              // -v*zi
+        const float2 t2 = __fmul2_rn(V[p], ZR[p]);            //  v*zr
+        U[p] = __ffma2_rn(a, ZR[p], t1);                      // u*zr - v*zi
+        V[p] = __ffma2_rn(a, ZI[p], t2);                      // u*zi + v*zr
       }
     }
     float2 sr = U[0], si = V[0];
@@ -324,7 +296,6 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
   strip.lane = threadIdx.x & 31;
   strip.row = reinterpret_cast<R*>(kp.partial) +
               (static_cast<int64_t>(blockIdx.x) * nw + (threadIdx.x >> 5)) * kp.part_stride;
-  R* part_row = strip.row;
 
 #pragma unroll
   for (int s = 0; s < S; ++s) {
@@ -354,16 +325,33 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
     }
 
     if (kind == OP_EVENT) {
-      const int flags = __ldg(&op->count), snap = __ldg(&op->aux), cls = __ldg(&op->cls), rc = __ldg(&op->rot);
+      const int flags = __ldg(&op->count), snap = __ldg(&op->aux), cls = __ldg(&op->cls), rc = __ldg(&op->rot),
+                pg = __ldg(&op->prg);
       if (rc >= 0) {  // repeated interval: tabulated propagator
 #pragma unroll
         for (int s = 0; s < S; ++s) {
           if (!sp.act(s)) continue;
-          const RotCoef k = rot_coef(kp, rc, sp.idx(s));
+          const RotCoef k = load_rot(kp, rc, sp.idx(s));
           const double x = sp.mx(s), y = sp.my(s);
           sp.mx(s) = k.cr * x - k.ci * y;
           sp.my(s) = k.cr * y + k.ci * x;
           sp.mz(s) = fma(sp.mz(s), k.a, k.b);
+        }
+      } else if (pg >= 0) {  // one member of an interval progression: C, then C *= q^adv
+        const int adv = __ldg(&op->flags);  // 0 (last member), 1 or 2
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          if (!sp.act(s)) continue;
+          double2* p = reinterpret_cast<double2*>(kp.prog) + (static_cast<int64_t>(pg) * kp.n + sp.idx(s)) * 4;
+          const double2 c = p[0], ab = __ldg(p + 3);
+          const double x = sp.mx(s), y = sp.my(s);
+          sp.mx(s) = c.x * x - c.y * y;
+          sp.my(s) = c.x * y + c.y * x;
+          sp.mz(s) = fma(sp.mz(s), ab.x, ab.y);
+          if (adv) {
+            const double2 q = __ldg(p + adv);  // [1] = q, [2] = q^2
+            p[0] = make_double2(c.x * q.x - c.y * q.y, c.x * q.y + c.y * q.x);
+          }
         }
       } else {
         const double dt = __ldg(&op->p[0]), dmx = __ldg(&op->p[1]), dmy = __ldg(&op->p[2]), dmz = __ldg(&op->p[3]);
@@ -388,7 +376,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
       const double dt = __ldg(&op->p[0]), dmx = __ldg(&op->p[1]), dmy = __ldg(&op->p[2]), dmz = __ldg(&op->p[3]);
       const double* mats = kp.mats + static_cast<int64_t>(m0i) * 9;
       constexpr int G = S < 4 ? S : 4;  // spins per register group
-#pragma unroll
+#pragma unroll 1
       for (int g0 = 0; g0 < S; g0 += G) {
         double x[G], y[G], z[G], zr[G], zi[G], e1[G], rg[G];
 #pragma unroll
@@ -401,24 +389,24 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
           zi[g] = 0.0;
           e1[g] = 1.0;
           rg[g] = 0.0;
-          if (!sp.act(s)) continue;
+          if (!sp.act(s) || !(flags & EV_MOVE)) continue;
           const int64_t i = sp.idx(s);
-          if (flags & EV_MOVE) {
-            double sn, cs;
-            phase_sincos<double>(spin_theta(kp, i, dt, dmx, dmy, dmz), sn, cs);
-            const double e2 = cls >= 0 ? rt_e2(kp, cls, i) : 1.0;
-            zr[g] = e2 * cs;
-            zi[g] = -e2 * sn;
-            if (cls >= 0) {
-              e1[g] = rt_e1(kp, cls, i);
-              rg[g] = kp.m0[i] * (1.0 - e1[g]);
-            }
-          }
+          const SC c = load_sc(kp, i);
+          const double2 e = cls >= 0 ? relax_pair(kp, cls, i) : make_double2(1.0, 1.0);
+          phase_factor(theta_of(c, dt, dmx, dmy, dmz), zr[g], zi[g]);
+          zr[g] *= e.y;
+          zi[g] *= e.y;
+          e1[g] = e.x;
+          rg[g] = c.m0 * (1.0 - e.x);
         }
-        for (int j = 0; j < cnt; ++j) {
-          double r[9];
+        // the pulse matrices are CTA-uniform: prefetch pulse j+1 while applying pulse j
+        double r[9], rn[9];
 #pragma unroll
-          for (int k = 0; k < 9; ++k) r[k] = __ldg(mats + 9 * j + k);
+        for (int k = 0; k < 9; ++k) r[k] = __ldg(mats + k);
+        for (int j = 0; j < cnt; ++j) {
+          const int jn = j + 1 < cnt ? j + 1 : j;
+#pragma unroll
+          for (int k = 0; k < 9; ++k) rn[k] = __ldg(mats + 9 * jn + k);
 #pragma unroll
           for (int g = 0; g < G; ++g) {
             const double nx = r[0] * x[g] + r[1] * y[g] + r[2] * z[g];
@@ -428,6 +416,8 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
             y[g] = nx * zi[g] + ny * zr[g];
             z[g] = fma(nz, e1[g], rg[g]);
           }
+#pragma unroll
+          for (int k = 0; k < 9; ++k) r[k] = rn[k];
         }
 #pragma unroll
         for (int g = 0; g < G; ++g) {
@@ -443,7 +433,6 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
       const int cnt = __ldg(&op->count), g0 = __ldg(&op->aux), s0 = __ldg(&op->s0);
       for (int k0 = 0; k0 < cnt; k0 += kSampPerChunk) {
         const int ck = min(kSampPerChunk, cnt - k0);
-        strip.reserve(ck * NC, part_row);
         R ar[kChunkSlots], ai[kChunkSlots];
 #pragma unroll
         for (int j = 0; j < kSampPerChunk; ++j) {
@@ -471,49 +460,43 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
       const double ddx = __ldg(&op->p[4]), ddy = __ldg(&op->p[5]), ddz = __ldg(&op->p[6]);
       for (int k0 = 0; k0 < cnt; k0 += kSampPerChunk) {
         const int ck = min(kSampPerChunk, cnt - k0);
-        strip.reserve(ck * NC, part_row);
         R ar[kChunkSlots], ai[kChunkSlots];
 #pragma unroll
         for (int j = 0; j < kChunkSlots; ++j) ar[j] = ai[j] = R(0);
-#pragma unroll
+#pragma unroll 1
         for (int s = 0; s < S; ++s) {
           if (!sp.act(s)) continue;
           const int64_t i = sp.idx(s);
+          const SC c = load_sc(kp, i);
+          const double2 e = cls >= 0 ? relax_pair(kp, cls, i) : make_double2(1.0, 1.0);
           // rotation factor of event k0 and the per-event phase step (exact per chunk)
-          const double b = fma(kp.z[i], ddz, fma(kp.y[i], ddy, kp.x[i] * ddx));
-          double sn, cs, qs, qc;
-          phase_sincos<double>(fma(static_cast<double>(k0), b, spin_theta(kp, i, dt, d0x, d0y, d0z)), sn, cs);
-          phase_sincos<double>(b, qs, qc);
-          const double e2 = cls >= 0 ? rt_e2(kp, cls, i) : 1.0;
-          const double e1 = cls >= 0 ? rt_e1(kp, cls, i) : 1.0;
-          const double rgw = kp.m0[i] * (1.0 - e1);
-          double rr = e2 * cs, ri = -e2 * sn;
+          const double b = fma(c.z, ddz, fma(c.y, ddy, c.x * ddx));
+          double rr, ri, qc, qs;
+          phase_factor(fma(static_cast<double>(k0), b, theta_of(c, dt, d0x, d0y, d0z)), rr, ri);
+          phase_factor(b, qc, qs);  // q = exp(-i b) = (qc, qs)
+          rr *= e.y;
+          ri *= e.y;
+          const double rgw = c.m0 * (1.0 - e.x);
           double x = sp.mx(s), y = sp.my(s), z = sp.mz(s);
-          double wr[NC], wi[NC];
+          double2 w[NC];
 #pragma unroll
-          for (int c = 0; c < NC; ++c) {
-            wr[c] = 1.0;
-            wi[c] = 0.0;
-            if (kp.w != nullptr) {
-              const double* p = kp.w + (static_cast<int64_t>(c) * kp.n + i) * 2;
-              wr[c] = p[0];
-              wi[c] = p[1];
-            }
-          }
+          for (int cc = 0; cc < NC; ++cc)
+            w[cc] = kp.w != nullptr ? __ldg(reinterpret_cast<const double2*>(kp.w) + static_cast<int64_t>(cc) * kp.n + i)
+                                    : make_double2(1.0, 0.0);
 #pragma unroll
           for (int j = 0; j < kSampPerChunk; ++j) {
             if (j < ck) {
               const double nx = x * rr - y * ri;
               y = x * ri + y * rr;
               x = nx;
-              if (cls >= 0) z = fma(z, e1, rgw);
+              if (cls >= 0) z = fma(z, e.x, rgw);
               const double a = rr;
-              rr = a * qc + ri * qs;  // r <- r * exp(-i b)
-              ri = ri * qc - a * qs;
+              rr = a * qc - ri * qs;  // r <- r * q
+              ri = a * qs + ri * qc;
 #pragma unroll
-              for (int c = 0; c < NC; ++c) {
-                ar[j * NC + c] += static_cast<R>(wr[c] * x - wi[c] * y);
-                ai[j * NC + c] += static_cast<R>(wr[c] * y + wi[c] * x);
+              for (int cc = 0; cc < NC; ++cc) {
+                ar[j * NC + cc] += static_cast<R>(w[cc].x * x - w[cc].y * y);
+                ai[j * NC + cc] += static_cast<R>(w[cc].x * y + w[cc].y * x);
               }
             }
           }
@@ -529,8 +512,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
     // OP_WINDOW
     {
       const int cnt = __ldg(&op->count), lead = __ldg(&op->aux), s0 = __ldg(&op->s0), rc = __ldg(&op->rot);
-      // per-spin setup from the rotation-class table: sample factor z and the
-      // closed-form exit propagator (C, A, B) of the whole window
+      // per-spin setup: sample factor z and the exit propagator of the whole run
       R zr[S], zi[S], ur[S], ui[S];
 #pragma unroll
       for (int s = 0; s < S; ++s) {
@@ -540,89 +522,79 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
         ui[s] = R(0);
         if (!sp.act(s)) continue;
         const int64_t i = sp.idx(s);
-        double pr = 1.0, pi = 0.0;
         RotCoef k;
         if (rc >= 0) {  // tabulated (pre, window, post) propagators
-          const double* t = rot_ptr(kp, rc, i);
-          pr = __ldg(t);
-          pi = __ldg(t + kp.n);
-          k = rot_coef(kp, rc, i);
-          zr[s] = static_cast<R>(__ldg(t + 6 * kp.n));
-          zi[s] = static_cast<R>(__ldg(t + 7 * kp.n));
+          k = load_rot(kp, rc, i);
         } else {  // on the fly: a window whose interval is not reused
           const int c1 = __ldg(&op->cls), cw = __ldg(&op->flags);
           const double dt = __ldg(&op->p[0]);
-          const double th = spin_theta(kp, i, dt, __ldg(&op->p[1]), __ldg(&op->p[2]), __ldg(&op->p[3]));
-          double sn, cs, SN, CS;
-          sincos(reduce_2pi(th), &sn, &cs);
-          sincos(reduce_2pi(th * static_cast<double>(cnt - lead)), &SN, &CS);
-          const double e2 = c1 >= 0 ? rt_e2(kp, c1, i) : 1.0;
-          const double E2 = cw >= 0 ? rt_e2(kp, cw, i) : 1.0;
-          k.a = cw >= 0 ? rt_e1(kp, cw, i) : 1.0;
-          k.b = kp.m0[i] * (1.0 - k.a);
-          k.cr = E2 * CS;
-          k.ci = -E2 * SN;
-          zr[s] = static_cast<R>(e2 * cs);
-          zi[s] = static_cast<R>(-e2 * sn);
+          const SC c = load_sc(kp, i);
+          const double th = theta_of(c, dt, __ldg(&op->p[1]), __ldg(&op->p[2]), __ldg(&op->p[3]));
+          const double2 e = c1 >= 0 ? relax_pair(kp, c1, i) : make_double2(1.0, 1.0);
+          const double2 E = cw >= 0 ? relax_pair(kp, cw, i) : make_double2(1.0, 1.0);
+          phase_factor(th, k.zr, k.zi);
+          phase_factor(th * static_cast<double>(cnt - lead), k.cr, k.ci);
+          k.zr *= e.y;
+          k.zi *= e.y;
+          k.cr *= E.y;
+          k.ci *= E.y;
+          k.a = E.x;
+          k.b = c.m0 * (1.0 - E.x);
+          k.pr = 1.0;
+          k.pi = 0.0;
         }
-        double w0r = 1.0, w0i = 0.0;
-        if (kp.w != nullptr && NC == 1) {
-          w0r = __ldg(kp.w + 2 * i);
-          w0i = __ldg(kp.w + 2 * i + 1);
-        }
+        zr[s] = static_cast<R>(k.zr);
+        zi[s] = static_cast<R>(k.zi);
+        double2 w0 = make_double2(1.0, 0.0);
+        if (kp.w != nullptr && NC == 1) w0 = __ldg(reinterpret_cast<const double2*>(kp.w) + i);
         const double x = sp.mx(s), y = sp.my(s);
         // state at the first sample: the absorbed pre-interval applied
-        const double x0 = pr * x - pi * y, y0 = pr * y + pi * x;
+        const double x0 = k.pr * x - k.pi * y, y0 = k.pr * y + k.pi * x;
         // NC == 1: track u = w*m (the weight rides along the recurrence); else m
-        ur[s] = static_cast<R>(w0r * x0 - w0i * y0);
-        ui[s] = static_cast<R>(w0r * y0 + w0i * x0);
+        ur[s] = static_cast<R>(w0.x * x0 - w0.y * y0);
+        ui[s] = static_cast<R>(w0.x * y0 + w0.y * x0);
         sp.mx(s) = k.cr * x - k.ci * y;
         sp.my(s) = k.cr * y + k.ci * x;
         sp.mz(s) = fma(sp.mz(s), k.a, k.b);
       }
       if constexpr (kPacked) {
         constexpr int P = S / 2;
-        float2 U[P], V[P], ZR[P], ZI[P], NZI[P];
+        float2 U[P], V[P], ZR[P], ZI[P];
 #pragma unroll
         for (int p = 0; p < P; ++p) {
           ZR[p] = make_float2(zr[2 * p], zr[2 * p + 1]);
           ZI[p] = make_float2(zi[2 * p], zi[2 * p + 1]);
           U[p] = make_float2(ur[2 * p], ur[2 * p + 1]);
           V[p] = make_float2(ui[2 * p], ui[2 * p + 1]);
-          NZI[p] = make_float2(-ZI[p].x, -ZI[p].y);
         }
         int k0 = 0;
         if (lead && cnt >= kChunkSlots) {
-          strip.reserve(kChunkSlots, part_row);
           R ar[kChunkSlots], ai[kChunkSlots];
-          window_chunk_f2<P, true, true>(U, V, ZR, ZI, NZI, ar, ai, kChunkSlots);
+          window_chunk_f2<P, true, true>(U, V, ZR, ZI, ar, ai, kChunkSlots);
           strip.push(ar, ai, kChunkSlots, s0);
           k0 = kChunkSlots;
         }
         // two chunks per trip in one basic block: the warp transpose-reduction of
         // the first (shuffle latency) overlaps the complex multiplies of the second
         for (; k0 + 2 * kChunkSlots <= cnt; k0 += 2 * kChunkSlots) {
-          strip.reserve(2 * kChunkSlots, part_row);
           R ar[kChunkSlots], ai[kChunkSlots], br[kChunkSlots], bi[kChunkSlots];
-          window_chunk_f2<P, true, false>(U, V, ZR, ZI, NZI, ar, ai, kChunkSlots);
-          window_chunk_f2<P, true, false>(U, V, ZR, ZI, NZI, br, bi, kChunkSlots);
+          window_chunk_f2<P, true, false>(U, V, ZR, ZI, ar, ai, kChunkSlots);
+          window_chunk_f2<P, true, false>(U, V, ZR, ZI, br, bi, kChunkSlots);
           strip.push(ar, ai, kChunkSlots, s0 + k0);
           strip.push(br, bi, kChunkSlots, s0 + k0 + kChunkSlots);
         }
         for (; k0 + kChunkSlots <= cnt; k0 += kChunkSlots) {
-          strip.reserve(kChunkSlots, part_row);
           R ar[kChunkSlots], ai[kChunkSlots];
-          window_chunk_f2<P, true, false>(U, V, ZR, ZI, NZI, ar, ai, kChunkSlots);
+          window_chunk_f2<P, true, false>(U, V, ZR, ZI, ar, ai, kChunkSlots);
           strip.push(ar, ai, kChunkSlots, s0 + k0);
         }
         if (k0 < cnt) {
           const int ck = cnt - k0;
-          strip.reserve(ck, part_row);
           R ar[kChunkSlots], ai[kChunkSlots];
           if (lead && k0 == 0)
-            window_chunk_f2<P, false, true>(U, V, ZR, ZI, NZI, ar, ai, ck);
+            window_chunk_f2<P, false, true>(U, V, ZR, ZI, ar, ai, ck);
           else
-            window_chunk_f2<P, false, false>(U, V, ZR, ZI, NZI, ar, ai, ck);
+            window_chunk_f2<P, false, false>(U, V, ZR, ZI, ar, ai, ck);
           strip.push(ar, ai, ck, s0 + k0);
         }
       } else {
@@ -633,29 +605,27 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
           for (int c = 0; c < NC; ++c) {
             wr[c][s] = wi[c][s] = R(0);
             if (NC > 1 && sp.act(s)) {
-              const double* q = kp.w + (static_cast<int64_t>(c) * kp.n + sp.idx(s)) * 2;
-              wr[c][s] = static_cast<R>(q[0]);
-              wi[c][s] = static_cast<R>(q[1]);
+              const double2 w =
+                  __ldg(reinterpret_cast<const double2*>(kp.w) + static_cast<int64_t>(c) * kp.n + sp.idx(s));
+              wr[c][s] = static_cast<R>(w.x);
+              wi[c][s] = static_cast<R>(w.y);
             }
           }
         }
         int k0 = 0;
         if (lead && cnt >= kSampPerChunk) {
-          strip.reserve(kChunkSlots, part_row);
           R ar[kChunkSlots], ai[kChunkSlots];
           window_chunk<R, S, NC, true, true>(ur, ui, zr, zi, wr, wi, ar, ai, kSampPerChunk);
           strip.push(ar, ai, kChunkSlots, s0 * NC);
           k0 = kSampPerChunk;
         }
         for (; k0 + kSampPerChunk <= cnt; k0 += kSampPerChunk) {
-          strip.reserve(kChunkSlots, part_row);
           R ar[kChunkSlots], ai[kChunkSlots];
           window_chunk<R, S, NC, true, false>(ur, ui, zr, zi, wr, wi, ar, ai, kSampPerChunk);
           strip.push(ar, ai, kChunkSlots, (s0 + k0) * NC);
         }
         if (k0 < cnt) {
           const int ck = cnt - k0;
-          strip.reserve(ck * NC, part_row);
           R ar[kChunkSlots], ai[kChunkSlots];
           if (lead && k0 == 0)
             window_chunk<R, S, NC, false, true>(ur, ui, zr, zi, wr, wi, ar, ai, ck);
@@ -669,95 +639,111 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
 }
 
 // ---------------------------------------------------------------------------
-// staging + fold
+// staging, class tables, fold
 // ---------------------------------------------------------------------------
 
-__global__ void prep_kernel(int64_t n, const double* __restrict__ pos, const double* __restrict__ t1,
-                            const double* __restrict__ t2, double* __restrict__ x, double* __restrict__ y,
-                            double* __restrict__ z, double* __restrict__ r1, double* __restrict__ r2) {
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    x[i] = pos[3 * i + 0];
-    y[i] = pos[3 * i + 1];
-    z[i] = pos[3 * i + 2];
-    r1[i] = 1.0 / t1[i];  // engine.py:270 (inf -> 0: no relaxation)
-    r2[i] = 1.0 / t2[i];
+__device__ __forceinline__ int64_t gtid() { return blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; }
+__device__ __forceinline__ int64_t gstride() { return static_cast<int64_t>(gridDim.x) * blockDim.x; }
+
+// SpinConst records from the caller's SoA inputs (engine.py:192-226 fields)
+__global__ void prep_kernel(int64_t n, const double* __restrict__ pos, const double* __restrict__ dw,
+                            const double* __restrict__ m0, const double* __restrict__ t1,
+                            const double* __restrict__ t2, SpinConst* __restrict__ sc) {
+  for (int64_t i = gtid(); i < n; i += gstride()) {
+    SpinConst c;
+    c.x = pos[3 * i + 0];
+    c.y = pos[3 * i + 1];
+    c.z = pos[3 * i + 2];
+    c.dw = dw[i];
+    c.m0 = m0[i];
+    c.r1 = 1.0 / t1[i];  // engine.py:270 (inf -> 0: no relaxation)
+    c.r2 = 1.0 / t2[i];
+    c.pad = 0.0;
+    sc[i] = c;
   }
 }
 
-// relax_cache restated (engine.py:292-299): e1 = exp(-T*inv_t1), e2 = exp(-T*inv_t2)
-__global__ void relax_table_kernel(int64_t n, int n_cls, const double* __restrict__ T, const double* __restrict__ r1,
-                                   const double* __restrict__ r2, double* __restrict__ out) {
+// relax_cache restated (engine.py:292-299): (e1, e2) = (exp(-T*inv_t1), exp(-T*inv_t2))
+__global__ void relax_table_kernel(int64_t n, int n_cls, const double* __restrict__ T,
+                                   const SpinConst* __restrict__ sc, double2* __restrict__ out) {
   const int64_t total = static_cast<int64_t>(n_cls) * n;
-  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  for (int64_t t = gtid(); t < total; t += gstride()) {
     const int64_t c = t / n, i = t - c * n;
-    const double dt = T[c];
-    out[(2 * c) * n + i] = exp(-dt * r1[i]);
-    out[(2 * c + 1) * n + i] = exp(-dt * r2[i]);
+    out[t] = make_double2(exp(-T[c] * sc[i].r1), exp(-T[c] * sc[i].r2));
   }
 }
 
 // rotation-class propagators, fp64 (program.h RotClass): for class c and spin i
-//   theta = pos.dmom + dw*dt; C = e2^m exp(-i m theta); A = e1^m; B = m0 (1 - A);
-//   z = e2 exp(-i theta)
-__global__ void rot_table_kernel(int64_t n, int n_cls, const RotClass* __restrict__ rc, const double* __restrict__ x,
-                                 const double* __restrict__ y, const double* __restrict__ z,
-                                 const double* __restrict__ dw, const double* __restrict__ r1,
-                                 const double* __restrict__ r2, const double* __restrict__ m0,
-                                 double* __restrict__ out) {
+//   Cpre = e2(pre) e^{-i th_pre}; C = e^{-T/T2} e^{-i (th_pre + m th + th_post)};
+//   A = e^{-T/T1}, B = m0 (1 - A); z = e2(main) e^{-i th}
+__global__ void rot_table_kernel(int64_t n, int n_cls, const RotClass* __restrict__ rc,
+                                 const SpinConst* __restrict__ sc, double2* __restrict__ out) {
   const int64_t total = static_cast<int64_t>(n_cls) * n;
-  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  for (int64_t t = gtid(); t < total; t += gstride()) {
     const int64_t c = t / n, i = t - c * n;
     const RotClass& k = rc[c];
-    const double xi = x[i], yi = y[i], zi = z[i], wi = dw[i];
-    auto theta = [&](const double* iv) { return fma(zi, iv[3], fma(yi, iv[2], xi * iv[1])) + wi * iv[0]; };
+    const SpinConst s = sc[i];
+    auto theta = [&](const double* iv) { return fma(s.z, iv[3], fma(s.y, iv[2], s.x * iv[1])) + s.dw * iv[0]; };
     const double th_pre = theta(k.pre), th = theta(k.main), th_post = theta(k.post);
     const double T = k.pre[0] + k.main[0] * k.mult + k.post[0];
-    double sp, cp, s1, c1, st, ct;
-    sincos(reduce_2pi(th_pre), &sp, &cp);
-    sincos(reduce_2pi(th), &s1, &c1);
-    sincos(reduce_2pi(th_pre + th * k.mult + th_post), &st, &ct);
-    const double ep = exp(-k.pre[0] * r2[i]);
-    const double e2 = exp(-k.main[0] * r2[i]);
-    const double E2 = exp(-T * r2[i]);
-    const double E1 = exp(-T * r1[i]);
-    double* o = out + c * kRotFields * n + i;
-    o[0] = ep * cp;
-    o[n] = -ep * sp;
-    o[2 * n] = E2 * ct;
-    o[3 * n] = -E2 * st;
-    o[4 * n] = E1;
-    o[5 * n] = m0[i] * (1.0 - E1);
-    o[6 * n] = e2 * c1;
-    o[7 * n] = -e2 * s1;
+    double pc, ps, c1, s1, tc, ts;
+    phase_factor(th_pre, pc, ps);
+    phase_factor(th, c1, s1);
+    phase_factor(th_pre + th * k.mult + th_post, tc, ts);
+    const double ep = exp(-k.pre[0] * s.r2), e2 = exp(-k.main[0] * s.r2);
+    const double E2 = exp(-T * s.r2), E1 = exp(-T * s.r1);
+    double2* o = out + t * 4;
+    o[0] = make_double2(ep * pc, ep * ps);
+    o[1] = make_double2(E2 * tc, E2 * ts);
+    o[2] = make_double2(E1, s.m0 * (1.0 - E1));
+    o[3] = make_double2(e2 * c1, e2 * s1);
+  }
+}
+
+// progression classes (program.h ProgClass): running factor C0 = e2 e^{-i th_0},
+// step q = e^{-i th_step} (same dt, so no off-resonance term), A = e1, B = m0 (1 - e1)
+__global__ void prog_table_kernel(int64_t n, int n_cls, const ProgClass* __restrict__ pc,
+                                  const SpinConst* __restrict__ sc, double2* __restrict__ out) {
+  const int64_t total = static_cast<int64_t>(n_cls) * n;
+  for (int64_t t = gtid(); t < total; t += gstride()) {
+    const int64_t c = t / n, i = t - c * n;
+    const ProgClass& k = pc[c];
+    const SpinConst s = sc[i];
+    const double th0 = fma(s.z, k.d0[2], fma(s.y, k.d0[1], s.x * k.d0[0])) + s.dw * k.dt;
+    const double thq = fma(s.z, k.step[2], fma(s.y, k.step[1], s.x * k.step[0]));
+    double c0, s0, cq, sq;
+    phase_factor(th0, c0, s0);
+    phase_factor(thq, cq, sq);
+    const double e2 = exp(-k.dt * s.r2), e1 = exp(-k.dt * s.r1);
+    double2* o = out + t * 4;
+    o[0] = make_double2(e2 * c0, e2 * s0);
+    o[1] = make_double2(cq, sq);
+    o[2] = make_double2(cq * cq - sq * sq, 2.0 * cq * sq);  // q^2: a member skipped in the series
+    o[3] = make_double2(e1, s.m0 * (1.0 - e1));
   }
 }
 
 // pad [nc][n][2] weights to [ncp][n][2] (zero coils beyond nc)
 __global__ void pad_weights_kernel(int64_t n, int nc, int ncp, const double* __restrict__ w, double* __restrict__ out) {
   const int64_t total = static_cast<int64_t>(ncp) * n * 2;
-  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  for (int64_t t = gtid(); t < total; t += gstride()) {
     const int64_t c = t / (n * 2);
     out[t] = c < nc ? w[t] : 0.0;
   }
 }
 
 template <typename R>
-__global__ void reduce_partials_kernel(const R* __restrict__ part, int grid, int64_t n_slots, int nc, int ncp,
+__global__ void reduce_partials_kernel(const R* __restrict__ part, int rows, int64_t n_slots, int nc, int ncp,
                                        const int64_t* __restrict__ sample_g, int64_t G, double* __restrict__ out) {
   const int64_t total = n_slots * 2;
-  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  for (int64_t t = gtid(); t < total; t += gstride()) {
     const int64_t sl = t >> 1;
     const int comp = static_cast<int>(t & 1);
     const int64_t s = sl / ncp;
     const int c = static_cast<int>(sl % ncp);
     if (c >= nc) continue;
     double acc = 0.0;
-    for (int b = 0; b < grid; ++b) acc += static_cast<double>(part[static_cast<int64_t>(b) * total + t]);
+    for (int b = 0; b < rows; ++b) acc += static_cast<double>(part[static_cast<int64_t>(b) * total + t]);
     out[(static_cast<int64_t>(c) * G + sample_g[s]) * 2 + comp] = acc;
   }
 }
@@ -768,8 +754,6 @@ __global__ void reduce_partials_kernel(const R* __restrict__ part, int grid, int
 
 template <typename R, int S, int NC>
 size_t integrate_smem_bytes(int threads) {
-  const int nw = threads / 32;
-  (void)nw;
   return static_cast<size_t>(3 * S * threads) * sizeof(double);
 }
 
@@ -787,29 +771,37 @@ cudaError_t launch_integrate(const KParams& kp, int grid, int threads, cudaStrea
 
 static int grid_for(int64_t total, int threads) {
   const int64_t blocks = (total + threads - 1) / threads;
-  return static_cast<int>(blocks < 8192 ? blocks : 8192);
+  return static_cast<int>(blocks < 8192 ? (blocks > 0 ? blocks : 1) : 8192);
 }
 
-cudaError_t launch_prep(int64_t n, const double* pos, const double* t1, const double* t2, double* x, double* y,
-                        double* z, double* r1, double* r2, cudaStream_t stream) {
+cudaError_t launch_prep(int64_t n, const double* pos, const double* dw, const double* m0, const double* t1,
+                        const double* t2, SpinConst* sc, cudaStream_t stream) {
   if (n == 0) return cudaSuccess;
-  prep_kernel<<<grid_for(n, 256), 256, 0, stream>>>(n, pos, t1, t2, x, y, z, r1, r2);
+  prep_kernel<<<grid_for(n, 256), 256, 0, stream>>>(n, pos, dw, m0, t1, t2, sc);
   return cudaGetLastError();
 }
 
-cudaError_t launch_relax_table(int64_t n, int n_cls, const double* T, const double* r1, const double* r2, double* out,
+cudaError_t launch_relax_table(int64_t n, int n_cls, const double* T, const SpinConst* sc, double* out,
                                cudaStream_t stream) {
   if (n == 0 || n_cls == 0) return cudaSuccess;
-  relax_table_kernel<<<grid_for(static_cast<int64_t>(n_cls) * n, 256), 256, 0, stream>>>(n, n_cls, T, r1, r2, out);
+  relax_table_kernel<<<grid_for(static_cast<int64_t>(n_cls) * n, 256), 256, 0, stream>>>(
+      n, n_cls, T, sc, reinterpret_cast<double2*>(out));
   return cudaGetLastError();
 }
 
-cudaError_t launch_rot_table(int64_t n, int n_cls, const RotClass* rc, const double* x, const double* y,
-                             const double* z, const double* dw, const double* r1, const double* r2, const double* m0,
-                             double* out, cudaStream_t stream) {
+cudaError_t launch_rot_table(int64_t n, int n_cls, const RotClass* rc, const SpinConst* sc, double* out,
+                             cudaStream_t stream) {
   if (n == 0 || n_cls == 0) return cudaSuccess;
-  rot_table_kernel<<<grid_for(static_cast<int64_t>(n_cls) * n, 256), 256, 0, stream>>>(n, n_cls, rc, x, y, z, dw, r1,
-                                                                                        r2, m0, out);
+  rot_table_kernel<<<grid_for(static_cast<int64_t>(n_cls) * n, 256), 256, 0, stream>>>(
+      n, n_cls, rc, sc, reinterpret_cast<double2*>(out));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prog_table(int64_t n, int n_cls, const ProgClass* pc, const SpinConst* sc, double* out,
+                              cudaStream_t stream) {
+  if (n == 0 || n_cls == 0) return cudaSuccess;
+  prog_table_kernel<<<grid_for(static_cast<int64_t>(n_cls) * n, 256), 256, 0, stream>>>(
+      n, n_cls, pc, sc, reinterpret_cast<double2*>(out));
   return cudaGetLastError();
 }
 
@@ -821,13 +813,13 @@ cudaError_t launch_pad_weights(int64_t n, int nc, int ncp, const double* w, doub
 }
 
 template <typename R>
-cudaError_t launch_reduce(const R* part, int grid, int64_t n_slots, int nc, int ncp, const int64_t* sample_g,
+cudaError_t launch_reduce(const R* part, int rows, int64_t n_slots, int nc, int ncp, const int64_t* sample_g,
                           int64_t G, double* out, cudaStream_t stream) {
   const int64_t total = n_slots * 2;
   if (total == 0) return cudaSuccess;
   const int64_t blocks = (total + 255) / 256;
   reduce_partials_kernel<R><<<static_cast<int>(blocks < 65535 ? blocks : 65535), 256, 0, stream>>>(
-      part, grid, n_slots, nc, ncp, sample_g, G, out);
+      part, rows, n_slots, nc, ncp, sample_g, G, out);
   return cudaGetLastError();
 }
 

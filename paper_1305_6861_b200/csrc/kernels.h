@@ -7,22 +7,29 @@
 
 namespace bloch {
 
+// per-spin constants, one 64-byte record (4 x 16-byte loads)
+struct alignas(16) SpinConst {
+  double x, y, z, dw;  // position (m), off-resonance (rad/s)
+  double m0, r1, r2;   // equilibrium magnetisation, 1/T1, 1/T2
+  double pad;
+};
+
 struct KParams {
   const DevOp* ops;
   int32_t n_ops;
   int32_t spins_per_cta;  // S * blockDim.x
   const GEv* gev;
-  const double* mats;  // OP_RFTRAIN matrices, 9 per pair
-  int64_t n;  // spins
-  const double *x, *y, *z, *dw;  // positions (m), off-resonance (rad/s)
-  const double *r1, *r2, *m0;    // 1/T1, 1/T2, equilibrium magnetisation
+  const double* mats;            // OP_RFTRAIN matrices, 9 per pair
+  int64_t n;                     // spins
+  const SpinConst* sc;           // [n]
   const double *mx0, *my0, *mz0; // initial state (SpinBlock.mx/my/mz)
   const double* w;               // [NC][n][2] complex weights, or nullptr = 1+0j
-  void* partial;                 // [grid][part_stride] of R
+  void* partial;                 // [warps of the grid][part_stride] of R
   int64_t part_stride;           // n_samples * NC * 2
   double* snaps;                 // [n_snap][n][3] or nullptr
-  const double* relax;           // [n_cls][2][n]: exp(-T_c/T1_i), exp(-T_c/T2_i)
-  const double* rot;             // [n_rot][8][n]: rotation-class propagators (rot_table_kernel)
+  const double* relax;           // [n_relax][n][2]: exp(-T_c/T1_i), exp(-T_c/T2_i)
+  const double* rot;             // [n_rot][n][8]: rotation-class propagators (rot_table_kernel)
+  double* prog;                  // [n_prog][n][8]: progression running factors (updated in place)
 };
 
 // Launch shape per variant: max threads per CTA and min resident CTAs per SM
@@ -57,14 +64,14 @@ template <typename R, int S, int NC>
 cudaError_t kernel_attrs(int* max_threads, int* regs);
 template <typename R, int S, int NC>
 size_t integrate_smem_bytes(int threads);
-cudaError_t launch_rot_table(int64_t n, int n_cls, const RotClass* rc, const double* x, const double* y,
-                             const double* z, const double* dw, const double* r1, const double* r2, const double* m0,
-                             double* out, cudaStream_t stream);
-cudaError_t launch_relax_table(int64_t n, int n_cls, const double* T, const double* r1, const double* r2, double* out,
+cudaError_t launch_prep(int64_t n, const double* pos, const double* dw, const double* m0, const double* t1,
+                        const double* t2, SpinConst* sc, cudaStream_t stream);
+cudaError_t launch_relax_table(int64_t n, int n_cls, const double* T, const SpinConst* sc, double* out,
                                cudaStream_t stream);
-
-cudaError_t launch_prep(int64_t n, const double* pos, const double* t1, const double* t2, double* x,
-                        double* y, double* z, double* r1, double* r2, cudaStream_t stream);
+cudaError_t launch_rot_table(int64_t n, int n_cls, const RotClass* rc, const SpinConst* sc, double* out,
+                             cudaStream_t stream);
+cudaError_t launch_prog_table(int64_t n, int n_cls, const ProgClass* pc, const SpinConst* sc, double* out,
+                              cudaStream_t stream);
 cudaError_t launch_pad_weights(int64_t n, int nc, int ncp, const double* w, double* out,
                                cudaStream_t stream);
 template <typename R>

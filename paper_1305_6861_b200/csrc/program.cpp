@@ -50,6 +50,7 @@ inline bool same_interval(double dt_a, const double* a, double dt_b, const doubl
 }  // namespace
 
 void fuse_intervals(Program& prog, const std::function<int32_t(double)>& relax_class);
+void find_progressions(Program& prog);
 
 void compile_program(const TablesView& t, Program& prog) {
   prog = Program();
@@ -414,6 +415,7 @@ void fuse_intervals(Program& prog, const std::function<int32_t(double)>& relax_c
   for (size_t k = 0; k < n_items; ++k) {
     if (absorbed[k]) continue;
     DevOp op = items[k].op;
+    op.prg = -1;
     if (op.kind == OP_WINDOW && !items[k].interval) {
       const RotKey key = win_key(k, pre_of[k], post_of[k]);
       auto f = rot_ids.find(key);
@@ -443,6 +445,102 @@ void fuse_intervals(Program& prog, const std::function<int32_t(double)>& relax_c
     out.push_back(op);
   }
   prog.ops.swap(out);
+  find_progressions(prog);
+}
+
+// Progression classes for the intervals left on the fly (program.h ProgClass).
+// Within each group of equal dt (op order), members are partitioned greedily
+// into arithmetic series d_j = d_prev + m*step, m in {1, 2}; a 1-member series
+// takes a second member only if the series it would start continues later in
+// the group (lookahead), so interleaved series (TSE blip-in / blip-out) split
+// correctly.  Series of >= 3 members become classes (at most kMaxProg).
+void find_progressions(Program& prog) {
+  constexpr size_t kMaxProg = 32;
+  constexpr int kLook = 6;
+  std::map<double, std::vector<size_t>> groups;
+  for (size_t k = 0; k < prog.ops.size(); ++k) {
+    const DevOp& op = prog.ops[k];
+    if (op.kind == OP_EVENT && op.rot < 0 && (op.count & EV_MOVE)) groups[op.p[0]].push_back(k);
+  }
+  auto close = [](const double* a, const double* b) {
+    const double mag = std::max(inf_norm(a), inf_norm(b));
+    for (int c = 0; c < 3; ++c)
+      if (std::fabs(a[c] - b[c]) > 1e-9 * mag) return false;
+    return true;
+  };
+  for (auto& g : groups) {
+    const std::vector<size_t>& mem = g.second;
+    if (mem.size() < 3) continue;
+    struct Series {
+      std::vector<size_t> idx;
+      std::vector<int> mult;  // multiple of step from the previous member
+      double step[3];
+      bool has_step = false;
+    };
+    std::vector<Series> ser;
+    auto dm = [&](size_t k) { return prog.ops[k].p + 1; };
+    for (size_t a = 0; a < mem.size(); ++a) {
+      const double* x = dm(mem[a]);
+      bool placed = false;
+      for (Series& s : ser) {  // continue a series with a known step
+        if (!s.has_step) continue;
+        const double* last = dm(s.idx.back());
+        for (int m = 1; m <= 2 && !placed; ++m) {
+          double pred[3];
+          for (int c = 0; c < 3; ++c) pred[c] = last[c] + m * s.step[c];
+          if (close(x, pred)) {
+            s.idx.push_back(mem[a]);
+            s.mult.push_back(m);
+            placed = true;
+          }
+        }
+        if (placed) break;
+      }
+      for (size_t si = 0; si < ser.size() && !placed; ++si) {  // second member of a 1-member series?
+        Series& s = ser[si];
+        if (s.has_step) continue;
+        const double* last = dm(s.idx.back());
+        double step[3], pred[3];
+        for (int c = 0; c < 3; ++c) {
+          step[c] = x[c] - last[c];
+          pred[c] = x[c] + step[c];
+        }
+        if (inf_norm(step) == 0.0) continue;
+        bool continues = false;
+        for (size_t b = a + 1; b < mem.size() && b <= a + kLook && !continues; ++b) continues = close(dm(mem[b]), pred);
+        if (continues) {
+          s.idx.push_back(mem[a]);
+          s.mult.push_back(1);
+          for (int c = 0; c < 3; ++c) s.step[c] = step[c];
+          s.has_step = true;
+          placed = true;
+        }
+      }
+      if (!placed) {
+        Series s;
+        s.idx.push_back(mem[a]);
+        s.mult.push_back(0);
+        ser.push_back(s);
+      }
+    }
+    for (const Series& s : ser) {
+      if (s.idx.size() < 3 || prog.prog_classes.size() >= kMaxProg) continue;
+      ProgClass pc{};
+      pc.dt = g.first;
+      for (int c = 0; c < 3; ++c) {
+        pc.d0[c] = dm(s.idx[0])[c];
+        pc.step[c] = s.step[c];
+      }
+      const int32_t id = static_cast<int32_t>(prog.prog_classes.size());
+      prog.prog_classes.push_back(pc);
+      for (size_t j = 0; j < s.idx.size(); ++j) {
+        DevOp& op = prog.ops[s.idx[j]];
+        op.prg = id;
+        op.flags = j + 1 < s.idx.size() ? s.mult[j + 1] : 0;  // advance to the next member: C *= q^m
+      }
+      prog.n_prog_intervals += static_cast<int64_t>(s.idx.size());
+    }
+  }
 }
 
 }  // namespace bloch

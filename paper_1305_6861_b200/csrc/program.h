@@ -51,8 +51,9 @@ struct alignas(16) DevOp {
                   // CHIRP: dt, dmom_0 (3), dd (3)
   int32_t flags;  // RFTRAIN: EV_* flags of the shared interval
   int32_t cls;    // relax class of dt (EVENT/CHIRP/RFTRAIN on-the-fly path), -1 = no relaxation
-  int32_t rot;    // rotation class (EVENT: repeated interval; WINDOW: always), -1 = none
-  int32_t pad[7];
+  int32_t rot;    // rotation class (EVENT: repeated interval; WINDOW: reused run), -1 = none
+  int32_t prg;    // EVENT: progression class (interval of an arithmetic series of moments), -1 = none
+  int32_t pad[6];
 };
 
 // A rotation class: pre, then `mult` times main, then post (intervals (dt,
@@ -70,6 +71,16 @@ struct alignas(16) RotClass {
 };
 static_assert(sizeof(RotClass) == 128, "RotClass must be 128 bytes");
 static_assert(sizeof(DevOp) == 128, "DevOp must be 128 bytes");
+
+// A progression class: intervals of equal dt whose moments form an arithmetic
+// series in op order, dmom_j = d0 + j*step (phase-encode lobes, blips).  Per
+// spin the factor of occurrence j is C0 q^j: one complex multiply per
+// occurrence instead of a sincos.
+struct alignas(16) ProgClass {
+  double dt, d0[3], step[3];
+  double pad;
+};
+static_assert(sizeof(ProgClass) == 64, "ProgClass must be 64 bytes");
 
 struct alignas(16) GEv {  // one generic sampled interval
   double dt, dmx, dmy, dmz;

@@ -28,12 +28,13 @@ struct Program {
   std::vector<int64_t> sample_g;  // compact sample -> acq * max_samples + index
   std::vector<double> relax_t;    // interval length of every relax class
   std::vector<RotClass> rot_classes;
+  std::vector<ProgClass> prog_classes;
   int32_t n_acq = 0, max_samples = 0, n_snap = 0;
   int64_t n_events = 0;  // reference table size incl. pulses
   int64_t n_samples = 0;
   int64_t n_rot = 0, n_interval = 0, n_window_ops = 0, n_window_samples = 0, n_gsamp_events = 0;
   int64_t n_chirp_ops = 0, n_chirp_samples = 0, n_train_ops = 0, n_train_pairs = 0;
-  int64_t n_fused_windows = 0, n_fused_intervals = 0;
+  int64_t n_fused_windows = 0, n_fused_intervals = 0, n_prog_intervals = 0;
 };
 
 // Throws std::invalid_argument on malformed tables.
