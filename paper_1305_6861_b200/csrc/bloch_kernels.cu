@@ -103,11 +103,15 @@ struct Strip {
     const int j = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
     if ((lane & 3) == 0 && j < cnt) {
       R* p = row + static_cast<int64_t>(first_id + j) * 2;
-      p[0] = re[0];
-      p[1] = im[0];
+      __stcs(p, re[0]);  // streaming: the partial rows must not evict the class tables from L2
+      __stcs(p + 1, im[0]);
     }
   }
 };
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+}
 
 // ---------------------------------------------------------------------------
 // spin state (shared memory, [3][S][blockDim] fp64) and per-spin constants
@@ -327,30 +331,53 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
     if (kind == OP_EVENT) {
       const int flags = __ldg(&op->count), snap = __ldg(&op->aux), cls = __ldg(&op->cls), rc = __ldg(&op->rot),
                 pg = __ldg(&op->prg);
+      // Two-phase per group of G spins: issue every table load of the group
+      // before any store, so the L2 round trips overlap instead of serialising
+      // behind possibly-aliasing shared/global stores.
+      constexpr int G = S < 2 ? S : 2;
       if (rc >= 0) {  // repeated interval: tabulated propagator
+        const double2* tb = reinterpret_cast<const double2*>(kp.rot) + static_cast<int64_t>(rc) * kp.n * 4;
 #pragma unroll
-        for (int s = 0; s < S; ++s) {
-          if (!sp.act(s)) continue;
-          const RotCoef k = load_rot(kp, rc, sp.idx(s));
-          const double x = sp.mx(s), y = sp.my(s);
-          sp.mx(s) = k.cr * x - k.ci * y;
-          sp.my(s) = k.cr * y + k.ci * x;
-          sp.mz(s) = fma(sp.mz(s), k.a, k.b);
+        for (int g0 = 0; g0 < S; g0 += G) {
+          double2 c[G], ab[G];
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const int64_t i = sp.act(g0 + g) ? sp.idx(g0 + g) : 0;
+            c[g] = __ldg(tb + i * 4 + 1);
+            ab[g] = __ldg(tb + i * 4 + 2);
+          }
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const int s = g0 + g;
+            const double x = sp.mx(s), y = sp.my(s);
+            sp.mx(s) = c[g].x * x - c[g].y * y;
+            sp.my(s) = c[g].x * y + c[g].y * x;
+            sp.mz(s) = fma(sp.mz(s), ab[g].x, ab[g].y);
+          }
         }
       } else if (pg >= 0) {  // one member of an interval progression: C, then C *= q^adv
         const int adv = __ldg(&op->flags);  // 0 (last member), 1 or 2
+        double2* tb = reinterpret_cast<double2*>(kp.prog) + static_cast<int64_t>(pg) * kp.n * 4;
 #pragma unroll
-        for (int s = 0; s < S; ++s) {
-          if (!sp.act(s)) continue;
-          double2* p = reinterpret_cast<double2*>(kp.prog) + (static_cast<int64_t>(pg) * kp.n + sp.idx(s)) * 4;
-          const double2 c = p[0], ab = __ldg(p + 3);
-          const double x = sp.mx(s), y = sp.my(s);
-          sp.mx(s) = c.x * x - c.y * y;
-          sp.my(s) = c.x * y + c.y * x;
-          sp.mz(s) = fma(sp.mz(s), ab.x, ab.y);
-          if (adv) {
-            const double2 q = __ldg(p + adv);  // [1] = q, [2] = q^2
-            p[0] = make_double2(c.x * q.x - c.y * q.y, c.x * q.y + c.y * q.x);
+        for (int g0 = 0; g0 < S; g0 += G) {
+          double2 c[G], ab[G], q[G];
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const int64_t i = sp.act(g0 + g) ? sp.idx(g0 + g) : 0;
+            c[g] = __ldcg(tb + i * 4);  // running factor: L2-coherent (rewritten below)
+            ab[g] = __ldg(tb + i * 4 + 3);
+            q[g] = adv ? __ldg(tb + i * 4 + adv) : make_double2(1.0, 0.0);  // [1] = q, [2] = q^2
+          }
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const int s = g0 + g;
+            const double x = sp.mx(s), y = sp.my(s);
+            sp.mx(s) = c[g].x * x - c[g].y * y;
+            sp.my(s) = c[g].x * y + c[g].y * x;
+            sp.mz(s) = fma(sp.mz(s), ab[g].x, ab[g].y);
+            if (adv && sp.act(s))
+              __stcg(tb + sp.idx(s) * 4, make_double2(c[g].x * q[g].x - c[g].y * q[g].y,
+                                                      c[g].x * q[g].y + c[g].y * q[g].x));
           }
         }
       } else {
@@ -512,6 +539,24 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
     // OP_WINDOW
     {
       const int cnt = __ldg(&op->count), lead = __ldg(&op->aux), s0 = __ldg(&op->s0), rc = __ldg(&op->rot);
+      // The sample loop below is long and touches no memory but its partial row:
+      // pull the per-spin records of the ops up to the next window into L2 now.
+      for (int o2 = o + 1; o2 < kp.n_ops && o2 <= o + 8; ++o2) {
+        const DevOp* nx = kp.ops + o2;
+        const int k2 = __ldg(&nx->kind);
+        const int r2 = __ldg(&nx->rot), g2 = __ldg(&nx->prg);
+        const double* base = nullptr;
+        if ((k2 == OP_EVENT || k2 == OP_WINDOW) && r2 >= 0)
+          base = kp.rot + static_cast<int64_t>(r2) * kp.n * 8;
+        else if (k2 == OP_EVENT && g2 >= 0)
+          base = kp.prog + static_cast<int64_t>(g2) * kp.n * 8;
+        if (base != nullptr) {
+#pragma unroll
+          for (int s = 0; s < S; ++s)
+            if (sp.act(s)) prefetch_l2(base + sp.idx(s) * 8);
+        }
+        if (k2 == OP_WINDOW) break;
+      }
       // per-spin setup: sample factor z and the exit propagator of the whole run
       R zr[S], zi[S], ur[S], ui[S];
 #pragma unroll
