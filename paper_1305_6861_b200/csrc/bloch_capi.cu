@@ -97,8 +97,8 @@ Variant pick_variant(int prec, int64_t n, int ncp, int n_sm) {
     switch (ncp) {
       case 1: return {32, n >= int64_t(n_sm) * 8 * 64 ? 8 : 2, 1};
       case 2: return {32, 4, 2};
-      case 4: return {32, 2, 4};
-      default: return {32, 2, 8};
+      case 4: return {32, 4, 4};
+      default: return {32, 4, 8};
     }
   }
   switch (ncp) {

@@ -279,6 +279,57 @@ __device__ __forceinline__ void window_chunk_f2(float2 (&U)[P], float2 (&V)[P], 
   }
 }
 
+// fp32, NC coils (even): track m per spin (scalar complex multiply) and
+// multiply-accumulate the coil weights packed two coils per FFMA2:
+//   (re_c, re_c+1) += (wr_c, wr_c+1) ur - (wi_c, wi_c+1) ui
+//   (im_c, im_c+1) += (wr_c, wr_c+1) ui + (wi_c, wi_c+1) ur
+template <int S, int NC, bool FULL, bool LEAD>
+__device__ __forceinline__ void window_chunk_mc2(float (&ur)[S], float (&ui)[S], const float (&zr)[S],
+                                                 const float (&zi)[S], const float2 (&WR)[NC / 2][S],
+                                                 const float2 (&WI)[NC / 2][S], float (&ar)[kChunkSlots],
+                                                 float (&ai)[kChunkSlots], int ck) {
+  constexpr int kSamp = kChunkSlots / NC;
+  constexpr int PC = NC / 2;
+#pragma unroll
+  for (int j = 0; j < kSamp; ++j) {
+    if (!FULL && j >= ck) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) ar[j * NC + c] = ai[j * NC + c] = 0.f;
+      continue;
+    }
+    if (!(LEAD && j == 0)) {
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const float x = ur[s], y = ui[s];
+        ur[s] = x * zr[s] - y * zi[s];
+        ui[s] = x * zi[s] + y * zr[s];
+      }
+    }
+    float2 re[PC], im[PC];
+#pragma unroll
+    for (int p = 0; p < PC; ++p) re[p] = im[p] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const float2 u2 = make_float2(ur[s], ur[s]), v2 = make_float2(ui[s], ui[s]);
+      const float2 nv2 = make_float2(-ui[s], -ui[s]);
+#pragma unroll
+      for (int p = 0; p < PC; ++p) {
+        re[p] = __ffma2_rn(WR[p][s], u2, re[p]);
+        re[p] = __ffma2_rn(WI[p][s], nv2, re[p]);
+        im[p] = __ffma2_rn(WR[p][s], v2, im[p]);
+        im[p] = __ffma2_rn(WI[p][s], u2, im[p]);
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < PC; ++p) {
+      ar[j * NC + 2 * p] = re[p].x;
+      ar[j * NC + 2 * p + 1] = re[p].y;
+      ai[j * NC + 2 * p] = im[p].x;
+      ai[j * NC + 2 * p + 1] = im[p].y;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // the integrator
 // ---------------------------------------------------------------------------
@@ -641,6 +692,44 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
           else
             window_chunk_f2<P, false, false>(U, V, ZR, ZI, ar, ai, ck);
           strip.push(ar, ai, ck, s0 + k0);
+        }
+      } else if constexpr (sizeof(R) == 4 && NC >= 2) {
+        constexpr int PC = NC / 2;
+        float2 WR[PC][S], WI[PC][S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+#pragma unroll
+          for (int p = 0; p < PC; ++p) {
+            WR[p][s] = WI[p][s] = make_float2(0.f, 0.f);
+            if (sp.act(s)) {
+              const double2* wp = reinterpret_cast<const double2*>(kp.w) + sp.idx(s);
+              const double2 a = __ldg(wp + static_cast<int64_t>(2 * p) * kp.n);
+              const double2 b = __ldg(wp + static_cast<int64_t>(2 * p + 1) * kp.n);
+              WR[p][s] = make_float2(static_cast<float>(a.x), static_cast<float>(b.x));
+              WI[p][s] = make_float2(static_cast<float>(a.y), static_cast<float>(b.y));
+            }
+          }
+        }
+        int k0 = 0;
+        if (lead && cnt >= kSampPerChunk) {
+          R ar[kChunkSlots], ai[kChunkSlots];
+          window_chunk_mc2<S, NC, true, true>(ur, ui, zr, zi, WR, WI, ar, ai, kSampPerChunk);
+          strip.push(ar, ai, kChunkSlots, s0 * NC);
+          k0 = kSampPerChunk;
+        }
+        for (; k0 + kSampPerChunk <= cnt; k0 += kSampPerChunk) {
+          R ar[kChunkSlots], ai[kChunkSlots];
+          window_chunk_mc2<S, NC, true, false>(ur, ui, zr, zi, WR, WI, ar, ai, kSampPerChunk);
+          strip.push(ar, ai, kChunkSlots, (s0 + k0) * NC);
+        }
+        if (k0 < cnt) {
+          const int ck = cnt - k0;
+          R ar[kChunkSlots], ai[kChunkSlots];
+          if (lead && k0 == 0)
+            window_chunk_mc2<S, NC, false, true>(ur, ui, zr, zi, WR, WI, ar, ai, ck);
+          else
+            window_chunk_mc2<S, NC, false, false>(ur, ui, zr, zi, WR, WI, ar, ai, ck);
+          strip.push(ar, ai, ck * NC, (s0 + k0) * NC);
         }
       } else {
         R wr[NC][S], wi[NC][S];
