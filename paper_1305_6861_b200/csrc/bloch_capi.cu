@@ -77,10 +77,10 @@ struct bloch_ctx {
   bloch::Program prog;
   bool has_prog = false;
   std::vector<uint8_t> snap_present;
-  DevBuf d_ops, d_gev, d_mats, d_sample_g, d_relax_t, d_rot_cls, d_prog_cls;
+  DevBuf d_ops, d_gev, d_mats, d_sample_g, d_relax_t, d_rot_cls, d_prog_cls, d_chirp_cls;
   DevBuf in_pos, in_mx, in_my, in_mz, in_t1, in_t2, in_m0, in_dw, in_w;
   DevBuf sc, wpad;
-  DevBuf partial, echo, snaps, relax, rot, progtab;
+  DevBuf partial, echo, snaps, relax, rot, progtab, chirptab;
   float kernel_ms = 0.f, device_ms = 0.f;
   int launches = 0;
 };
@@ -226,7 +226,7 @@ int bloch_destroy(bloch_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (DevBuf* b : {&c->d_ops, &c->d_gev, &c->d_mats, &c->d_sample_g, &c->d_relax_t, &c->relax, &c->d_rot_cls, &c->rot, &c->in_pos, &c->in_mx, &c->in_my, &c->in_mz,
                     &c->in_t1, &c->in_t2, &c->in_m0, &c->in_dw, &c->in_w, &c->sc, &c->wpad, &c->partial,
-                    &c->echo, &c->snaps, &c->d_prog_cls, &c->progtab})
+                    &c->echo, &c->snaps, &c->d_prog_cls, &c->progtab, &c->d_chirp_cls, &c->chirptab})
     b->release();
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
@@ -278,6 +278,8 @@ int bloch_set_tables(bloch_ctx* c, int32_t n_es, const int64_t* es_ev_offset,
       upload(c->d_relax_t, prog.relax_t.data(), prog.relax_t.size() * sizeof(double), c->stream);
       upload(c->d_rot_cls, prog.rot_classes.data(), prog.rot_classes.size() * sizeof(bloch::RotClass), c->stream);
       upload(c->d_prog_cls, prog.prog_classes.data(), prog.prog_classes.size() * sizeof(bloch::ProgClass),
+             c->stream);
+      upload(c->d_chirp_cls, prog.chirp_classes.data(), prog.chirp_classes.size() * sizeof(bloch::ChirpClass),
              c->stream);
       upload(c->d_sample_g, prog.sample_g.data(), prog.sample_g.size() * sizeof(int64_t), c->stream);
       ck(cudaStreamSynchronize(c->stream), "set_tables sync");
@@ -405,6 +407,14 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
            "progression table kernel");
         c->launches++;
       }
+      const int n_chirp = static_cast<int>(P.chirp_classes.size());
+      if (n_chirp > 0) {
+        c->chirptab.ensure(8 * nd * n_chirp);
+        ck(bloch::launch_chirp_table(n, n_chirp, c->d_chirp_cls.as<bloch::ChirpClass>(), d_sc,
+                                     c->chirptab.as<double>(), st),
+           "chirp table kernel");
+        c->launches++;
+      }
       if (d_w && ncp != n_coils) {
         c->wpad.ensure(2 * nd * ncp);
         ck(bloch::launch_pad_weights(n, n_coils, ncp, d_w, c->wpad.as<double>(), st), "pad kernel");
@@ -458,6 +468,7 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       kp.relax = c->relax.as<double>();
       kp.rot = c->rot.as<double>();
       kp.prog = c->progtab.as<double>();
+      kp.chirp = c->chirptab.as<double>();
       ck(cudaEventRecord(c->ev[1], st), "event");
       ck(dispatch(v, kp, static_cast<int>(grid), static_cast<int>(threads), st), "integrate kernel");
       ck(cudaEventRecord(c->ev[2], st), "event");

@@ -532,7 +532,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
     }
 
     if (kind == OP_CHIRP) {  // linear-increment sampled run: geometric rotation factors, fp64
-      const int cnt = __ldg(&op->count), s0 = __ldg(&op->s0), cls = __ldg(&op->cls);
+      const int cnt = __ldg(&op->count), s0 = __ldg(&op->s0), cls = __ldg(&op->cls), crc = __ldg(&op->rot);
       const double dt = __ldg(&op->p[0]);
       const double d0x = __ldg(&op->p[1]), d0y = __ldg(&op->p[2]), d0z = __ldg(&op->p[3]);
       const double ddx = __ldg(&op->p[4]), ddy = __ldg(&op->p[5]), ddz = __ldg(&op->p[6]);
@@ -545,16 +545,36 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
         for (int s = 0; s < S; ++s) {
           if (!sp.act(s)) continue;
           const int64_t i = sp.idx(s);
-          const SC c = load_sc(kp, i);
-          const double2 e = cls >= 0 ? relax_pair(kp, cls, i) : make_double2(1.0, 1.0);
-          // rotation factor of event k0 and the per-event phase step (exact per chunk)
-          const double b = fma(c.z, ddz, fma(c.y, ddy, c.x * ddx));
-          double rr, ri, qc, qs;
-          phase_factor(fma(static_cast<double>(k0), b, theta_of(c, dt, d0x, d0y, d0z)), rr, ri);
-          phase_factor(b, qc, qs);  // q = exp(-i b) = (qc, qs)
-          rr *= e.y;
-          ri *= e.y;
-          const double rgw = c.m0 * (1.0 - e.x);
+          double rr, ri, qc, qs, e1, rgw;
+          if (crc >= 0) {  // tabulated chirp class: r0, q, q^8, (A, B)
+            const double2* tb = reinterpret_cast<const double2*>(kp.chirp) + (static_cast<int64_t>(crc) * kp.n + i) * 4;
+            const double2 r0 = __ldg(tb), q = __ldg(tb + 1), ab = __ldg(tb + 3);
+            rr = r0.x;
+            ri = r0.y;
+            if (k0 > 0) {  // advance to event k0 (chirps are a few chunks long)
+              const double2 q8 = __ldg(tb + 2);
+              for (int a8 = 0; a8 < k0; a8 += kChunkSlots) {
+                const double a = rr;
+                rr = a * q8.x - ri * q8.y;
+                ri = a * q8.y + ri * q8.x;
+              }
+            }
+            qc = q.x;
+            qs = q.y;
+            e1 = ab.x;
+            rgw = ab.y;
+          } else {
+            const SC c = load_sc(kp, i);
+            const double2 e = cls >= 0 ? relax_pair(kp, cls, i) : make_double2(1.0, 1.0);
+            // rotation factor of event k0 and the per-event phase step (exact per chunk)
+            const double b = fma(c.z, ddz, fma(c.y, ddy, c.x * ddx));
+            phase_factor(fma(static_cast<double>(k0), b, theta_of(c, dt, d0x, d0y, d0z)), rr, ri);
+            phase_factor(b, qc, qs);  // q = exp(-i b) = (qc, qs)
+            rr *= e.y;
+            ri *= e.y;
+            e1 = e.x;
+            rgw = c.m0 * (1.0 - e.x);
+          }
           double x = sp.mx(s), y = sp.my(s), z = sp.mz(s);
           double2 w[NC];
 #pragma unroll
@@ -567,7 +587,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
               const double nx = x * rr - y * ri;
               y = x * ri + y * rr;
               x = nx;
-              if (cls >= 0) z = fma(z, e.x, rgw);
+              z = fma(z, e1, rgw);  // e1 = 1, rgw = 0 without relaxation
               const double a = rr;
               rr = a * qc - ri * qs;  // r <- r * q
               ri = a * qs + ri * qc;
@@ -599,6 +619,8 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
         const double* base = nullptr;
         if ((k2 == OP_EVENT || k2 == OP_WINDOW) && r2 >= 0)
           base = kp.rot + static_cast<int64_t>(r2) * kp.n * 8;
+        else if (k2 == OP_CHIRP && r2 >= 0)
+          base = kp.chirp + static_cast<int64_t>(r2) * kp.n * 8;
         else if (k2 == OP_EVENT && g2 >= 0)
           base = kp.prog + static_cast<int64_t>(g2) * kp.n * 8;
         if (base != nullptr) {
@@ -857,6 +879,30 @@ __global__ void prog_table_kernel(int64_t n, int n_cls, const ProgClass* __restr
   }
 }
 
+// chirp classes (program.h ChirpClass): r0 = e2 e^{-i th_0}, q = e^{-i th_dd},
+// q^8 = one chunk of kChunkSlots events ahead, (A, B) = (e1, m0 (1 - e1))
+__global__ void chirp_table_kernel(int64_t n, int n_cls, const ChirpClass* __restrict__ cc,
+                                   const SpinConst* __restrict__ sc, double2* __restrict__ out) {
+  const int64_t total = static_cast<int64_t>(n_cls) * n;
+  for (int64_t t = gtid(); t < total; t += gstride()) {
+    const int64_t c = t / n, i = t - c * n;
+    const ChirpClass& k = cc[c];
+    const SpinConst s = sc[i];
+    const double th0 = fma(s.z, k.d0[2], fma(s.y, k.d0[1], s.x * k.d0[0])) + s.dw * k.dt;
+    const double thq = fma(s.z, k.dd[2], fma(s.y, k.dd[1], s.x * k.dd[0]));
+    double c0, s0, cq, sq, c8, s8;
+    phase_factor(th0, c0, s0);
+    phase_factor(thq, cq, sq);
+    phase_factor(thq * static_cast<double>(kChunkSlots), c8, s8);
+    const double e2 = exp(-k.dt * s.r2), e1 = exp(-k.dt * s.r1);
+    double2* o = out + t * 4;
+    o[0] = make_double2(e2 * c0, e2 * s0);
+    o[1] = make_double2(cq, sq);
+    o[2] = make_double2(c8, s8);
+    o[3] = make_double2(e1, s.m0 * (1.0 - e1));
+  }
+}
+
 // pad [nc][n][2] weights to [ncp][n][2] (zero coils beyond nc)
 __global__ void pad_weights_kernel(int64_t n, int nc, int ncp, const double* __restrict__ w, double* __restrict__ out) {
   const int64_t total = static_cast<int64_t>(ncp) * n * 2;
@@ -936,6 +982,14 @@ cudaError_t launch_prog_table(int64_t n, int n_cls, const ProgClass* pc, const S
   if (n == 0 || n_cls == 0) return cudaSuccess;
   prog_table_kernel<<<grid_for(static_cast<int64_t>(n_cls) * n, 256), 256, 0, stream>>>(
       n, n_cls, pc, sc, reinterpret_cast<double2*>(out));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_chirp_table(int64_t n, int n_cls, const ChirpClass* cc, const SpinConst* sc, double* out,
+                               cudaStream_t stream) {
+  if (n == 0 || n_cls == 0) return cudaSuccess;
+  chirp_table_kernel<<<grid_for(static_cast<int64_t>(n_cls) * n, 256), 256, 0, stream>>>(
+      n, n_cls, cc, sc, reinterpret_cast<double2*>(out));
   return cudaGetLastError();
 }
 

@@ -30,6 +30,7 @@ struct KParams {
   const double* relax;           // [n_relax][n][2]: exp(-T_c/T1_i), exp(-T_c/T2_i)
   const double* rot;             // [n_rot][n][8]: rotation-class propagators (rot_table_kernel)
   double* prog;                  // [n_prog][n][8]: progression running factors (updated in place)
+  const double* chirp;           // [n_chirp][n][8]: chirp-class factors (chirp_table_kernel)
 };
 
 // Launch shape per variant: max threads per CTA and min resident CTAs per SM
@@ -72,6 +73,8 @@ cudaError_t launch_rot_table(int64_t n, int n_cls, const RotClass* rc, const Spi
                              cudaStream_t stream);
 cudaError_t launch_prog_table(int64_t n, int n_cls, const ProgClass* pc, const SpinConst* sc, double* out,
                               cudaStream_t stream);
+cudaError_t launch_chirp_table(int64_t n, int n_cls, const ChirpClass* cc, const SpinConst* sc, double* out,
+                               cudaStream_t stream);
 cudaError_t launch_pad_weights(int64_t n, int nc, int ncp, const double* w, double* out,
                                cudaStream_t stream);
 template <typename R>

@@ -51,6 +51,7 @@ inline bool same_interval(double dt_a, const double* a, double dt_b, const doubl
 
 void fuse_intervals(Program& prog, const std::function<int32_t(double)>& relax_class);
 void find_progressions(Program& prog);
+void find_chirp_classes(Program& prog);
 
 void compile_program(const TablesView& t, Program& prog) {
   prog = Program();
@@ -446,6 +447,38 @@ void fuse_intervals(Program& prog, const std::function<int32_t(double)>& relax_c
   }
   prog.ops.swap(out);
   find_progressions(prog);
+  find_chirp_classes(prog);
+}
+
+// Chirp classes (program.h ChirpClass): a ramp that recurs (every EPI line) is
+// tabulated once per spin; OP_CHIRP.rot then indexes the chirp table.
+void find_chirp_classes(Program& prog) {
+  constexpr size_t kMaxChirp = 16;
+  using Key = std::array<double, 7>;
+  std::map<Key, int64_t> uses;
+  auto key_of = [](const DevOp& op) { return Key{op.p[0], op.p[1], op.p[2], op.p[3], op.p[4], op.p[5], op.p[6]}; };
+  for (const DevOp& op : prog.ops)
+    if (op.kind == OP_CHIRP) uses[key_of(op)]++;
+  std::map<Key, int32_t> ids;
+  for (DevOp& op : prog.ops) {
+    if (op.kind != OP_CHIRP) continue;
+    const Key k = key_of(op);
+    op.rot = -1;
+    if (uses[k] < 2) continue;
+    auto f = ids.find(k);
+    if (f == ids.end()) {
+      if (prog.chirp_classes.size() >= kMaxChirp) continue;
+      ChirpClass cc{};
+      cc.dt = k[0];
+      for (int a = 0; a < 3; ++a) {
+        cc.d0[a] = k[1 + a];
+        cc.dd[a] = k[4 + a];
+      }
+      f = ids.emplace(k, static_cast<int32_t>(prog.chirp_classes.size())).first;
+      prog.chirp_classes.push_back(cc);
+    }
+    op.rot = f->second;
+  }
 }
 
 // Progression classes for the intervals left on the fly (program.h ProgClass).

@@ -82,6 +82,15 @@ struct alignas(16) ProgClass {
 };
 static_assert(sizeof(ProgClass) == 64, "ProgClass must be 64 bytes");
 
+// A chirp class: a reused OP_CHIRP run (trapezoid ramp under the ADC): dt and
+// the increments dmom_k = d0 + k*dd.  Per spin the table holds
+//   r0 = e2 exp(-i th_0), q = exp(-i th_dd), q^8 (one chunk ahead), A = e1, B = m0 (1 - e1).
+struct alignas(16) ChirpClass {
+  double dt, d0[3], dd[3];
+  double pad;
+};
+static_assert(sizeof(ChirpClass) == 64, "ChirpClass must be 64 bytes");
+
 struct alignas(16) GEv {  // one generic sampled interval
   double dt, dmx, dmy, dmz;
   int32_t flags;

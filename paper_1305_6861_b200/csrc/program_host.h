@@ -29,6 +29,7 @@ struct Program {
   std::vector<double> relax_t;    // interval length of every relax class
   std::vector<RotClass> rot_classes;
   std::vector<ProgClass> prog_classes;
+  std::vector<ChirpClass> chirp_classes;
   int32_t n_acq = 0, max_samples = 0, n_snap = 0;
   int64_t n_events = 0;  // reference table size incl. pulses
   int64_t n_samples = 0;
