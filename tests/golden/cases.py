@@ -120,6 +120,8 @@ def small_cases():
                         snapshot_times=(0.0, 1e-3, t_sample, 4.4e-3, mixed.end_time))
     out["mixed_coils"] = dict(sequence=mixed, spins=_spins(120, rng, dw_sigma=300.0, n_coils=3),
                               snapshot_times=(mixed.end_time,))
+    out["tse_2coil"] = dict(sequence=build_tse(0.5, 16, 4, 0.03, 0.8, readout_gradient(0.5, 16, 0.01)),
+                            spins=_spins(333, rng, n_coils=2), snapshot_times=(0.4,))
     return out
 
 

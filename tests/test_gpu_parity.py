@@ -24,7 +24,7 @@ from paper_1305_6861_b200 import SpinBlock, compute_block, precompute_sequence_t
 
 pytestmark = pytest.mark.gpu
 
-SMALL = ["fid", "pair", "se16_box", "tse16", "epi16", "cpmg8", "mixed", "mixed_coils"]
+SMALL = ["fid", "pair", "se16_box", "tse16", "epi16", "cpmg8", "mixed", "mixed_coils", "tse_2coil"]
 CONFIGS = ["cfg0", "cfg1", "cfg2", "cfg3", "cfg4"]
 
 KSPACE_TOL = {32: 1e-4, 64: 1e-11}

@@ -22,7 +22,7 @@ from oracle import bloch_oracle as O
 from paper_1305_6861_b200 import configs, flatten_tables, precompute_sequence_tables
 from paper_1305_6861_b200.phantom import rasterize_arrays
 
-SMALL = ["fid", "pair", "se16_box", "tse16", "epi16", "cpmg8", "mixed", "mixed_coils"]
+SMALL = ["fid", "pair", "se16_box", "tse16", "epi16", "cpmg8", "mixed", "mixed_coils", "tse_2coil"]
 CONFIGS = ["cfg0", "cfg1", "cfg2", "cfg3", "cfg4"]
 
 
