@@ -42,8 +42,8 @@ struct KernelTraits {
 };
 template <>
 struct KernelTraits<float, 8, 1> {  // the fp32 single-coil workhorse: 2 CTAs x 10 warps per SM
-  static constexpr int kMaxThreads = 320;
-  static constexpr int kMinBlocks = 2;
+  static constexpr int kMaxThreads = 320;   // measured: 1 x 16 warps 17.6 ms, 2 x 10 warps 14.1 ms,
+  static constexpr int kMinBlocks = 2;      // 3 x 8 warps (80 regs, spills) 15.5 ms on config 1
 };
 
 // (real type, spins per thread, coils) instantiated in bloch_kernels.cu
