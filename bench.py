@@ -185,7 +185,7 @@ def main():
         w = configs.make(args.config)
         tables = precompute_sequence_tables(w.sequence)
         E = event_counts(tables)["events"]
-        cb = cpu_sample(w, tables, E, max(64, args.cpu_spins_per_core // 2), steps=args.steps,
+        cb = cpu_sample(w, tables, E, args.cpu_spins_per_core, steps=args.steps,
                         warmup=args.warmup, quiet=args.quiet)
         line = {
             "metric": metric, "value": cb["value"], "unit": cb["unit"], "impl": "reference", "n_gpus": args.gpus,

@@ -29,7 +29,18 @@ from .engine import (
     run,
     simulate_spin,
 )
-from .errors import DeviceError, InvalidParameter, MrSimError, SpinBudgetExceeded, TimingInfeasible, WorkerPanic
+from .errors import (
+    DeviceError,
+    FitDiverged,
+    InvalidParameter,
+    MrSimError,
+    ParseError,
+    SpinBudgetExceeded,
+    TimingInfeasible,
+    TrajectoryMismatch,
+    WorkerPanic,
+)
+from .recon import ImageVolume, KSpaceMatrix, assemble_kspace, cpmg_fit, reconstruct
 from .phantom import Phantom, PhantomBox, SpinSample, rasterize, rasterize_arrays
 from .sequence import (
     AcquisitionSpec,

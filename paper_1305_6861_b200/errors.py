@@ -21,6 +21,18 @@ class TimingInfeasible(MrSimError):
     """A sequence builder was asked for intervals that come out negative."""
 
 
+class ParseError(MrSimError):
+    """A file or description violates its format (errors.py:16-27)."""
+
+
+class TrajectoryMismatch(MrSimError):
+    """Echo records and trajectory metadata disagree in shape (errors.py:49-50)."""
+
+
+class FitDiverged(MrSimError):
+    """A relaxometry fit failed to converge (errors.py:53-54)."""
+
+
 class SpinBudgetExceeded(MrSimError):
     """Rasterization would produce more spins than the configured cap."""
 
