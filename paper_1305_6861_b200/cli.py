@@ -53,6 +53,8 @@ def _cmd_simulate(args) -> int:
     timing = eng.last_timing()
     stats = eng.program_stats()
     echoes = echoes / n  # engine.py:507
+    if echoes.ndim == 2:  # single receive weight: (n_acq, max_ns)
+        echoes = echoes[None]
     n_coils = echoes.shape[0]
     ns = [t.size for t in tables.acq_times]
     os.makedirs(args.out, exist_ok=True)
