@@ -128,6 +128,75 @@ int bloch_compute_block(bloch_ctx* ctx, int64_t n, const double* pos, const doub
                         const double* weight, int32_t n_coils, double* echoes_out,
                         double* snaps_out, uint8_t* snap_present, uint32_t flags);
 
+/*
+ * Device-side object model — replaces the host
+ * rasterisation feeding compute_block: phantom.rasterize (phantom.py:98-142),
+ * the per-spin fold of engine.build_spin_arrays (engine.py:192-226) with
+ * system.spin_off_resonance (system.py:123-132) and complex_weight
+ * (system.py:203-211).  Spins are produced directly in device memory in the
+ * reference's order (box, then z, y, x with x fastest; sites whose M0 is zero
+ * emit no spin), ready for bloch_compute_block(..., BLOCH_IN_DEVICE).
+ *
+ * Tissue of a box: the constants m0/t1/t2/dw, overridden inside each of its
+ * shapes [shape_begin, shape_begin+shape_count) — later shapes win (label
+ * maps; the seeded ellipse phantoms of the benchmark configs).  A shape is an
+ * ellipse (ax[2] <= 0: z ignored) or ellipsoid rotated by angle a in the
+ * x-y plane; a site is inside when u^2 + v^2 (+ w^2) <= 1 with
+ * u = (dx cos a + dy sin a)/ax[0], v = (-dx sin a + dy cos a)/ax[1], w = dz/ax[2].
+ */
+typedef struct {
+  double base[3];    /* first lattice site per axis: origin + (size - (n-1)*spacing)/2 */
+  double step[3];    /* lattice spacing per axis (m); site k sits at base + step*k */
+  int64_t count[3];  /* lattice sites per axis (phantom._lattice) */
+  double m0, t1, t2, dw; /* background tissue of the box */
+  int32_t shape_begin, shape_count;
+} bloch_box_t;
+
+typedef struct {
+  double c[3], ax[3];  /* centre and semi-axes (m) */
+  double cos_a, sin_a; /* in-plane rotation */
+  double m0, t1, t2, dw;
+} bloch_shape_t;
+
+/* Off-resonance map added to the tissue dw (rad/s), evaluated per spin:
+ *   dw += const_dw
+ *       + poly_scale * sum_k coef_k * (x/s)^px_k * (y/s)^py_k * (z/s)^pz_k
+ *       + sum_j amp_j * exp(-|r - c_j|^2 / (2 sigma_j^2))     (bumps; 2-D when c_j[2] is NaN)
+ * poly_peak > 0 rescales the polynomial so its peak |value| over the emitted
+ * spins equals poly_peak (poly_scale is then ignored). */
+typedef struct {
+  double const_dw;
+  int32_t n_poly, n_bumps;
+  const double* poly;  /* n_poly x 4: coef, px, py, pz */
+  double poly_len;     /* s */
+  double poly_scale, poly_peak;
+  const double* bumps; /* n_bumps x 5: cx, cy, cz, sigma, amp */
+} bloch_field_t;
+
+/* Receive coils: n_coils Gaussian coils (centre, sigma, azimuth phase), or
+ * n_coils = 0 for the uniform sensitivity S (weight S + 0j). */
+typedef struct {
+  double c[3], sigma, cos_p, sin_p;
+} bloch_coil_t;
+
+/*
+ * Rasterise onto `ctx`'s device and stream.  Outputs are device pointers with
+ * room for `capacity` spins (the lattice site total bounds the spin count):
+ * pos capacity*3, mx/my/mz/t1/t2/m0/domega capacity each, weight
+ * max(n_coils,1)*capacity*2 doubles.  The first *n_out entries are written,
+ * weight as [coil][spin] interleaved complex with coil stride *n_out — the
+ * layout bloch_compute_block reads.  Host pointers (poly, bumps, boxes,
+ * shapes, coils) are read during the call only.  The call synchronises the
+ * stream once (to learn the spin count).  BLOCH_E_INVALID when the sites
+ * exceed `capacity` or an emitted tissue value is invalid (m0 < 0,
+ * T1/T2 <= 0), as phantom.rasterize / RelaxationParams reject them.
+ */
+int bloch_rasterize(bloch_ctx* ctx, const bloch_box_t* boxes, int32_t n_boxes,
+                    const bloch_shape_t* shapes, int32_t n_shapes, const bloch_field_t* field,
+                    const bloch_coil_t* coils, int32_t n_coils, double uniform_s, int64_t capacity,
+                    double* pos, double* mx, double* my, double* mz, double* t1, double* t2,
+                    double* m0, double* domega, double* weight, int64_t* n_out);
+
 /* Device time (ms, CUDA events on the context stream) of the last
  * bloch_compute_block: the integrator kernel alone, and all device work of the
  * call (staging kernels + integrator + reduction). */

@@ -24,6 +24,32 @@ BLOCH_IN_DEVICE = 1
 BLOCH_OUT_DEVICE = 2
 BLOCH_NO_SYNC = 4
 
+
+class BoxT(ctypes.Structure):
+    """bloch_box_t"""
+    _fields_ = [("base", c_double * 3), ("step", c_double * 3), ("count", c_int64 * 3), ("m0", c_double),
+                ("t1", c_double), ("t2", c_double), ("dw", c_double), ("shape_begin", c_int32),
+                ("shape_count", c_int32)]
+
+
+class ShapeT(ctypes.Structure):
+    """bloch_shape_t"""
+    _fields_ = [("c", c_double * 3), ("ax", c_double * 3), ("cos_a", c_double), ("sin_a", c_double),
+                ("m0", c_double), ("t1", c_double), ("t2", c_double), ("dw", c_double)]
+
+
+class FieldT(ctypes.Structure):
+    """bloch_field_t"""
+    _fields_ = [("const_dw", c_double), ("n_poly", c_int32), ("n_bumps", c_int32), ("poly", POINTER(c_double)),
+                ("poly_len", c_double), ("poly_scale", c_double), ("poly_peak", c_double),
+                ("bumps", POINTER(c_double))]
+
+
+class CoilT(ctypes.Structure):
+    """bloch_coil_t"""
+    _fields_ = [("c", c_double * 3), ("sigma", c_double), ("cos_p", c_double), ("sin_p", c_double)]
+
+
 # every symbol the header declares, with (restype, argtypes)
 _PD = POINTER(c_double)
 SIGNATURES = {
@@ -52,6 +78,11 @@ SIGNATURES = {
          POINTER(c_uint8), c_uint32],
     ),
     "bloch_last_timing": (c_int, [c_void_p, POINTER(c_float), POINTER(c_float), POINTER(c_int32)]),
+    "bloch_rasterize": (
+        c_int,
+        [c_void_p, POINTER(BoxT), c_int32, POINTER(ShapeT), c_int32, POINTER(FieldT), POINTER(CoilT), c_int32,
+         c_double, c_int64, _PD, _PD, _PD, _PD, _PD, _PD, _PD, _PD, _PD, POINTER(c_int64)],
+    ),
 }
 
 _lib = None

@@ -155,13 +155,43 @@ def _plane(pixels: int, iso: int, ell: _Ellipses) -> Dict[str, np.ndarray]:
 # ---------------------------------------------------------------------------
 
 
+def config_sequence(index: int, rf=None) -> Sequence:
+    """The sequence of config `index` (config 2 draws its refocusing jitter from the RF stream)."""
+    if index in (0, 1):
+        n, te, tr = (64, 0.020, 0.500) if index == 0 else (256, 0.030, 0.800)
+        return build_spin_echo(FOV, n, te=te, tr=tr, readout_grad=readout_gradient(FOV, n, (n - 1) * 10e-6),
+                               refocus_phi=math.pi / 2.0)
+    if index == 2:
+        if rf is None:
+            rf = list(_streams(2))[3]
+        n, tf = 512, 16
+        jitter = rf.uniform(-5.0, 5.0, (n // tf, tf))
+        return build_tse(FOV, n, tf, 0.010, tr=2.0, readout_grad=readout_gradient(FOV, n, (n - 1) * 10e-6),
+                         refocus_alpha=lambda s, e: math.radians(160.0 + jitter[s, e]))
+    if index == 3:
+        return epi_trapezoid_sequence()
+    if index == 4:
+        return multipulse_3d_sequence()
+    raise KeyError(index)
+
+
+def _ring_coils(coil_rng, n_coils: int):
+    """Gaussian coils on a ring of radius 0.5 FOV with a small seeded azimuth jitter."""
+    ring = 0.5 * FOV
+    jitter = coil_rng.uniform(-0.05, 0.05, n_coils)
+    coils = []
+    for c in range(n_coils):
+        phi = 2.0 * math.pi * c / n_coils + jitter[c]
+        coils.append(GaussianCoil(center=(ring * math.cos(phi), ring * math.sin(phi), 0.0), sigma=0.4 * FOV,
+                                  phase=phi))
+    return coils
+
+
 def config0() -> Workload:
     geo, tissue, _dw, _rf, _coil = _streams(0)
     ell = _Ellipses(geo, tissue)
     spins = _plane(64, 1, ell)
-    n = 64
-    seq = build_spin_echo(FOV, n, te=0.020, tr=0.500, readout_grad=readout_gradient(FOV, n, (n - 1) * 10e-6),
-                          refocus_phi=math.pi / 2.0)
+    seq = config_sequence(0)
     blk = _block(spins, np.zeros(spins["m0"].size), np.full(spins["m0"].size, 1.0 + 0.0j))
     return Workload(0, "cfg0_se64", seq, blk, {"fov": FOV, "grid": [64, 64], "iso": 1, "te": 0.02, "tr": 0.5,
                                                  "dwell": 10e-6})
@@ -171,9 +201,7 @@ def config1() -> Workload:
     geo, tissue, dwr, _rf, _coil = _streams(1)
     ell = _Ellipses(geo, tissue)
     spins = _plane(256, 4, ell)
-    n = 256
-    seq = build_spin_echo(FOV, n, te=0.030, tr=0.800, readout_grad=readout_gradient(FOV, n, (n - 1) * 10e-6),
-                          refocus_phi=math.pi / 2.0)
+    seq = config_sequence(1)
     dw = dwr.normal(0.0, 2.0 * math.pi * 20.0, spins["m0"].size)
     blk = _block(spins, dw, np.full(spins["m0"].size, 1.0 + 0.0j))
     return Workload(1, "cfg1_se256_iso4", seq, blk, {"fov": FOV, "grid": [256, 256], "iso": 4, "te": 0.03,
@@ -185,9 +213,7 @@ def config2() -> Workload:
     ell = _Ellipses(geo, tissue)
     spins = _plane(512, 2, ell)
     n, tf = 512, 16
-    jitter = rf.uniform(-5.0, 5.0, (n // tf, tf))
-    seq = build_tse(FOV, n, tf, 0.010, tr=2.0, readout_grad=readout_gradient(FOV, n, (n - 1) * 10e-6),
-                    refocus_alpha=lambda s, e: math.radians(160.0 + jitter[s, e]))
+    seq = config_sequence(2, rf)
     # smooth cubic 2-D polynomial B0 map, peak +-2pi*100 rad/s over the lattice
     coef = dwr.normal(0.0, 1.0, 10)
     u = spins["pos"][:, 0] / (FOV / 2)
@@ -235,7 +261,7 @@ def config3() -> Workload:
     geo, tissue, dwr, _rf, _coil = _streams(3)
     ell = _Ellipses(geo, tissue, t2_range=(0.02, 0.12))
     spins = _plane(128, 8, ell)
-    seq = epi_trapezoid_sequence()
+    seq = config_sequence(3)
     c = dwr.uniform(-0.4, 0.4, (5, 2)) * FOV
     sig = dwr.uniform(0.05, 0.15, 5) * FOV
     amp = np.where(dwr.uniform(0.0, 1.0, 5) < 0.5, -1.0, 1.0) * 2.0 * math.pi * 150.0
@@ -309,14 +335,8 @@ def config4(n_coils: int = 8) -> Workload:
     spacing = FOV / 128
     ph = ell.phantom(origin=(-FOV / 2, -FOV / 2, -FOV / 4), size=(FOV, FOV, FOV / 2))
     spins = rasterize_arrays(ph, (spacing, spacing, spacing), cap=4_000_000)
-    seq = multipulse_3d_sequence()
-    ring = 0.5 * FOV
-    jitter = coil.uniform(-0.05, 0.05, n_coils)  # small seeded azimuth jitter of the ring positions
-    coils = []
-    for c in range(n_coils):
-        phi = 2.0 * math.pi * c / n_coils + jitter[c]
-        coils.append(GaussianCoil(center=(ring * math.cos(phi), ring * math.sin(phi), 0.0), sigma=0.4 * FOV,
-                                  phase=phi))
+    seq = config_sequence(4)
+    coils = _ring_coils(coil, n_coils)
     w = np.stack([complex_weight(cc, spins["pos"]) for cc in coils]) if spins["m0"].size else np.zeros((n_coils, 0))
     blk = _block(spins, np.zeros(spins["m0"].size), w)
     return Workload(4, "cfg4_3d_multipulse_8coil", seq, blk,
@@ -329,3 +349,98 @@ BUILDERS = {0: config0, 1: config1, 2: config2, 3: config3, 4: config4}
 
 def make(index: int) -> Workload:
     return BUILDERS[int(index)]()
+
+
+# ---------------------------------------------------------------------------
+# the same workloads as device scenes (objects.DeviceScene)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class SceneWorkload:
+    """A config whose spins are rasterised on the GPU (objects.rasterize_device)."""
+
+    index: int
+    name: str
+    sequence: Sequence
+    scene: object
+    spacing: tuple
+    extra_dw: Optional[object] = None  # n -> (n,) host array added per spin (random maps), or None
+    cap: int = 4_000_000
+
+    def rasterize(self, engine=None):
+        from .objects import rasterize_device
+
+        if self.extra_dw is None:
+            return rasterize_device(self.scene, self.spacing, engine, cap=self.cap)
+        # the count is only known after the lattice pass: rasterise, then add the per-spin map
+        spins = rasterize_device(self.scene, self.spacing, engine, cap=self.cap)
+        import torch
+
+        spins.domega += torch.from_numpy(self.extra_dw(spins.n)).to(spins.domega.device)
+        torch.cuda.current_stream(spins.domega.device).synchronize()
+        return spins
+
+
+def _label_box(ell: "_Ellipses", origin, size):
+    from .objects import Ellipse, LabelBox
+
+    shapes = []
+    for k in range(ell.pd.size):
+        shapes.append(Ellipse(center=tuple(ell.c[k]), axes=tuple(ell.ax[k]), angle=float(ell.ang[k]),
+                              m0=float(ell.pd[k]), t1=float(ell.t1[k]), t2=float(ell.t2[k])))
+    return LabelBox(origin=origin, size=size, m0=0.0, t1=1.0, t2=0.1, shapes=tuple(shapes))
+
+
+def _plane_scene(pixels, iso, ell, **kw):
+    from .objects import DeviceScene
+
+    spacing = FOV / (pixels * iso)
+    box = _label_box(ell, (-FOV / 2, -FOV / 2, -spacing / 2), (FOV, FOV, spacing))
+    return DeviceScene([box], **kw), (spacing, spacing, spacing)
+
+
+def scene(index: int) -> SceneWorkload:
+    """Config `index` as a device scene: same seeded streams, same spins as make(index)."""
+    from .objects import GaussianBumps, PolynomialField
+
+    index = int(index)
+    geo, tissue, dwr, rf, coil = _streams(index)
+    if index == 0:
+        ell = _Ellipses(geo, tissue)
+        sc, sp = _plane_scene(64, 1, ell)
+        return SceneWorkload(0, "cfg0_se64", config_sequence(0), sc, sp)
+    if index == 1:
+        ell = _Ellipses(geo, tissue)
+        sc, sp = _plane_scene(256, 4, ell)
+        return SceneWorkload(1, "cfg1_se256_iso4", config_sequence(1), sc, sp,
+                             extra_dw=lambda n: dwr.normal(0.0, 2.0 * math.pi * 20.0, n))
+    if index == 2:
+        ell = _Ellipses(geo, tissue)
+        seq = config_sequence(2, rf)
+        coef = dwr.normal(0.0, 1.0, 10)
+        expo = ((0, 0, 0), (1, 0, 0), (0, 1, 0), (2, 0, 0), (1, 1, 0), (0, 2, 0), (3, 0, 0), (2, 1, 0), (1, 2, 0),
+                (0, 3, 0))
+        poly = PolynomialField(coef=tuple(float(c) for c in coef), exponents=expo, length=FOV / 2,
+                               peak=2.0 * math.pi * 100.0)
+        sc, sp = _plane_scene(512, 2, ell, polynomial=poly)
+        return SceneWorkload(2, "cfg2_tse512_iso2", seq, sc, sp)
+    if index == 3:
+        ell = _Ellipses(geo, tissue, t2_range=(0.02, 0.12))
+        c = dwr.uniform(-0.4, 0.4, (5, 2)) * FOV
+        sig = dwr.uniform(0.05, 0.15, 5) * FOV
+        amp = np.where(dwr.uniform(0.0, 1.0, 5) < 0.5, -1.0, 1.0) * 2.0 * math.pi * 150.0
+        bumps = GaussianBumps(centers=tuple(tuple(map(float, ck)) for ck in c), sigmas=tuple(map(float, sig)),
+                              amps=tuple(map(float, amp)))
+        sc, sp = _plane_scene(128, 8, ell, bumps=bumps)
+        return SceneWorkload(3, "cfg3_epi128_iso8", config_sequence(3), sc, sp)
+    if index == 4:
+        from .objects import DeviceScene
+
+        ext = (FOV, FOV, FOV / 2)
+        ell = _Ellipses(geo, tissue, dim=3, extent=ext)
+        spacing = FOV / 128
+        box = _label_box(ell, (-FOV / 2, -FOV / 2, -FOV / 4), (FOV, FOV, FOV / 2))
+        sc = DeviceScene([box], receive=CoilArray(_ring_coils(coil, 8)))
+        return SceneWorkload(4, "cfg4_3d_multipulse_8coil", config_sequence(4), sc, (spacing,) * 3)
+    raise KeyError(index)

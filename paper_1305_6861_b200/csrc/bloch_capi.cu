@@ -13,6 +13,7 @@
 #include "../../include/bloch_b200.h"
 #include "kernels.h"
 #include "program_host.h"
+#include "raster.h"
 
 #ifndef BLOCH_VERSION_STRING
 #define BLOCH_VERSION_STRING "bloch_b200 0.1.0 (sm_100a)"
@@ -82,6 +83,8 @@ struct bloch_ctx {
   DevBuf in_pos, in_mx, in_my, in_mz, in_t1, in_t2, in_m0, in_dw, in_w;
   DevBuf sc, wpad;
   DevBuf partial, echo, snaps, relax, rot, progtab, chirptab;
+  DevBuf raster_scratch;
+  std::vector<unsigned char> raster_staging;
   float kernel_ms = 0.f, device_ms = 0.f;
   int launches = 0;
 };
@@ -227,7 +230,8 @@ int bloch_destroy(bloch_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (DevBuf* b : {&c->d_ops, &c->d_gev, &c->d_mats, &c->d_sample_g, &c->d_relax_t, &c->relax, &c->d_rot_cls, &c->rot, &c->in_pos, &c->in_mx, &c->in_my, &c->in_mz,
                     &c->in_t1, &c->in_t2, &c->in_m0, &c->in_dw, &c->in_w, &c->sc, &c->wpad, &c->partial,
-                    &c->echo, &c->snaps, &c->d_prog_cls, &c->progtab, &c->d_chirp_cls, &c->chirptab})
+                    &c->echo, &c->snaps, &c->d_prog_cls, &c->progtab, &c->d_chirp_cls, &c->chirptab,
+                    &c->raster_scratch})
     b->release();
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
@@ -505,6 +509,78 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       for (int32_t i = 0; i < P.n_snap; ++i) snap_present[i] = c->snap_present[i];
   } catch (const InvalidArg& ex) {
     return fail(BLOCH_E_INVALID, ex.what());
+  } catch (const std::exception& ex) {
+    return fail(BLOCH_E_CUDA, ex.what());
+  }
+  return BLOCH_OK;
+}
+
+int bloch_rasterize(bloch_ctx* c, const bloch_box_t* boxes, int32_t n_boxes, const bloch_shape_t* shapes,
+                    int32_t n_shapes, const bloch_field_t* field, const bloch_coil_t* coils, int32_t n_coils,
+                    double uniform_s, int64_t capacity, double* pos, double* mx, double* my, double* mz,
+                    double* t1, double* t2, double* m0, double* domega, double* weight, int64_t* n_out) {
+  if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
+  if (c->device == BLOCH_HOST_ONLY) return fail(BLOCH_E_STATE, "host-only context cannot rasterize");
+  if (!n_out) return fail(BLOCH_E_INVALID, "n_out is NULL");
+  *n_out = 0;
+  if (n_boxes < 1 || n_boxes > bloch::kMaxRasterBoxes || !boxes)
+    return fail(BLOCH_E_INVALID, "need 1.." + std::to_string(bloch::kMaxRasterBoxes) + " boxes");
+  if (n_shapes < 0 || n_shapes > bloch::kMaxShapes || (n_shapes && !shapes))
+    return fail(BLOCH_E_INVALID, "shape count out of range");
+  if (n_coils < 0 || n_coils > 8 || (n_coils && !coils)) return fail(BLOCH_E_INVALID, "n_coils must be in [0, 8]");
+  bloch_field_t f{};
+  if (field) f = *field;
+  if (f.n_poly < 0 || f.n_poly > bloch::kMaxPoly || (f.n_poly && !f.poly) || f.n_bumps < 0 ||
+      f.n_bumps > bloch::kMaxBumps || (f.n_bumps && !f.bumps))
+    return fail(BLOCH_E_INVALID, "field model out of range");
+  if (f.n_poly && !(f.poly_len > 0.0)) return fail(BLOCH_E_INVALID, "poly_len must be > 0");
+  for (int k = 0; k < f.n_poly; ++k)
+    for (int j = 1; j < 4; ++j) {
+      const double e = f.poly[4 * k + j];
+      if (!(e >= 0.0 && e <= 16.0 && e == (double)(int)e))
+        return fail(BLOCH_E_INVALID, "polynomial exponents must be integers in [0, 16]");
+    }
+  int64_t sites = 0;
+  for (int b = 0; b < n_boxes; ++b) {
+    const bloch_box_t& bx = boxes[b];
+    if (bx.shape_count < 0 || bx.shape_begin < 0 || bx.shape_begin + bx.shape_count > n_shapes)
+      return fail(BLOCH_E_INVALID, "box " + std::to_string(b) + " shape range outside the shape table");
+    int64_t cnt = 1;
+    for (int a = 0; a < 3; ++a) {
+      if (bx.count[a] < 1) return fail(BLOCH_E_INVALID, "box lattice counts must be >= 1");
+      cnt *= bx.count[a];
+    }
+    sites += cnt;
+  }
+  if (sites > capacity)
+    return fail(BLOCH_E_INVALID, std::to_string(sites) + " lattice sites exceed the capacity of " +
+                                     std::to_string(capacity));
+  if (sites >= (int64_t)INT32_MAX) return fail(BLOCH_E_INVALID, "more than 2^31 lattice sites");
+  if (sites > 0 && (!pos || !mx || !my || !mz || !t1 || !t2 || !m0 || !domega || !weight))
+    return fail(BLOCH_E_INVALID, "NULL output array");
+  try {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    const size_t need = bloch::raster_scratch_bytes(sites);
+    c->raster_scratch.ensure(need);
+    c->raster_staging.resize(bloch::raster_staging_bytes());
+    bloch::RasterArgs a{};
+    a.boxes = boxes;
+    a.n_boxes = n_boxes;
+    a.shapes = shapes;
+    a.n_shapes = n_shapes;
+    a.field = f;
+    a.coils = coils;
+    a.n_coils = n_coils;
+    a.uniform_s = uniform_s;
+    a.capacity = capacity;
+    a.out = bloch::RasterOut{pos, mx, my, mz, t1, t2, m0, domega, weight};
+    int64_t n = 0;
+    int bad = 0;
+    ck(bloch::raster_run(a, c->raster_scratch.p, c->raster_scratch.cap, c->raster_staging.data(), c->n_sm,
+                         c->stream, &n, &bad),
+       "rasterize");
+    *n_out = n;
+    if (bad) return fail(BLOCH_E_INVALID, "rasterized tissue has m0 < 0 or T1/T2 <= 0");
   } catch (const std::exception& ex) {
     return fail(BLOCH_E_CUDA, ex.what());
   }

@@ -18,6 +18,7 @@ classes defined here.
 from __future__ import annotations
 
 import ctypes
+import dataclasses
 import math
 import os
 import platform
@@ -33,7 +34,7 @@ from .bloch import GAMMA_PROTON, hard_pulse_matrix
 from .errors import InvalidParameter
 from .phantom import DEFAULT_SPIN_CAP, Phantom, rasterize_arrays
 from .sequence import Sequence
-from .system import SystemModel, default_system, receive_weights, spin_off_resonance
+from .system import SystemModel, UniformSensitivity, default_system, receive_weights, spin_off_resonance
 
 # ---------------------------------------------------------------------------
 # event tables (master side) — engine.py:51-164
@@ -364,12 +365,13 @@ class BlochEngine:
 
     # -- compute -------------------------------------------------------------
     def compute_device(self, tables, spins: Dict[str, int], n: int, n_coils: int, out_echoes: int,
-                       out_snaps: int = 0, sync: bool = False) -> None:
+                       out_snaps: int = 0, sync: bool = False, present: Optional[np.ndarray] = None) -> None:
         """compute_block on device-resident float64 arrays (raw CUDA pointers).
 
         ``spins`` maps pos/mx/my/mz/t1/t2/m0/domega/weight to device pointers
         (weight 0 = uniform 1+0j); outputs are device pointers.  Asynchronous on
-        the engine's stream unless ``sync``.
+        the engine's stream unless ``sync``.  ``present`` (uint8, one per
+        snapshot time) receives which snapshots were taken.
         """
         f = self.set_tables(tables)
         ptr = lambda key: ctypes.cast(ctypes.c_void_p(int(spins[key])), ctypes.POINTER(ctypes.c_double)) \
@@ -380,7 +382,7 @@ class BlochEngine:
             ptr("domega"), ptr("weight"), int(n_coils),
             ctypes.cast(ctypes.c_void_p(int(out_echoes)), ctypes.POINTER(ctypes.c_double)) if out_echoes else None,
             ctypes.cast(ctypes.c_void_p(int(out_snaps)), ctypes.POINTER(ctypes.c_double)) if out_snaps else None,
-            None, flags,
+            present.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)) if present is not None else None, flags,
         )
         _capi.check(st, "bloch_compute_block")
         del f
@@ -547,6 +549,10 @@ def run(exp: Experiment) -> RunResult:
         )
     wall_start = time.perf_counter()
     spacing = tuple(float(s) for s in exp.spacing)
+    from .objects import DeviceScene
+
+    if isinstance(exp.phantom, DeviceScene):
+        return _run_device_scene(exp, spacing, wall_start)
     spins = rasterize_arrays(exp.phantom, spacing, cap=exp.spin_cap)
     if spins["m0"].size == 0:
         raise InvalidParameter("the phantom rasterized to zero spins")
@@ -579,6 +585,60 @@ def run(exp: Experiment) -> RunResult:
     snapshots = [
         (t, snaps[i] if snaps[i] is not None else np.zeros((0, 3))) for i, t in enumerate(tables.snapshot_times)
     ]
+    return RunResult(echoes=records, metrics=metrics, snapshots=snapshots, spin_count=n_spins, spacing=spacing)
+
+
+def _run_device_scene(exp: Experiment, spacing, wall_start: float) -> RunResult:
+    """run() for a DeviceScene: spins are rasterised on the GPU and never visit the host."""
+    import torch
+
+    from .objects import rasterize_device
+
+    sysm = exp.system
+    if sysm.field.inhomogeneity is not None:
+        raise InvalidParameter("a DeviceScene carries its own off-resonance maps; the system inhomogeneity "
+                               "callable has no device form")
+    tables = precompute_sequence_tables(exp.sequence, gamma=sysm.gamma, snapshot_times=exp.snapshot_times)
+    eng = get_engine(exp.device, exp.precision)
+    ctx = sysm.frame()
+    scene = exp.phantom
+    base = ctx.gamma * sysm.field.b0 - ctx.omega_hf
+    if base != 0.0:
+        scene = dataclasses.replace(scene, const_dw=scene.const_dw + base)
+    spins = rasterize_device(scene, spacing, eng, cap=exp.spin_cap)
+    f = eng.set_tables(tables)
+    dev = spins.pos.device
+    echo = torch.zeros((spins.n_coils, f["n_acq"], f["max_ns"]), dtype=torch.complex128, device=dev)
+    snaps = torch.zeros((f["n_snap"], spins.n, 3), dtype=torch.float64, device=dev) if f["n_snap"] else None
+    present = np.zeros(max(f["n_snap"], 1), dtype=np.uint8)
+    torch.cuda.current_stream(dev).synchronize()
+    t_k = time.perf_counter()
+    ptrs = spins.pointers()
+    if spins.n_coils == 1 and isinstance(scene.receive, UniformSensitivity) and scene.receive.s == 1.0:
+        ptrs["weight"] = 0
+    eng.compute_device(tables, ptrs, spins.n, spins.n_coils, echo.data_ptr(),
+                       snaps.data_ptr() if snaps is not None else 0, sync=True, present=present)
+    busy = time.perf_counter() - t_k
+    echo_sum = echo.cpu().numpy()
+    if spins.n_coils == 1:
+        echo_sum = echo_sum[0]
+    n_spins = spins.n
+    records = []
+    if tables.n_acq:
+        echo_sum = echo_sum / n_spins  # engine.py:507
+        for i in range(tables.n_acq):
+            records.append(EchoRecord(acq_index=i, values=echo_sum[..., i, : tables.acq_times[i].size],
+                                      timestamps=tables.acq_times[i]))
+    snap_host = snaps.cpu().numpy() if snaps is not None else None
+    wall = time.perf_counter() - wall_start
+    timing = eng.last_timing()
+    metrics = RunMetrics(
+        wall_time_s=wall, spin_count=n_spins, throughput=n_spins / wall if wall > 0 else math.inf,
+        workers=1, blocks=1, busy_fraction={0: busy / wall} if wall > 0 else {},
+        hardware=f"{platform.machine()} cuda:{eng.device} sm_100a", kernel_ms=timing["kernel_ms"],
+        events_per_spin=eng.program_stats()["events"],
+    )
+    snapshots = [(t, snap_host[i] if present[i] else np.zeros((0, 3))) for i, t in enumerate(tables.snapshot_times)]
     return RunResult(echoes=records, metrics=metrics, snapshots=snapshots, spin_count=n_spins, spacing=spacing)
 
 
