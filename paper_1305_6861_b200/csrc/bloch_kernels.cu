@@ -330,6 +330,124 @@ __device__ __forceinline__ void window_chunk_mc2(float (&ur)[S], float (&ui)[S],
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// ADC windows on the tensor cores (fp32 mode, one receive weight)
+// ---------------------------------------------------------------------------
+//
+// The window's samples are S_k = sum_s u_s z_s^k (k = 0..cnt-1, u_s the
+// weighted transverse magnetisation at the first sample, z_s the per-sample
+// factor).  Split k = 64 j + 8 a + b: S_k = sum_s z_s^b * (u_s z_s^(64 j + 8 a)),
+// a complex (8 x spins) x (spins x 8) product per 64-sample tile — a GEMM whose
+// contraction runs over the spins.  Embedded as a real m16n8k8 product:
+//   A[(b, re)][(s, re)] = Re z^b   A[(b, re)][(s, im)] = -Im z^b
+//   A[(b, im)][(s, re)] = Im z^b   A[(b, im)][(s, im)] =  Re z^b
+//   B[(s, re)][a] = Re V           B[(s, im)][a] = Im V,  V = u z^(64 j + 8 a)
+// so D[(b, re/im)][a] = Re/Im S_(64 j + 8 a + b).  One warp contracts its own
+// 32*S spins, 4 per mma (k = 8 = 4 spins x re/im), accumulating in fp32
+// registers; the per-sample spin sum never touches the CUDA cores.
+//
+// Precision: each operand is split x = hi + lo with both parts exact tf32
+// values (low 13 mantissa bits zero) and the product formed as
+// hi*hi + hi*lo + lo*hi (3 mma) — ~2^-20 relative per product, below the
+// fp32 recurrence it replaces.  Lane (g = lane/4, t = lane%4) needs z^g and
+// u z^(8 g) of spin t; it forms them from z by squarings.
+
+constexpr int kMmaMinWindow = 32;  // shorter windows use the recurrence path
+
+struct cf {
+  float r, i;
+};
+__device__ __forceinline__ cf cmul(cf a, cf b) { return cf{a.r * b.r - a.i * b.i, a.r * b.i + a.i * b.r}; }
+__device__ __forceinline__ cf csq(cf a) { return cf{a.r * a.r - a.i * a.i, 2.f * a.r * a.i}; }
+__device__ __forceinline__ cf csel(bool c, cf a) { return c ? a : cf{1.f, 0.f}; }
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+  hi = __float_as_uint(x) & 0xffffe000u;
+  lo = __float_as_uint(x - __uint_as_float(hi)) & 0xffffe000u;
+}
+
+__device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// Per-warp stage of one round (one spin per lane): for lane-spin q and power g,
+// (Re z^g, Im z^g, Re V_g, Im V_g) with V_g = u z^(8 g) at [g][q ^ 4 (g & 1)]
+// (the swizzle makes both the staging stores and the k-block loads
+// conflict-free), then z^64 per spin.
+constexpr int kStageFloat4 = 8 * 32;
+constexpr int kStageBytes = kStageFloat4 * 16 + 32 * 8 + 32 * 32;  // + cp.async slot (Cpre, z) per lane
+__device__ __forceinline__ int stage_idx(int g, int q) { return g * 32 + (q ^ ((g & 1) << 2)); }
+
+// One lane's spin into the stage: its 8 powers z^g and 8 values u z^(8g).
+__device__ __forceinline__ void stage_spin(float4* __restrict__ st, float2* __restrict__ z64s, int lane, cf u, cf z) {
+  cf zg{1.f, 0.f};
+  const cf z2 = csq(z), z4 = csq(z2), z8 = csq(z4);
+  cf v = u;
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    st[stage_idx(g, lane)] = make_float4(zg.r, zg.i, v.r, v.i);
+    zg = cmul(zg, z);
+    v = cmul(v, z8);
+  }
+  const cf z64 = csq(csq(csq(z8)));
+  z64s[lane] = make_float2(z64.r, z64.i);
+}
+
+// The 8 k-blocks (4 spins each) of one staged round into the NT tile
+// accumulators.  The three split products are issued pass-major across the NT
+// independent accumulators so consecutive mma never wait on each other.
+template <int NT>
+__device__ __forceinline__ void mma_round_t(const float4* __restrict__ st, const float2* __restrict__ z64s, int lane,
+                                            float (&acc)[4][4]) {
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll 2
+  for (int kb = 0; kb < 8; ++kb) {
+    const int q = 4 * kb + t;
+    const float4 e = st[stage_idx(g, q)];
+    const float2 w = z64s[q];
+    const cf z64{w.x, w.y};
+    uint32_t arh, arl, aih, ail;
+    split_tf32(e.x, arh, arl);
+    split_tf32(e.y, aih, ail);
+    const uint32_t naih = aih ^ 0x80000000u, nail = ail ^ 0x80000000u;
+    uint32_t brh[NT], brl[NT], bih[NT], bil[NT];
+    cf v{e.z, e.w};
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      split_tf32(v.r, brh[j], brl[j]);
+      split_tf32(v.i, bih[j], bil[j]);
+      if (j + 1 < NT) v = cmul(v, z64);
+    }
+#pragma unroll
+    for (int j = 0; j < NT; ++j) mma_tf32(acc[j], arh, aih, naih, arh, brh[j], bih[j]);
+#pragma unroll
+    for (int j = 0; j < NT; ++j) mma_tf32(acc[j], arh, aih, naih, arh, brl[j], bil[j]);
+#pragma unroll
+    for (int j = 0; j < NT; ++j) mma_tf32(acc[j], arl, ail, nail, arl, brh[j], bih[j]);
+  }
+}
+
+__device__ __forceinline__ void mma_round(const float4* __restrict__ st, const float2* __restrict__ z64s, int lane,
+                                          int ntile, float (&acc)[4][4]) {
+  switch (ntile) {
+    case 4: mma_round_t<4>(st, z64s, lane, acc); break;
+    case 3: mma_round_t<3>(st, z64s, lane, acc); break;
+    case 2: mma_round_t<2>(st, z64s, lane, acc); break;
+    default: mma_round_t<1>(st, z64s, lane, acc); break;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // the integrator
 // ---------------------------------------------------------------------------
@@ -629,6 +747,108 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
             if (sp.act(s)) prefetch_l2(base + sp.idx(s) * 8);
         }
         if (k2 == OP_WINDOW) break;
+      }
+      if constexpr (kPacked) {
+        if (cnt >= kMmaMinWindow) {  // tensor-core window (see the notes above stage_spin)
+          char* stb = reinterpret_cast<char*>(smem_raw) + static_cast<size_t>(3 * S) * bd * sizeof(double) +
+                      static_cast<size_t>(threadIdx.x >> 5) * kStageBytes;
+          float4* st = reinterpret_cast<float4*>(stb);
+          float2* z64s = reinterpret_cast<float2*>(stb + kStageFloat4 * 16);
+          double2* pf = reinterpret_cast<double2*>(stb + kStageFloat4 * 16 + 32 * 8);  // [lane][Cpre, z]
+          const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+          float2* out = reinterpret_cast<float2*>(strip.row) + s0;
+          const double2* tb = rc >= 0 ? reinterpret_cast<const double2*>(kp.rot) + static_cast<int64_t>(rc) * kp.n * 4
+                                      : nullptr;
+          for (int p0 = 0; p0 < cnt; p0 += 256) {  // passes of up to 4 tiles of 64 samples
+            const int ntile = min(4, (cnt - p0 + 63) >> 6);
+            const bool last = p0 + 256 >= cnt;
+            float acc[4][4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+            if (tb != nullptr && sp.act(0)) {  // (Cpre, z) of round 0 into this lane's prefetch slot
+              cp_async16(pf + 2 * lane, tb + sp.idx(0) * 4);
+              cp_async16(pf + 2 * lane + 1, tb + sp.idx(0) * 4 + 3);
+            }
+            cp_async_commit();
+#pragma unroll 1
+            for (int r = 0; r < S; ++r) {
+              cf u{0.f, 0.f}, z{0.f, 0.f};
+              cp_async_wait_all();
+              const double2 cpre = pf[2 * lane], zz = pf[2 * lane + 1];
+              if (tb != nullptr && r + 1 < S && sp.act(r + 1)) {  // next round's row lands during this round's mma
+                cp_async16(pf + 2 * lane, tb + sp.idx(r + 1) * 4);
+                cp_async16(pf + 2 * lane + 1, tb + sp.idx(r + 1) * 4 + 3);
+              }
+              cp_async_commit();
+              if (sp.act(r)) {
+                const int64_t i = sp.idx(r);
+                double pr = cpre.x, pi = cpre.y, zr0 = zz.x, zi0 = zz.y;
+                double th = 0.0;
+                SC c{};
+                if (tb == nullptr) {  // on the fly: a window whose interval is not reused
+                  const int c1 = __ldg(&op->cls);
+                  c = load_sc(kp, i);
+                  th = theta_of(c, __ldg(&op->p[0]), __ldg(&op->p[1]), __ldg(&op->p[2]), __ldg(&op->p[3]));
+                  const double2 e = c1 >= 0 ? relax_pair(kp, c1, i) : make_double2(1.0, 1.0);
+                  phase_factor(th, zr0, zi0);
+                  zr0 *= e.y;
+                  zi0 *= e.y;
+                  pr = 1.0;
+                  pi = 0.0;
+                }
+                double2 w0 = make_double2(1.0, 0.0);
+                if (kp.w != nullptr) w0 = __ldg(reinterpret_cast<const double2*>(kp.w) + i);
+                const double x = sp.mx(r), y = sp.my(r);
+                const double x0 = pr * x - pi * y, y0 = pr * y + pi * x;
+                u = cf{static_cast<float>(w0.x * x0 - w0.y * y0), static_cast<float>(w0.x * y0 + w0.y * x0)};
+                z = cf{static_cast<float>(zr0), static_cast<float>(zi0)};
+                if (!lead) u = cmul(u, z);  // first sample after one interval
+                if (p0 > 0) {               // later pass: u z^p0
+                  const cf z256 = csq(csq(csq(csq(csq(csq(csq(csq(z))))))));
+                  for (int q = 0; q < p0; q += 256) u = cmul(u, z256);
+                }
+                if (tb == nullptr && last) {  // exit propagator of the whole run, on the fly
+                  const int cw = __ldg(&op->flags);
+                  const double2 E = cw >= 0 ? relax_pair(kp, cw, i) : make_double2(1.0, 1.0);
+                  double cr, ci;
+                  phase_factor(th * static_cast<double>(cnt - lead), cr, ci);
+                  sp.mx(r) = E.y * (cr * x - ci * y);
+                  sp.my(r) = E.y * (cr * y + ci * x);
+                  sp.mz(r) = fma(sp.mz(r), E.x, c.m0 * (1.0 - E.x));
+                }
+              }
+              stage_spin(st, z64s, lane, u, z);
+              __syncwarp();
+              mma_round(st, z64s, lane, ntile, acc);
+              __syncwarp();  // the stage is rewritten by the next round
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              if (j < ntile) {
+                const int k1 = p0 + 64 * j + 16 * t + g, k2 = k1 + 8;
+                if (k1 < cnt) __stcs(out + k1, make_float2(acc[j][0], acc[j][2]));
+                if (k2 < cnt) __stcs(out + k2, make_float2(acc[j][1], acc[j][3]));
+              }
+            }
+          }
+          if (tb != nullptr) {  // exit: C m, mz -> A mz + B for all spins, loads issued together
+            double2 c[S], ab[S];
+#pragma unroll
+            for (int r = 0; r < S; ++r) {
+              const int64_t i = sp.act(r) ? sp.idx(r) : 0;
+              c[r] = __ldg(tb + i * 4 + 1);
+              ab[r] = __ldg(tb + i * 4 + 2);
+            }
+#pragma unroll
+            for (int r = 0; r < S; ++r) {
+              const double x = sp.mx(r), y = sp.my(r);
+              sp.mx(r) = c[r].x * x - c[r].y * y;
+              sp.my(r) = c[r].x * y + c[r].y * x;
+              sp.mz(r) = fma(sp.mz(r), ab[r].x, ab[r].y);
+            }
+          }
+          continue;
+        }
       }
       // per-spin setup: sample factor z and the exit propagator of the whole run
       R zr[S], zi[S], ur[S], ui[S];
@@ -934,7 +1154,10 @@ __global__ void reduce_partials_kernel(const R* __restrict__ part, int rows, int
 
 template <typename R, int S, int NC>
 size_t integrate_smem_bytes(int threads) {
-  return static_cast<size_t>(3 * S * threads) * sizeof(double);
+  constexpr bool kPacked = sizeof(R) == 4 && NC == 1 && (S % 2 == 0);
+  // fp64 spin state [3][S][threads] + (fp32 single-coil) the tensor-core window stage, 16 B per spin
+  return static_cast<size_t>(3 * S * threads) * sizeof(double) +
+         (kPacked ? static_cast<size_t>(threads / 32) * kStageBytes : 0);
 }
 
 template <typename R, int S, int NC>
