@@ -88,11 +88,14 @@ SIGNATURES = {
 _lib = None
 
 
-def load(path: str = LIB_PATH) -> ctypes.CDLL:
-    """Load and type the library once; raises ImportError if it is missing."""
+def load(path: str = None) -> ctypes.CDLL:
+    """Load and type the library once; raises ImportError if it is missing.
+
+    ``BLOCH_LIB`` overrides the path (A/B timing of two builds on one box)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("BLOCH_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise ImportError(
             f"{path} is missing: build it with `python -m paper_1305_6861_b200.build` "

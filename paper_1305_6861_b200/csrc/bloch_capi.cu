@@ -93,13 +93,21 @@ namespace {
 
 struct Variant {
   int prec, S, NC;
+  bool full = true;  // program uses RF trains / chirps / generic sampled events
 };
 
 // pick (S, NC) for a block of n spins with ncp (power-of-two) coils
 Variant pick_variant(int prec, int64_t n, int ncp, int n_sm) {
   if (prec == BLOCH_PREC_F32) {
     switch (ncp) {
-      case 1: return {32, n >= int64_t(n_sm) * 8 * 64 ? 8 : 2, 1};
+      case 1: {
+        static const int force_s = [] {  // experiment hook: BLOCH_F32_SPINS=4|8
+          const char* e = getenv("BLOCH_F32_SPINS");
+          return e ? atoi(e) : 0;
+        }();
+        if (force_s == 4 || force_s == 8) return {32, force_s, 1};
+        return {32, n >= int64_t(n_sm) * 8 * 64 ? 8 : 2, 1};
+      }
       case 2: return {32, 4, 2};
       case 4: return {32, 4, 4};
       default: return {32, 4, 8};
@@ -135,7 +143,7 @@ cudaError_t dispatch_one(const Variant& v, const bloch::KParams& kp, int grid, i
                          cudaStream_t st, bool* matched) {
   if (v.prec == int(8 * sizeof(R)) && v.S == S && v.NC == NC) {
     *matched = true;
-    return bloch::launch_integrate<R, S, NC>(kp, grid, threads, st);
+    return bloch::launch_integrate<R, S, NC>(kp, grid, threads, st, v.full);
   }
   return cudaSuccess;
 }
@@ -440,7 +448,10 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
     // 4. integrator + ordered fold
     float kms = 0.f;
     if (n > 0) {
-      const Variant v = pick_variant(c->precision, n, ncp, c->n_sm);
+      Variant v = pick_variant(c->precision, n, ncp, c->n_sm);
+      v.full = false;
+      for (const bloch::DevOp& op : P.ops)
+        if (op.kind == bloch::OP_RFTRAIN || op.kind == bloch::OP_CHIRP || op.kind == bloch::OP_GSAMP) v.full = true;
       int max_t = 512, min_b = 1;
       variant_shape(v, &max_t, &min_b);
       const int64_t slots = int64_t(c->n_sm) * min_b;  // resident CTAs per wave

@@ -157,6 +157,26 @@ __device__ __forceinline__ RotCoef load_rot(const KParams& kp, int c, int64_t i)
   return RotCoef{a.x, a.y, b.x, b.y, d.x, d.y, e.x, e.y};
 }
 
+// a hard pulse fused into the following op (DevOp.pre): 9 uniform matrix entries, bloch.py:124-139
+struct Mat3 {
+  double r[9];
+};
+__device__ __forceinline__ Mat3 load_mat(const KParams& kp, int pre) {
+  Mat3 m;
+  const double* q = kp.mats + static_cast<int64_t>(pre) * 9;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) m.r[k] = __ldg(q + k);
+  return m;
+}
+__device__ __forceinline__ void rotate(const Mat3& m, double& x, double& y, double& z) {
+  const double nx = m.r[0] * x + m.r[1] * y + m.r[2] * z;
+  const double ny = m.r[3] * x + m.r[4] * y + m.r[5] * z;
+  const double nz = m.r[6] * x + m.r[7] * y + m.r[8] * z;
+  x = nx;
+  y = ny;
+  z = nz;
+}
+
 // one interval on spin s (on the fly): precession (+ relaxation), fp64 — engine.py:288-302
 template <int S>
 __device__ __forceinline__ void interval(const KParams& kp, Spins<S>& sp, int s, int flags, int cls, double dt,
@@ -171,6 +191,20 @@ __device__ __forceinline__ void interval(const KParams& kp, Spins<S>& sp, int s,
   sp.mx(s) = e.y * (cs * x - ms * y);  // clockwise: (c - i s)(x + i y), bloch.py:10-17
   sp.my(s) = e.y * (cs * y + ms * x);
   if (cls >= 0) sp.mz(s) = fma(sp.mz(s), e.x, c.m0 * (1.0 - e.x));
+}
+
+// the fused pulse on its own pass over the state (paths that do not load the state anyway)
+template <int S>
+__device__ __forceinline__ void apply_pre(const KParams& kp, Spins<S>& sp, int pre) {
+  const Mat3 m = load_mat(kp, pre);
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    double x = sp.mx(s), y = sp.my(s), z = sp.mz(s);
+    rotate(m, x, y, z);
+    sp.mx(s) = x;
+    sp.my(s) = y;
+    sp.mz(s) = z;
+  }
 }
 
 // receive-weighted transverse magnetisation of the (fp64) state summed over the
@@ -452,7 +486,10 @@ __device__ __forceinline__ void mma_round(const float4* __restrict__ st, const f
 // the integrator
 // ---------------------------------------------------------------------------
 
-template <typename R, int S, int NC>
+// kFull: the program uses RF trains, chirps or generic sampled events.  Programs
+// made only of pulses, intervals and uniform windows (spin/turbo-spin echoes) run
+// a kernel without those handlers: less register pressure in the hot loop.
+template <typename R, int S, int NC, bool kFull>
 __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTraits<R, S, NC>::kMinBlocks)
     integrate_kernel(const KParams kp) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -499,7 +536,10 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
 
     if (kind == OP_EVENT) {
       const int flags = __ldg(&op->count), snap = __ldg(&op->aux), cls = __ldg(&op->cls), rc = __ldg(&op->rot),
-                pg = __ldg(&op->prg);
+                pg = __ldg(&op->prg), pre = __ldg(&op->pre);
+      if constexpr (!kFull) {  // a fused pulse (basic programs only): its own pass over the state
+        if (pre >= 0) apply_pre<S>(kp, sp, pre);
+      }
       // Two-phase per group of G spins: issue every table load of the group
       // before any store, so the L2 round trips overlap instead of serialising
       // behind possibly-aliasing shared/global stores.
@@ -567,6 +607,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
       continue;
     }
 
+    if constexpr (kFull) {
     if (kind == OP_RFTRAIN) {  // discretised shaped pulse: (pulse_j, identical interval) x count
       const int cnt = __ldg(&op->count), m0i = __ldg(&op->aux), flags = __ldg(&op->flags), cls = __ldg(&op->cls);
       const double dt = __ldg(&op->p[0]), dmx = __ldg(&op->p[1]), dmy = __ldg(&op->p[2]), dmz = __ldg(&op->p[3]);
@@ -725,9 +766,12 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
       continue;
     }
 
+    }
+
     // OP_WINDOW
     {
-      const int cnt = __ldg(&op->count), lead = __ldg(&op->aux), s0 = __ldg(&op->s0), rc = __ldg(&op->rot);
+      const int cnt = __ldg(&op->count), lead = __ldg(&op->aux), s0 = __ldg(&op->s0), rc = __ldg(&op->rot),
+                pre = __ldg(&op->pre);
       // The sample loop below is long and touches no memory but its partial row:
       // pull the per-spin records of the ops up to the next window into L2 now.
       for (int o2 = o + 1; o2 < kp.n_ops && o2 <= o + 8; ++o2) {
@@ -747,6 +791,9 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
             if (sp.act(s)) prefetch_l2(base + sp.idx(s) * 8);
         }
         if (k2 == OP_WINDOW) break;
+      }
+      if constexpr (!kFull) {
+        if (pre >= 0) apply_pre<S>(kp, sp, pre);
       }
       if constexpr (kPacked) {
         if (cnt >= kMmaMinWindow) {  // tensor-core window (see the notes above stage_spin)
@@ -1160,16 +1207,22 @@ size_t integrate_smem_bytes(int threads) {
          (kPacked ? static_cast<size_t>(threads / 32) * kStageBytes : 0);
 }
 
-template <typename R, int S, int NC>
-cudaError_t launch_integrate(const KParams& kp, int grid, int threads, cudaStream_t stream) {
+template <typename R, int S, int NC, bool kFull>
+static cudaError_t launch_one(const KParams& kp, int grid, int threads, cudaStream_t stream) {
   const size_t smem = integrate_smem_bytes<R, S, NC>(threads);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(integrate_kernel<R, S, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+    cudaError_t e = cudaFuncSetAttribute(integrate_kernel<R, S, NC, kFull>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  integrate_kernel<R, S, NC><<<grid, threads, smem, stream>>>(kp);
+  integrate_kernel<R, S, NC, kFull><<<grid, threads, smem, stream>>>(kp);
   return cudaGetLastError();
+}
+
+template <typename R, int S, int NC>
+cudaError_t launch_integrate(const KParams& kp, int grid, int threads, cudaStream_t stream, bool full) {
+  return full ? launch_one<R, S, NC, true>(kp, grid, threads, stream)
+              : launch_one<R, S, NC, false>(kp, grid, threads, stream);
 }
 
 static int grid_for(int64_t total, int threads) {
@@ -1237,7 +1290,7 @@ cudaError_t launch_reduce(const R* part, int rows, int64_t n_slots, int nc, int 
 template <typename R, int S, int NC>
 cudaError_t kernel_attrs(int* max_threads, int* regs) {
   cudaFuncAttributes a;
-  cudaError_t e = cudaFuncGetAttributes(&a, integrate_kernel<R, S, NC>);
+  cudaError_t e = cudaFuncGetAttributes(&a, integrate_kernel<R, S, NC, true>);
   if (e != cudaSuccess) return e;
   *max_threads = a.maxThreadsPerBlock;
   *regs = a.numRegs;
@@ -1245,7 +1298,7 @@ cudaError_t kernel_attrs(int* max_threads, int* regs) {
 }
 
 #define BLOCH_INST(R, S, NC)                                                              \
-  template cudaError_t launch_integrate<R, S, NC>(const KParams&, int, int, cudaStream_t); \
+  template cudaError_t launch_integrate<R, S, NC>(const KParams&, int, int, cudaStream_t, bool); \
   template cudaError_t kernel_attrs<R, S, NC>(int*, int*);                                 \
   template size_t integrate_smem_bytes<R, S, NC>(int);
 BLOCH_FOR_EACH_VARIANT(BLOCH_INST)

@@ -49,6 +49,7 @@ struct KernelTraits<float, 8, 1> {  // the fp32 single-coil workhorse: 2 CTAs x 
 // (real type, spins per thread, coils) instantiated in bloch_kernels.cu
 #define BLOCH_FOR_EACH_VARIANT(X) \
   X(float, 8, 1)                  \
+  X(float, 4, 1)                  \
   X(float, 2, 1)                  \
   X(float, 4, 2)                  \
   X(float, 4, 4)                  \
@@ -59,8 +60,14 @@ struct KernelTraits<float, 8, 1> {  // the fp32 single-coil workhorse: 2 CTAs x 
   X(double, 2, 4)                 \
   X(double, 1, 8)
 
+template <>
+struct KernelTraits<float, 4, 1> {  // experiment: 2 CTAs x 12 warps, 4 spins per thread
+  static constexpr int kMaxThreads = 384;
+  static constexpr int kMinBlocks = 2;
+};
+
 template <typename R, int S, int NC>
-cudaError_t launch_integrate(const KParams& kp, int grid, int threads, cudaStream_t stream);
+cudaError_t launch_integrate(const KParams& kp, int grid, int threads, cudaStream_t stream, bool full);
 template <typename R, int S, int NC>
 cudaError_t kernel_attrs(int* max_threads, int* regs);
 template <typename R, int S, int NC>

@@ -52,6 +52,7 @@ inline bool same_interval(double dt_a, const double* a, double dt_b, const doubl
 void fuse_intervals(Program& prog, const std::function<int32_t(double)>& relax_class);
 void find_progressions(Program& prog);
 void find_chirp_classes(Program& prog);
+void fuse_pulses(Program& prog);
 
 void compile_program(const TablesView& t, Program& prog) {
   prog = Program();
@@ -448,6 +449,38 @@ void fuse_intervals(Program& prog, const std::function<int32_t(double)>& relax_c
   prog.ops.swap(out);
   find_progressions(prog);
   find_chirp_classes(prog);
+  fuse_pulses(prog);
+}
+
+// A hard pulse followed by an interval or a window is applied by that op
+// (DevOp.pre): one op dispatch less per pulse.  The matrix moves to the shared
+// matrix table; the arithmetic is unchanged (R m first, then the op), so results
+// are bit-identical.  Only programs of pulses, intervals and windows are fused:
+// their kernel variant (kFull = false) is the one that handles DevOp.pre.
+void fuse_pulses(Program& prog) {
+  std::vector<DevOp> out;
+  out.reserve(prog.ops.size());
+  bool basic = true;  // only pulses, intervals and windows: the kernel variant that handles DevOp.pre
+  for (auto& op : prog.ops) {
+    op.pre = -1;
+    if (op.kind == OP_RFTRAIN || op.kind == OP_CHIRP || op.kind == OP_GSAMP) basic = false;
+  }
+  if (!basic) return;
+  for (size_t k = 0; k < prog.ops.size(); ++k) {
+    const DevOp& op = prog.ops[k];
+    if (op.kind == OP_ROT && k + 1 < prog.ops.size() &&
+        (prog.ops[k + 1].kind == OP_EVENT || prog.ops[k + 1].kind == OP_WINDOW)) {
+      DevOp next = prog.ops[k + 1];
+      next.pre = static_cast<int32_t>(prog.mats.size() / 9);
+      prog.mats.insert(prog.mats.end(), op.p, op.p + 9);
+      out.push_back(next);
+      prog.n_fused_pulses++;
+      ++k;
+      continue;
+    }
+    out.push_back(op);
+  }
+  prog.ops.swap(out);
 }
 
 // Chirp classes (program.h ChirpClass): a ramp that recurs (every EPI line) is

@@ -53,7 +53,8 @@ struct alignas(16) DevOp {
   int32_t cls;    // relax class of dt (EVENT/CHIRP/RFTRAIN on-the-fly path), -1 = no relaxation
   int32_t rot;    // rotation class (EVENT: repeated interval; WINDOW: reused run), -1 = none
   int32_t prg;    // EVENT: progression class (interval of an arithmetic series of moments), -1 = none
-  int32_t pad[6];
+  int32_t pre;    // EVENT/WINDOW: hard pulse applied first (matrix index into mats, fused OP_ROT), -1 = none
+  int32_t pad[5];
 };
 
 // A rotation class: pre, then `mult` times main, then post (intervals (dt,

@@ -35,7 +35,7 @@ struct Program {
   int64_t n_samples = 0;
   int64_t n_rot = 0, n_interval = 0, n_window_ops = 0, n_window_samples = 0, n_gsamp_events = 0;
   int64_t n_chirp_ops = 0, n_chirp_samples = 0, n_train_ops = 0, n_train_pairs = 0;
-  int64_t n_fused_windows = 0, n_fused_intervals = 0, n_prog_intervals = 0;
+  int64_t n_fused_windows = 0, n_fused_intervals = 0, n_prog_intervals = 0, n_fused_pulses = 0;
 };
 
 // Throws std::invalid_argument on malformed tables.
