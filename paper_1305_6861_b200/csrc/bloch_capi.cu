@@ -81,7 +81,7 @@ struct bloch_ctx {
   std::vector<uint8_t> snap_present;
   DevBuf d_ops, d_gev, d_mats, d_sample_g, d_relax_t, d_rot_cls, d_prog_cls, d_chirp_cls;
   DevBuf in_pos, in_mx, in_my, in_mz, in_t1, in_t2, in_m0, in_dw, in_w;
-  DevBuf sc, wpad;
+  DevBuf sc, wpad, w32;
   DevBuf partial, echo, snaps, relax, rot, progtab, chirptab;
   DevBuf raster_scratch;
   std::vector<unsigned char> raster_staging;
@@ -237,7 +237,7 @@ int bloch_destroy(bloch_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (DevBuf* b : {&c->d_ops, &c->d_gev, &c->d_mats, &c->d_sample_g, &c->d_relax_t, &c->relax, &c->d_rot_cls, &c->rot, &c->in_pos, &c->in_mx, &c->in_my, &c->in_mz,
-                    &c->in_t1, &c->in_t2, &c->in_m0, &c->in_dw, &c->in_w, &c->sc, &c->wpad, &c->partial,
+                    &c->in_t1, &c->in_t2, &c->in_m0, &c->in_dw, &c->in_w, &c->sc, &c->wpad, &c->w32, &c->partial,
                     &c->echo, &c->snaps, &c->d_prog_cls, &c->progtab, &c->d_chirp_cls, &c->chirptab,
                     &c->raster_scratch})
     b->release();
@@ -434,6 +434,11 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
         c->launches++;
         d_w = c->wpad.as<double>();
       }
+      if (d_w && ncp >= 2 && c->precision == BLOCH_PREC_F32) {  // fp32 weights for the tensor-core windows
+        c->w32.ensure(static_cast<size_t>(n) * ncp * sizeof(float2));
+        ck(bloch::launch_weights_f32(n, ncp, d_w, c->w32.as<float2>(), st), "weights kernel");
+        c->launches++;
+      }
     }
     // 3. outputs
     const size_t echo_bytes = static_cast<size_t>(G) * n_coils * 2 * sizeof(double);
@@ -478,6 +483,7 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       kp.my0 = d_my;
       kp.mz0 = d_mz;
       kp.w = d_w;
+      kp.w32 = (d_w && ncp >= 2 && c->precision == BLOCH_PREC_F32) ? c->w32.as<float2>() : nullptr;
       kp.partial = c->partial.p;
       kp.part_stride = n_slots * 2;
       kp.snaps = d_snap;

@@ -482,6 +482,61 @@ __device__ __forceinline__ void mma_round(const float4* __restrict__ st, const f
   }
 }
 
+// Multi-coil windows: S_(k,c) = sum_s z_s^b * (w_(c,s) u_s z_s^(64 j + 8 a)).  The
+// A operand (z^b) is shared by the coils; each coil has its own B = w_c V.  One
+// 64-sample tile at a time (NC x 4 accumulators), rounds of one spin per lane
+// inside; the coil weights (fp32, spin-major) arrive by cp.async one round
+// ahead, double-buffered.
+template <int NC>
+struct McStage {
+  static constexpr int kW = 32 * NC * 8;                            // one weight buffer: [lane spin][coil] float2
+  static constexpr int kBytes = kStageFloat4 * 16 + 2 * kW + 32 * 32;  // + cp.async slot (Cpre, z)
+};
+
+__device__ __forceinline__ void stage_spin_mc(float4* __restrict__ st, int lane, cf u, cf z) {
+  const cf z8 = csq(csq(csq(z)));
+  cf zg{1.f, 0.f}, v = u;
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    st[stage_idx(g, lane)] = make_float4(zg.r, zg.i, v.r, v.i);
+    zg = cmul(zg, z);
+    v = cmul(v, z8);
+  }
+}
+
+template <int NC>
+__device__ __forceinline__ void mma_round_mc(const float4* __restrict__ st, const float2* __restrict__ wst, int lane,
+                                             float (&acc)[NC][4]) {
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll 1
+  for (int kb = 0; kb < 8; ++kb) {
+    const int q = 4 * kb + t;
+    const float4 e = st[stage_idx(g, q)];
+    uint32_t arh, arl, aih, ail;
+    split_tf32(e.x, arh, arl);
+    split_tf32(e.y, aih, ail);
+    const uint32_t naih = aih ^ 0x80000000u, nail = ail ^ 0x80000000u;
+    const cf v{e.z, e.w};
+    uint32_t brh[NC], brl[NC], bih[NC], bil[NC];
+    const float4* wq = reinterpret_cast<const float4*>(wst + q * NC);
+#pragma unroll
+    for (int c2 = 0; c2 < NC / 2; ++c2) {
+      const float4 w2 = wq[c2];
+      const cf b0 = cmul(cf{w2.x, w2.y}, v), b1 = cmul(cf{w2.z, w2.w}, v);
+      split_tf32(b0.r, brh[2 * c2], brl[2 * c2]);
+      split_tf32(b0.i, bih[2 * c2], bil[2 * c2]);
+      split_tf32(b1.r, brh[2 * c2 + 1], brl[2 * c2 + 1]);
+      split_tf32(b1.i, bih[2 * c2 + 1], bil[2 * c2 + 1]);
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) mma_tf32(acc[c], arh, aih, naih, arh, brh[c], bih[c]);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) mma_tf32(acc[c], arh, aih, naih, arh, brl[c], bil[c]);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) mma_tf32(acc[c], arl, ail, nail, arl, brh[c], bih[c]);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // the integrator
 // ---------------------------------------------------------------------------
@@ -794,6 +849,105 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
       }
       if constexpr (!kFull) {
         if (pre >= 0) apply_pre<S>(kp, sp, pre);
+      }
+      if constexpr (sizeof(R) == 4 && NC >= 2) {
+        if (cnt >= kMmaMinWindow && kp.w32 != nullptr) {  // tensor-core multi-coil window
+          char* stb = reinterpret_cast<char*>(smem_raw) + static_cast<size_t>(3 * S) * bd * sizeof(double) +
+                      static_cast<size_t>(threadIdx.x >> 5) * McStage<NC>::kBytes;
+          float4* st = reinterpret_cast<float4*>(stb);
+          float2* wbuf = reinterpret_cast<float2*>(stb + kStageFloat4 * 16);  // 2 x [32][NC]
+          double2* pf = reinterpret_cast<double2*>(stb + kStageFloat4 * 16 + 2 * McStage<NC>::kW);
+          const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+          float2* out = reinterpret_cast<float2*>(strip.row);
+          const double2* tb = rc >= 0 ? reinterpret_cast<const double2*>(kp.rot) + static_cast<int64_t>(rc) * kp.n * 4
+                                      : nullptr;
+          const int ntile = (cnt + 63) >> 6;
+          for (int j = 0; j < ntile; ++j) {
+            const bool last = j + 1 == ntile;
+            float acc[NC][4];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) acc[c][0] = acc[c][1] = acc[c][2] = acc[c][3] = 0.f;
+            auto fetch = [&](int r, int buf) {  // (Cpre, z) and the coil weights of this lane's spin r
+              if (!sp.act(r)) return;
+              const int64_t i = sp.idx(r);
+              if (tb != nullptr) {
+                cp_async16(pf + 2 * lane, tb + i * 4);
+                cp_async16(pf + 2 * lane + 1, tb + i * 4 + 3);
+              }
+              const float2* wsrc = kp.w32 + i * NC;
+#pragma unroll
+              for (int c2 = 0; c2 < NC / 2; ++c2)
+                cp_async16(wbuf + buf * 32 * NC + lane * NC + 2 * c2, wsrc + 2 * c2);
+            };
+            fetch(0, 0);
+            cp_async_commit();
+#pragma unroll 1
+            for (int r = 0; r < S; ++r) {
+              cp_async_wait_all();
+              const double2 cpre = pf[2 * lane], zz = pf[2 * lane + 1];
+              if (!sp.act(r)) {  // inactive spin: zero weights (the buffer may hold another spin's)
+#pragma unroll
+                for (int c = 0; c < NC; ++c) wbuf[(r & 1) * 32 * NC + lane * NC + c] = make_float2(0.f, 0.f);
+              }
+              if (r + 1 < S) fetch(r + 1, (r + 1) & 1);
+              cp_async_commit();
+              cf u{0.f, 0.f}, z{0.f, 0.f};
+              if (sp.act(r)) {
+                const int64_t i = sp.idx(r);
+                double pr = cpre.x, pi = cpre.y, zr0 = zz.x, zi0 = zz.y, th = 0.0;
+                SC c{};
+                if (tb == nullptr) {
+                  const int c1 = __ldg(&op->cls);
+                  c = load_sc(kp, i);
+                  th = theta_of(c, __ldg(&op->p[0]), __ldg(&op->p[1]), __ldg(&op->p[2]), __ldg(&op->p[3]));
+                  const double2 e = c1 >= 0 ? relax_pair(kp, c1, i) : make_double2(1.0, 1.0);
+                  phase_factor(th, zr0, zi0);
+                  zr0 *= e.y;
+                  zi0 *= e.y;
+                  pr = 1.0;
+                  pi = 0.0;
+                }
+                const double x = sp.mx(r), y = sp.my(r);
+                u = cf{static_cast<float>(pr * x - pi * y), static_cast<float>(pr * y + pi * x)};
+                z = cf{static_cast<float>(zr0), static_cast<float>(zi0)};
+                if (!lead) u = cmul(u, z);
+                const cf z64 = csq(csq(csq(csq(csq(csq(z))))));
+                for (int q = 0; q < j; ++q) u = cmul(u, z64);  // this tile starts at sample 64 j
+                if (tb == nullptr && last) {
+                  const int cw = __ldg(&op->flags);
+                  const double2 E = cw >= 0 ? relax_pair(kp, cw, i) : make_double2(1.0, 1.0);
+                  double cr, ci;
+                  phase_factor(th * static_cast<double>(cnt - lead), cr, ci);
+                  sp.mx(r) = E.y * (cr * x - ci * y);
+                  sp.my(r) = E.y * (cr * y + ci * x);
+                  sp.mz(r) = fma(sp.mz(r), E.x, c.m0 * (1.0 - E.x));
+                }
+              }
+              stage_spin_mc(st, lane, u, z);
+              __syncwarp();
+              mma_round_mc<NC>(st, wbuf + (r & 1) * 32 * NC, lane, acc);
+              __syncwarp();
+            }
+            const int k1 = 64 * j + 16 * t + g, k2 = k1 + 8;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+              if (k1 < cnt) __stcs(out + static_cast<int64_t>(s0 + k1) * NC + c, make_float2(acc[c][0], acc[c][2]));
+              if (k2 < cnt) __stcs(out + static_cast<int64_t>(s0 + k2) * NC + c, make_float2(acc[c][1], acc[c][3]));
+            }
+          }
+          if (tb != nullptr) {
+#pragma unroll
+            for (int r = 0; r < S; ++r) {
+              const int64_t i = sp.act(r) ? sp.idx(r) : 0;
+              const double2 c = __ldg(tb + i * 4 + 1), ab = __ldg(tb + i * 4 + 2);
+              const double x = sp.mx(r), y = sp.my(r);
+              sp.mx(r) = c.x * x - c.y * y;
+              sp.my(r) = c.x * y + c.y * x;
+              sp.mz(r) = fma(sp.mz(r), ab.x, ab.y);
+            }
+          }
+          continue;
+        }
       }
       if constexpr (kPacked) {
         if (cnt >= kMmaMinWindow) {  // tensor-core window (see the notes above stage_spin)
@@ -1179,6 +1333,16 @@ __global__ void pad_weights_kernel(int64_t n, int nc, int ncp, const double* __r
   }
 }
 
+// fp32 copy of the (padded) coil weights, spin-major: out[i][c] = w[c][i]
+__global__ void weights_f32_kernel(int64_t n, int ncp, const double2* __restrict__ w, float2* __restrict__ out) {
+  const int64_t total = static_cast<int64_t>(ncp) * n;
+  for (int64_t t = gtid(); t < total; t += gstride()) {
+    const int64_t i = t / ncp, c = t % ncp;
+    const double2 v = w[c * n + i];
+    out[t] = make_float2(static_cast<float>(v.x), static_cast<float>(v.y));
+  }
+}
+
 template <typename R>
 __global__ void reduce_partials_kernel(const R* __restrict__ part, int rows, int64_t n_slots, int nc, int ncp,
                                        const int64_t* __restrict__ sample_g, int64_t G, double* __restrict__ out) {
@@ -1203,8 +1367,10 @@ template <typename R, int S, int NC>
 size_t integrate_smem_bytes(int threads) {
   constexpr bool kPacked = sizeof(R) == 4 && NC == 1 && (S % 2 == 0);
   // fp64 spin state [3][S][threads] + (fp32 single-coil) the tensor-core window stage, 16 B per spin
-  return static_cast<size_t>(3 * S * threads) * sizeof(double) +
-         (kPacked ? static_cast<size_t>(threads / 32) * kStageBytes : 0);
+  size_t stage = 0;
+  if constexpr (kPacked) stage = kStageBytes;
+  if constexpr (sizeof(R) == 4 && NC >= 2) stage = McStage<NC>::kBytes;
+  return static_cast<size_t>(3 * S * threads) * sizeof(double) + static_cast<size_t>(threads / 32) * stage;
 }
 
 template <typename R, int S, int NC, bool kFull>
@@ -1273,6 +1439,13 @@ cudaError_t launch_pad_weights(int64_t n, int nc, int ncp, const double* w, doub
   const int64_t total = static_cast<int64_t>(ncp) * n * 2;
   if (total == 0) return cudaSuccess;
   pad_weights_kernel<<<grid_for(total, 256), 256, 0, stream>>>(n, nc, ncp, w, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_weights_f32(int64_t n, int ncp, const double* w, float2* out, cudaStream_t stream) {
+  const int64_t total = static_cast<int64_t>(ncp) * n;
+  if (total == 0) return cudaSuccess;
+  weights_f32_kernel<<<grid_for(total, 256), 256, 0, stream>>>(n, ncp, reinterpret_cast<const double2*>(w), out);
   return cudaGetLastError();
 }
 
