@@ -408,7 +408,8 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       const int n_rot = static_cast<int>(P.rot_classes.size());
       if (n_rot > 0) {
         c->rot.ensure(8 * nd * n_rot);
-        ck(bloch::launch_rot_table(n, n_rot, c->d_rot_cls.as<bloch::RotClass>(), d_sc, c->rot.as<double>(), st),
+        ck(bloch::launch_rot_table(n, n_rot, c->d_rot_cls.as<bloch::RotClass>(), d_sc, n_coils == 1 ? d_w : nullptr,
+                                   c->rot.as<double>(), st),
            "rotation table kernel");
         c->launches++;
       }

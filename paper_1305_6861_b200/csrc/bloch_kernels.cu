@@ -997,8 +997,8 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
                   pr = 1.0;
                   pi = 0.0;
                 }
-                double2 w0 = make_double2(1.0, 0.0);
-                if (kp.w != nullptr) w0 = __ldg(reinterpret_cast<const double2*>(kp.w) + i);
+                double2 w0 = make_double2(1.0, 0.0);  // tabulated windows carry w in Cpre
+                if (kp.w != nullptr && tb == nullptr) w0 = __ldg(reinterpret_cast<const double2*>(kp.w) + i);
                 const double x = sp.mx(r), y = sp.my(r);
                 const double x0 = pr * x - pi * y, y0 = pr * y + pi * x;
                 u = cf{static_cast<float>(w0.x * x0 - w0.y * y0), static_cast<float>(w0.x * y0 + w0.y * x0)};
@@ -1084,8 +1084,8 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
         }
         zr[s] = static_cast<R>(k.zr);
         zi[s] = static_cast<R>(k.zi);
-        double2 w0 = make_double2(1.0, 0.0);
-        if (kp.w != nullptr && NC == 1) w0 = __ldg(reinterpret_cast<const double2*>(kp.w) + i);
+        double2 w0 = make_double2(1.0, 0.0);  // tabulated windows carry w in Cpre
+        if (kp.w != nullptr && NC == 1 && rc < 0) w0 = __ldg(reinterpret_cast<const double2*>(kp.w) + i);
         const double x = sp.mx(s), y = sp.my(s);
         // state at the first sample: the absorbed pre-interval applied
         const double x0 = k.pr * x - k.pi * y, y0 = k.pr * y + k.pi * x;
@@ -1253,8 +1253,11 @@ __global__ void relax_table_kernel(int64_t n, int n_cls, const double* __restric
 // rotation-class propagators, fp64 (program.h RotClass): for class c and spin i
 //   Cpre = e2(pre) e^{-i th_pre}; C = e^{-T/T2} e^{-i (th_pre + m th + th_post)};
 //   A = e^{-T/T1}, B = m0 (1 - A); z = e2(main) e^{-i th}
+// w1: single-coil receive weights (or nullptr): folded into Cpre, so a window forms
+// u = (w Cpre) m straight from the table (no per-window weight load)
 __global__ void rot_table_kernel(int64_t n, int n_cls, const RotClass* __restrict__ rc,
-                                 const SpinConst* __restrict__ sc, double2* __restrict__ out) {
+                                 const SpinConst* __restrict__ sc, const double2* __restrict__ w1,
+                                 double2* __restrict__ out) {
   const int64_t total = static_cast<int64_t>(n_cls) * n;
   for (int64_t t = gtid(); t < total; t += gstride()) {
     const int64_t c = t / n, i = t - c * n;
@@ -1270,7 +1273,8 @@ __global__ void rot_table_kernel(int64_t n, int n_cls, const RotClass* __restric
     const double ep = exp(-k.pre[0] * s.r2), e2 = exp(-k.main[0] * s.r2);
     const double E2 = exp(-T * s.r2), E1 = exp(-T * s.r1);
     double2* o = out + t * 4;
-    o[0] = make_double2(ep * pc, ep * ps);
+    const double2 w = w1 != nullptr ? w1[i] : make_double2(1.0, 0.0);
+    o[0] = make_double2(w.x * (ep * pc) - w.y * (ep * ps), w.x * (ep * ps) + w.y * (ep * pc));
     o[1] = make_double2(E2 * tc, E2 * ts);
     o[2] = make_double2(E1, s.m0 * (1.0 - E1));
     o[3] = make_double2(e2 * c1, e2 * s1);
@@ -1411,11 +1415,11 @@ cudaError_t launch_relax_table(int64_t n, int n_cls, const double* T, const Spin
   return cudaGetLastError();
 }
 
-cudaError_t launch_rot_table(int64_t n, int n_cls, const RotClass* rc, const SpinConst* sc, double* out,
-                             cudaStream_t stream) {
+cudaError_t launch_rot_table(int64_t n, int n_cls, const RotClass* rc, const SpinConst* sc, const double* w1,
+                             double* out, cudaStream_t stream) {
   if (n == 0 || n_cls == 0) return cudaSuccess;
   rot_table_kernel<<<grid_for(static_cast<int64_t>(n_cls) * n, 256), 256, 0, stream>>>(
-      n, n_cls, rc, sc, reinterpret_cast<double2*>(out));
+      n, n_cls, rc, sc, reinterpret_cast<const double2*>(w1), reinterpret_cast<double2*>(out));
   return cudaGetLastError();
 }
 

@@ -77,8 +77,8 @@ cudaError_t launch_prep(int64_t n, const double* pos, const double* dw, const do
                         const double* t2, SpinConst* sc, cudaStream_t stream);
 cudaError_t launch_relax_table(int64_t n, int n_cls, const double* T, const SpinConst* sc, double* out,
                                cudaStream_t stream);
-cudaError_t launch_rot_table(int64_t n, int n_cls, const RotClass* rc, const SpinConst* sc, double* out,
-                             cudaStream_t stream);
+cudaError_t launch_rot_table(int64_t n, int n_cls, const RotClass* rc, const SpinConst* sc, const double* w1,
+                             double* out, cudaStream_t stream);
 cudaError_t launch_prog_table(int64_t n, int n_cls, const ProgClass* pc, const SpinConst* sc, double* out,
                               cudaStream_t stream);
 cudaError_t launch_chirp_table(int64_t n, int n_cls, const ChirpClass* cc, const SpinConst* sc, double* out,

@@ -418,15 +418,24 @@ class BlochEngine:
         else:
             snaps = np.zeros((n_snap, n, 3)) if n_snap else None
         present = np.zeros(max(n_snap, 1), dtype=np.uint8)
+        # the uniform receive weight 1+0j (the reference's default system) travels as NULL: no
+        # upload, and the kernel skips the weighting (bloch_b200.h: weight NULL = uniform 1+0j)
+        wptr = None if (n_coils == 1 and n and _unit_weight(wc)) else _capi.dptr(wc.view(np.float64))
         st = self._lib.bloch_compute_block(
             self._h, n, _capi.dptr(pos), *[_capi.dptr(a) for a in arrs],
-            _capi.dptr(wc.view(np.float64)), n_coils, _capi.dptr(echoes.view(np.float64)),
+            wptr, n_coils, _capi.dptr(echoes.view(np.float64)),
             _capi.dptr(snaps) if snaps is not None else None,
             present.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), 0,
         )
         _capi.check(st, "bloch_compute_block", block_index)
         snap_list = [snaps[i] if present[i] else None for i in range(n_snap)]
         return (echoes if multi else echoes[0]), snap_list
+
+
+def _unit_weight(wc: np.ndarray) -> bool:
+    """All weights exactly 1+0j (checked without a temporary complex comparison array)."""
+    f = wc.view(np.float64)
+    return bool(np.all(f[..., 0::2] == 1.0) and not np.any(f[..., 1::2]))
 
 
 _ENGINES: Dict[Tuple[int, int], BlochEngine] = {}
