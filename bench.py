@@ -348,6 +348,29 @@ def main():
             traffic = json.load(fh).get(f"config{args.config}")
     except Exception:
         pass
+    # the contract's measured denominators (MEASURED_PEAKS.json), beside the SURVEY §8d model:
+    # HBM traffic of the integrator (ncu capture) and the tensor pipe's actual work in the ADC
+    # windows (mma.sync tf32, 3 split passes x 4 real MAC per spin-sample-coil), whose measured
+    # peak is 512 MAC/clk/SM (profiles/r1_mma_microbench.txt).
+    hbm_peak = bf16_peak = None
+    try:
+        with open(peaks_path) as fh:
+            mp = json.load(fh)
+        hbm_peak, bf16_peak = float(mp["hbm_gbs"]), float(mp["bf16_tflops"])
+    except Exception:
+        pass
+    w_mma = n_local * pstats["window_samples"] * C * 12 if args.precision == 32 else 0
+    p_mma = n_sm * 512 * f_max * 1e6
+    measured = {
+        "hbm": {"achieved_gbs": traffic / t_kernel / 1e9 if traffic else None, "peak_gbs": hbm_peak,
+                "frac": traffic / t_kernel / 1e9 / hbm_peak if traffic and hbm_peak else None,
+                "source": "peak of measured (MEASURED_PEAKS.json hbm_gbs)"},
+        "tensor_mma_tf32": {"achieved_tflops": 2 * w_mma / t_kernel / 1e12, "peak_tflops": 2 * p_mma / 1e12,
+                            "frac": w_mma / p_mma / t_kernel,
+                            "source": "peak of measured (mma.sync m16n8k8 tf32 512 MAC/clk/SM, "
+                                      "profiles/r1_mma_microbench.txt); bf16 GEMM peak of measured "
+                                      f"{bf16_peak} TFLOP/s is tcgen05 bf16 and does not apply"},
+    }
     roofline = {
         "bound": "fp32+mufu",
         "achieved": model_ops / t_kernel / 1e12,
@@ -361,6 +384,7 @@ def main():
         "kernel_ms": t_kernel * 1e3,
         "roofline_ms": t_star * 1e3,
         "updates_per_s_at_roofline": n_local * E / t_star,
+        "measured_peaks": measured,
     }
 
     line = {
