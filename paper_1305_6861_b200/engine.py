@@ -432,10 +432,18 @@ class BlochEngine:
         return (echoes if multi else echoes[0]), snap_list
 
 
-def _unit_weight(wc: np.ndarray) -> bool:
-    """All weights exactly 1+0j (checked without a temporary complex comparison array)."""
-    f = wc.view(np.float64)
-    return bool(np.all(f[..., 0::2] == 1.0) and not np.any(f[..., 1::2]))
+def _unit_weight(wc: np.ndarray, chunk: int = 1 << 15) -> bool:
+    """All weights exactly 1+0j.  Bit-compared in cache-sized chunks (early exit): the check
+    must cost less than the 16 B/spin upload it saves."""
+    u = np.ascontiguousarray(wc).reshape(-1).view(np.uint64)
+    one = np.uint64(0x3FF0000000000000)
+    pattern = np.empty(min(2 * chunk, u.size), dtype=np.uint64)
+    pattern[0::2], pattern[1::2] = one, 0
+    for i in range(0, u.size, 2 * chunk):
+        seg = u[i: i + 2 * chunk]
+        if not np.array_equal(seg, pattern[: seg.size]):
+            return False
+    return True
 
 
 _ENGINES: Dict[Tuple[int, int], BlochEngine] = {}
