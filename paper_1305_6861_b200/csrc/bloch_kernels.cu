@@ -746,15 +746,20 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
     }
 
     if (kind == OP_CHIRP) {  // linear-increment sampled run: geometric rotation factors, fp64
+      // Spin-outer over blocks of two chunks: each spin's chirp-class row (or its
+      // SpinConst) is read once per block, not once per 8-sample chunk.
       const int cnt = __ldg(&op->count), s0 = __ldg(&op->s0), cls = __ldg(&op->cls), crc = __ldg(&op->rot);
       const double dt = __ldg(&op->p[0]);
       const double d0x = __ldg(&op->p[1]), d0y = __ldg(&op->p[2]), d0z = __ldg(&op->p[3]);
       const double ddx = __ldg(&op->p[4]), ddy = __ldg(&op->p[5]), ddz = __ldg(&op->p[6]);
-      for (int k0 = 0; k0 < cnt; k0 += kSampPerChunk) {
-        const int ck = min(kSampPerChunk, cnt - k0);
-        R ar[kChunkSlots], ai[kChunkSlots];
+      constexpr int kBlk = 2 * kSampPerChunk;
+      for (int k0 = 0; k0 < cnt; k0 += kBlk) {
+        const int cb = min(kBlk, cnt - k0);
+        R ar[2][kChunkSlots], ai[2][kChunkSlots];
 #pragma unroll
-        for (int j = 0; j < kChunkSlots; ++j) ar[j] = ai[j] = R(0);
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int j = 0; j < kChunkSlots; ++j) ar[h][j] = ai[h][j] = R(0);
 #pragma unroll 1
         for (int s = 0; s < S; ++s) {
           if (!sp.act(s)) continue;
@@ -765,12 +770,13 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
             const double2 r0 = __ldg(tb), q = __ldg(tb + 1), ab = __ldg(tb + 3);
             rr = r0.x;
             ri = r0.y;
-            if (k0 > 0) {  // advance to event k0 (chirps are a few chunks long)
+            if (k0 > 0) {  // advance to event k0 by q^16 per block (chirps are a block or two long)
               const double2 q8 = __ldg(tb + 2);
-              for (int a8 = 0; a8 < k0; a8 += kChunkSlots) {
+              const double q16r = q8.x * q8.x - q8.y * q8.y, q16i = 2.0 * q8.x * q8.y;
+              for (int a16 = 0; a16 < k0; a16 += kBlk) {
                 const double a = rr;
-                rr = a * q8.x - ri * q8.y;
-                ri = a * q8.y + ri * q8.x;
+                rr = a * q16r - ri * q16i;
+                ri = a * q16i + ri * q16r;
               }
             }
             qc = q.x;
@@ -780,7 +786,6 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
           } else {
             const SC c = load_sc(kp, i);
             const double2 e = cls >= 0 ? relax_pair(kp, cls, i) : make_double2(1.0, 1.0);
-            // rotation factor of event k0 and the per-event phase step (exact per chunk)
             const double b = fma(c.z, ddz, fma(c.y, ddy, c.x * ddx));
             phase_factor(fma(static_cast<double>(k0), b, theta_of(c, dt, d0x, d0y, d0z)), rr, ri);
             phase_factor(b, qc, qs);  // q = exp(-i b) = (qc, qs)
@@ -796,19 +801,22 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
             w[cc] = kp.w != nullptr ? __ldg(reinterpret_cast<const double2*>(kp.w) + static_cast<int64_t>(cc) * kp.n + i)
                                     : make_double2(1.0, 0.0);
 #pragma unroll
-          for (int j = 0; j < kSampPerChunk; ++j) {
-            if (j < ck) {
-              const double nx = x * rr - y * ri;
-              y = x * ri + y * rr;
-              x = nx;
-              z = fma(z, e1, rgw);  // e1 = 1, rgw = 0 without relaxation
-              const double a = rr;
-              rr = a * qc - ri * qs;  // r <- r * q
-              ri = a * qs + ri * qc;
+          for (int h = 0; h < 2; ++h) {
 #pragma unroll
-              for (int cc = 0; cc < NC; ++cc) {
-                ar[j * NC + cc] += static_cast<R>(w[cc].x * x - w[cc].y * y);
-                ai[j * NC + cc] += static_cast<R>(w[cc].x * y + w[cc].y * x);
+            for (int j = 0; j < kSampPerChunk; ++j) {
+              if (h * kSampPerChunk + j < cb) {
+                const double nx = x * rr - y * ri;
+                y = x * ri + y * rr;
+                x = nx;
+                z = fma(z, e1, rgw);  // e1 = 1, rgw = 0 without relaxation
+                const double a = rr;
+                rr = a * qc - ri * qs;  // r <- r * q
+                ri = a * qs + ri * qc;
+#pragma unroll
+                for (int cc = 0; cc < NC; ++cc) {
+                  ar[h][j * NC + cc] += static_cast<R>(w[cc].x * x - w[cc].y * y);
+                  ai[h][j * NC + cc] += static_cast<R>(w[cc].x * y + w[cc].y * x);
+                }
               }
             }
           }
@@ -816,7 +824,8 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
           sp.my(s) = y;
           sp.mz(s) = z;
         }
-        strip.push(ar, ai, ck * NC, (s0 + k0) * NC);
+        strip.push(ar[0], ai[0], min(kSampPerChunk, cb) * NC, (s0 + k0) * NC);
+        if (cb > kSampPerChunk) strip.push(ar[1], ai[1], (cb - kSampPerChunk) * NC, (s0 + k0 + kSampPerChunk) * NC);
       }
       continue;
     }
