@@ -109,9 +109,6 @@ struct Strip {
   }
 };
 
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
-}
 
 // ---------------------------------------------------------------------------
 // spin state (shared memory, [3][S][blockDim] fp64) and per-spin constants
@@ -598,7 +595,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
       // Two-phase per group of G spins: issue every table load of the group
       // before any store, so the L2 round trips overlap instead of serialising
       // behind possibly-aliasing shared/global stores.
-      constexpr int G = S < 2 ? S : 2;
+      constexpr int G = S < 4 ? S : 4;
       if (rc >= 0) {  // repeated interval: tabulated propagator
         const double2* tb = reinterpret_cast<const double2*>(kp.rot) + static_cast<int64_t>(rc) * kp.n * 4;
 #pragma unroll
@@ -836,26 +833,6 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
     {
       const int cnt = __ldg(&op->count), lead = __ldg(&op->aux), s0 = __ldg(&op->s0), rc = __ldg(&op->rot),
                 pre = __ldg(&op->pre);
-      // The sample loop below is long and touches no memory but its partial row:
-      // pull the per-spin records of the ops up to the next window into L2 now.
-      for (int o2 = o + 1; o2 < kp.n_ops && o2 <= o + 8; ++o2) {
-        const DevOp* nx = kp.ops + o2;
-        const int k2 = __ldg(&nx->kind);
-        const int r2 = __ldg(&nx->rot), g2 = __ldg(&nx->prg);
-        const double* base = nullptr;
-        if ((k2 == OP_EVENT || k2 == OP_WINDOW) && r2 >= 0)
-          base = kp.rot + static_cast<int64_t>(r2) * kp.n * 8;
-        else if (k2 == OP_CHIRP && r2 >= 0)
-          base = kp.chirp + static_cast<int64_t>(r2) * kp.n * 8;
-        else if (k2 == OP_EVENT && g2 >= 0)
-          base = kp.prog + static_cast<int64_t>(g2) * kp.n * 8;
-        if (base != nullptr) {
-#pragma unroll
-          for (int s = 0; s < S; ++s)
-            if (sp.act(s)) prefetch_l2(base + sp.idx(s) * 8);
-        }
-        if (k2 == OP_WINDOW) break;
-      }
       if constexpr (!kFull) {
         if (pre >= 0) apply_pre<S>(kp, sp, pre);
       }
