@@ -688,6 +688,33 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
           e1[g] = e.x;
           rg[g] = c.m0 * (1.0 - e.x);
         }
+        if (__ldg(&op->tmode) == 1) {  // x-axis sub-pulses: (x, y, z) -> (x, r4 y + r5 z, r7 y + r8 z)
+          double a4 = __ldg(mats + 4), a5 = __ldg(mats + 5), a7 = __ldg(mats + 7), a8 = __ldg(mats + 8);
+          for (int j = 0; j < cnt; ++j) {
+            const double* mn = mats + 9 * (j + 1 < cnt ? j + 1 : j);
+            const double b4 = __ldg(mn + 4), b5 = __ldg(mn + 5), b7 = __ldg(mn + 7), b8 = __ldg(mn + 8);
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              const double ny = a4 * y[g] + a5 * z[g];
+              const double nz = a7 * y[g] + a8 * z[g];
+              const double nx = x[g];
+              x[g] = nx * zr[g] - ny * zi[g];
+              y[g] = nx * zi[g] + ny * zr[g];
+              z[g] = fma(nz, e1[g], rg[g]);
+            }
+            a4 = b4;
+            a5 = b5;
+            a7 = b7;
+            a8 = b8;
+          }
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            sp.mx(g0 + g) = x[g];
+            sp.my(g0 + g) = y[g];
+            sp.mz(g0 + g) = z[g];
+          }
+          continue;
+        }
         // the pulse matrices are CTA-uniform: prefetch pulse j+1 while applying pulse j
         double r[9], rn[9];
 #pragma unroll

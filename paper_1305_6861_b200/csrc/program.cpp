@@ -127,6 +127,15 @@ void compile_program(const TablesView& t, Program& prog) {
         op.flags = (moving(op.p[0], op.p + 1) ? EV_MOVE : 0) | (op.p[0] != 0.0 ? EV_RELAX : 0);
         op.cls = relax_class(op.p[0]);
         op.rot = -1;
+        // a real envelope (phase 0 or pi, sequence.py:650-674) rotates about x only: the kernel then
+        // needs 4 of the 9 entries.  sin(pi) leaves ~1e-16 off-axis terms, below the 1e-15 cut.
+        op.tmode = 1;
+        for (int32_t j = 0; j < op.count && op.tmode; ++j) {
+          const double* m = prog.mats.data() + 9 * (static_cast<size_t>(op.aux) + j);
+          if (std::fabs(m[0] - 1.0) > 1e-15 || std::fabs(m[1]) > 1e-15 || std::fabs(m[2]) > 1e-15 ||
+              std::fabs(m[3]) > 1e-15 || std::fabs(m[6]) > 1e-15)
+            op.tmode = 0;
+        }
         prog.ops.push_back(op);
         prog.n_events += k - es;
         prog.n_train_ops++;

@@ -54,7 +54,8 @@ struct alignas(16) DevOp {
   int32_t rot;    // rotation class (EVENT: repeated interval; WINDOW: reused run), -1 = none
   int32_t prg;    // EVENT: progression class (interval of an arithmetic series of moments), -1 = none
   int32_t pre;    // EVENT/WINDOW: hard pulse applied first (matrix index into mats, fused OP_ROT), -1 = none
-  int32_t pad[5];
+  int32_t tmode;  // RFTRAIN: 1 = every sub-pulse rotates about the x axis (real envelope), else general
+  int32_t pad[4];
 };
 
 // A rotation class: pre, then `mult` times main, then post (intervals (dt,
