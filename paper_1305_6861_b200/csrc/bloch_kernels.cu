@@ -438,9 +438,9 @@ __device__ __forceinline__ void stage_spin(float4* __restrict__ st, float2* __re
 // The 8 k-blocks (4 spins each) of one staged round into the NT tile
 // accumulators.  The three split products are issued pass-major across the NT
 // independent accumulators so consecutive mma never wait on each other.
-template <int NT>
+template <int NT, int MT>
 __device__ __forceinline__ void mma_round_t(const float4* __restrict__ st, const float2* __restrict__ z64s, int lane,
-                                            float (&acc)[4][4]) {
+                                            float (&acc)[MT][4]) {
   const int g = lane >> 2, t = lane & 3;
 #pragma unroll 2
   for (int kb = 0; kb < 8; ++kb) {
@@ -469,13 +469,19 @@ __device__ __forceinline__ void mma_round_t(const float4* __restrict__ st, const
   }
 }
 
+// MT: tiles per pass (accumulator rows), 8 in the basic kernel, 4 in the full one
+template <int MT>
 __device__ __forceinline__ void mma_round(const float4* __restrict__ st, const float2* __restrict__ z64s, int lane,
-                                          int ntile, float (&acc)[4][4]) {
+                                          int ntile, float (&acc)[MT][4]) {
   switch (ntile) {
-    case 4: mma_round_t<4>(st, z64s, lane, acc); break;
-    case 3: mma_round_t<3>(st, z64s, lane, acc); break;
-    case 2: mma_round_t<2>(st, z64s, lane, acc); break;
-    default: mma_round_t<1>(st, z64s, lane, acc); break;
+    case 8: if constexpr (MT >= 8) mma_round_t<8, MT>(st, z64s, lane, acc); break;
+    case 7: if constexpr (MT >= 7) mma_round_t<7, MT>(st, z64s, lane, acc); break;
+    case 6: if constexpr (MT >= 6) mma_round_t<6, MT>(st, z64s, lane, acc); break;
+    case 5: if constexpr (MT >= 5) mma_round_t<5, MT>(st, z64s, lane, acc); break;
+    case 4: mma_round_t<4, MT>(st, z64s, lane, acc); break;
+    case 3: mma_round_t<3, MT>(st, z64s, lane, acc); break;
+    case 2: mma_round_t<2, MT>(st, z64s, lane, acc); break;
+    default: mma_round_t<1, MT>(st, z64s, lane, acc); break;
   }
 }
 
@@ -973,12 +979,13 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
           float2* out = reinterpret_cast<float2*>(strip.row) + s0;
           const double2* tb = rc >= 0 ? reinterpret_cast<const double2*>(kp.rot) + static_cast<int64_t>(rc) * kp.n * 4
                                       : nullptr;
-          for (int p0 = 0; p0 < cnt; p0 += 256) {  // passes of up to 4 tiles of 64 samples
-            const int ntile = min(4, (cnt - p0 + 63) >> 6);
-            const bool last = p0 + 256 >= cnt;
-            float acc[4][4];
+          constexpr int kMaxTiles = kFull ? 4 : 8;  // 64-sample tiles per pass (4 accumulators each)
+          for (int p0 = 0; p0 < cnt; p0 += 64 * kMaxTiles) {  // passes of up to kMaxTiles tiles of 64 samples
+            const int ntile = min(kMaxTiles, (cnt - p0 + 63) >> 6);
+            const bool last = p0 + 64 * kMaxTiles >= cnt;
+            float acc[kMaxTiles][4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+            for (int j = 0; j < kMaxTiles; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
             if (tb != nullptr && sp.act(0)) {  // (Cpre, z) of round 0 into this lane's prefetch slot
               cp_async16(pf + 2 * lane, tb + sp.idx(0) * 4);
               cp_async16(pf + 2 * lane + 1, tb + sp.idx(0) * 4 + 3);
@@ -1018,8 +1025,10 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
                 z = cf{static_cast<float>(zr0), static_cast<float>(zi0)};
                 if (!lead) u = cmul(u, z);  // first sample after one interval
                 if (p0 > 0) {               // later pass: u z^p0
-                  const cf z256 = csq(csq(csq(csq(csq(csq(csq(csq(z))))))));
-                  for (int q = 0; q < p0; q += 256) u = cmul(u, z256);
+                  cf zp = z;
+#pragma unroll
+                  for (int q = 1; q < 64 * kMaxTiles; q <<= 1) zp = csq(zp);  // z^(64 kMaxTiles)
+                  for (int q = 0; q < p0; q += 64 * kMaxTiles) u = cmul(u, zp);
                 }
                 if (tb == nullptr && last) {  // exit propagator of the whole run, on the fly
                   const int cw = __ldg(&op->flags);
@@ -1033,11 +1042,11 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
               }
               stage_spin(st, z64s, lane, u, z);
               __syncwarp();
-              mma_round(st, z64s, lane, ntile, acc);
+              mma_round<kMaxTiles>(st, z64s, lane, ntile, acc);
               __syncwarp();  // the stage is rewritten by the next round
             }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < kMaxTiles; ++j) {
               if (j < ntile) {
                 const int k1 = p0 + 64 * j + 16 * t + g, k2 = k1 + 8;
                 if (k1 < cnt) __stcs(out + k1, make_float2(acc[j][0], acc[j][2]));
