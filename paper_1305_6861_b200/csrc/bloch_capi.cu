@@ -96,8 +96,9 @@ struct Variant {
   bool full = true;  // program uses RF trains / chirps / generic sampled events
 };
 
-// pick (S, NC) for a block of n spins with ncp (power-of-two) coils
-Variant pick_variant(int prec, int64_t n, int ncp, int n_sm) {
+// pick (S, NC) for a block of n spins with ncp (power-of-two) coils; max_window: the longest
+// uniform ADC window of the program (samples)
+Variant pick_variant(int prec, int64_t n, int ncp, int n_sm, int max_window) {
   if (prec == BLOCH_PREC_F32) {
     switch (ncp) {
       case 1: {
@@ -106,7 +107,10 @@ Variant pick_variant(int prec, int64_t n, int ncp, int n_sm) {
           return e ? atoi(e) : 0;
         }();
         if (force_s == 4 || force_s == 8) return {32, force_s, 1};
-        return {32, n >= int64_t(n_sm) * 8 * 64 ? 8 : 2, 1};
+        if (n < int64_t(n_sm) * 8 * 64) return {32, 2, 1};
+        // measured (B200): 256-sample windows run fastest with 8 spins per thread (config 1:
+        // 10.25 vs 10.90 ms), 512-sample windows with 4 (config 2: 35.0 vs 38.1 ms)
+        return {32, max_window >= 384 ? 4 : 8, 1};
       }
       case 2: return {32, 4, 2};
       case 4: return {32, 4, 4};
@@ -454,7 +458,10 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
     // 4. integrator + ordered fold
     float kms = 0.f;
     if (n > 0) {
-      Variant v = pick_variant(c->precision, n, ncp, c->n_sm);
+      int max_window = 0;
+      for (const bloch::DevOp& op : P.ops)
+        if (op.kind == bloch::OP_WINDOW) max_window = std::max(max_window, static_cast<int>(op.count));
+      Variant v = pick_variant(c->precision, n, ncp, c->n_sm, max_window);
       v.full = false;
       for (const bloch::DevOp& op : P.ops)
         if (op.kind == bloch::OP_RFTRAIN || op.kind == bloch::OP_CHIRP || op.kind == bloch::OP_GSAMP) v.full = true;

@@ -62,7 +62,7 @@ struct KernelTraits<float, 8, 1> {  // the fp32 single-coil workhorse: 2 CTAs x 
   X(double, 1, 8)
 
 template <>
-struct KernelTraits<float, 4, 1> {  // experiment: 2 CTAs x 12 warps, 4 spins per thread
+struct KernelTraits<float, 4, 1> {  // long windows (>= 384 samples): 2 CTAs x 12 warps, 4 spins per thread
   static constexpr int kMaxThreads = 384;
   static constexpr int kMinBlocks = 2;
 };
