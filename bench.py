@@ -391,7 +391,8 @@ def main():
         "metric": metric, "value": value, "unit": metric, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_total_s * 1e3 / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None,
-        "dtype": "f32 ADC recurrence, f64 spin state/phase/signal" if args.precision == 32 else "f64",
+        "dtype": ("f64 spin state/phase/fold; f32 ADC sums (3-pass split tf32 on the tensor cores)"
+                  if args.precision == 32 else "f64"),
         "data": "synthetic (seeded, BASELINE.json config recipe)",
         "config": {"workload": w.name, "config_index": w.index, "spins_total": w.n_spins, "spins_per_rank": n_local,
                    "events_per_spin": E, "coils": C, "event_classes": counts, "program": pstats,
