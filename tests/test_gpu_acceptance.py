@@ -1,0 +1,118 @@
+"""Reference acceptance criteria that pin the event arithmetic, restated through the GPU engine.
+
+* criterion 1 (reference tests/test_acceptance.py:73-119): the three event kinds the kernel
+  applies — precession with relaxation, a hard pulse, a gradient interval with relaxation —
+  against an independent 4th-order Runge-Kutta integration of the Bloch equation
+  dM/dt = gamma M x B - relaxation (the reference's ODE oracle, tests/oracles.py:42-67,
+  restated here), rel error <= 1e-6;
+* criterion 4 (tests/test_acceptance.py:234-255): Hahn echo peak = M0 exp(-TE/T2) within 1e-4
+  through run(Experiment).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from paper_1305_6861_b200 import (
+    GAMMA_PROTON,
+    ElementarySequence,
+    Experiment,
+    GradientWaveform,
+    HardPulse,
+    Phantom,
+    PhantomBox,
+    Sequence,
+    SpinBlock,
+    build_spin_echo,
+    compute_block,
+    precompute_sequence_tables,
+    readout_gradient,
+    run,
+)
+
+pytestmark = pytest.mark.gpu
+
+
+def rk4_bloch(m, b, gamma, t1, t2, m0, dt, steps):
+    """Classical RK4 of dM/dt = gamma M x B - (Mx/T2, My/T2, (Mz - M0)/T1), one row per case."""
+    m = np.array(m, dtype=float)
+    h = (np.asarray(dt, float) / steps)[:, None]
+
+    def f(s):
+        d = gamma * np.cross(s, b)
+        d[:, 0] -= s[:, 0] / t2
+        d[:, 1] -= s[:, 1] / t2
+        d[:, 2] -= (s[:, 2] - m0) / t1
+        return d
+
+    for _ in range(steps):
+        k1 = f(m)
+        k2 = f(m + 0.5 * h * k1)
+        k3 = f(m + 0.5 * h * k2)
+        k4 = f(m + h * k3)
+        m = m + (h / 6.0) * (k1 + 2 * k2 + 2 * k3 + k4)
+    return m
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+def test_event_kinds_match_ode(precision):
+    rng = np.random.default_rng(20240901)
+    n = 60
+    start = rng.uniform(-1.0, 1.0, size=(n, 3))
+    start /= np.maximum(np.linalg.norm(start, axis=1, keepdims=True), 1.0)
+    kinds = rng.integers(0, 3, size=n)
+    t1 = rng.uniform(0.05, 2.0, size=n)
+    t2 = np.minimum(rng.uniform(0.02, 1.0, size=n), t1)
+    m0 = rng.uniform(0.0, 1.0, size=n)
+    dt = rng.uniform(1e-4, 10e-3, size=n)
+    b = np.zeros((n, 3))
+    got = np.zeros((n, 3))
+    for i in range(n):
+        pos = np.zeros((1, 3))
+        dw = 0.0
+        if kinds[i] == 0:  # free precession with relaxation: off-resonance dw
+            dw = rng.uniform(-2 * math.pi * 400, 2 * math.pi * 400)
+            es = ElementarySequence(duration=dt[i])
+            b[i] = (0.0, 0.0, dw / GAMMA_PROTON)
+        elif kinds[i] == 1:  # hard pulse, relaxation-free (T1 = T2 = 1e9, M0 = 0)
+            alpha, phi = rng.uniform(0.05, math.pi), rng.uniform(0.0, 2 * math.pi)
+            dt[i] = 1e-4
+            t1[i] = t2[i] = 1e9
+            m0[i] = 0.0
+            es = ElementarySequence(pulse=HardPulse(alpha, phi), duration=dt[i])
+            b1 = alpha / (GAMMA_PROTON * dt[i])  # the same rotation as a B1 field held for dt
+            b[i] = (b1 * math.cos(phi), b1 * math.sin(phi), 0.0)
+        else:  # gradient interval with relaxation: a spin at z = 1 m under gz, moment = rotation angle
+            moment = rng.uniform(-25.0, 25.0)
+            gz = moment / (GAMMA_PROTON * dt[i])
+            pos[0, 2] = 1.0
+            es = ElementarySequence(gradient=GradientWaveform.constant(gz=gz), duration=dt[i])
+            b[i] = (0.0, 0.0, gz)
+        seq = Sequence([es], name=f"case{i}")
+        tables = precompute_sequence_tables(seq, snapshot_times=(seq.end_time,))
+        blk = SpinBlock(index=0, pos=pos, mx=start[i, :1].copy(), my=start[i, 1:2].copy(), mz=start[i, 2:].copy(),
+                        t1=t1[i:i + 1].copy(), t2=t2[i:i + 1].copy(), m0=m0[i:i + 1].copy(),
+                        domega=np.array([dw]), weight=np.array([1.0 + 0.0j]))
+        _, snaps = compute_block(tables, blk, precision=precision)
+        got[i] = snaps[0][0]
+    ref = rk4_bloch(start, b, GAMMA_PROTON, t1, t2, m0, dt, steps=4000)
+    rel = np.linalg.norm(got - ref, axis=1) / np.maximum(np.linalg.norm(ref, axis=1), 1e-9)
+    assert rel.max() <= 1e-6, f"worst rel err {rel.max():.2e} (precision {precision})"
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+def test_hahn_echo_amplitude(precision):
+    t2 = 0.2
+    worst = 0.0
+    for te in (0.02, 0.05, 0.1):
+        n = 65  # odd: one sample falls exactly on the echo
+        seq = build_spin_echo(fov=0.5, n=n, te=te, tr=te + 1.0, readout_grad=readout_gradient(0.5, n, te / 2))
+        one = Sequence(seq.elements[:4], name="one_rep")
+        ph = Phantom([PhantomBox(origin=(-1e-4,) * 3, size=(2e-4,) * 3, m0=1.0, t1=1.0, t2=t2)])
+        res = run(Experiment(sequence=one, phantom=ph, spacing=(1e-3,) * 3, precision=precision))
+        rec = res.echoes[0]
+        mid = (n - 1) // 2
+        assert rec.timestamps[mid] == pytest.approx(te, rel=1e-12)
+        worst = max(worst, abs(abs(rec.values[mid]) / math.exp(-te / t2) - 1.0))
+    assert worst <= 1e-4, f"worst rel deviation {worst:.2e}"
