@@ -23,6 +23,7 @@ BLOCH_PREC_F64 = 64
 BLOCH_IN_DEVICE = 1
 BLOCH_OUT_DEVICE = 2
 BLOCH_NO_SYNC = 4
+BLOCH_HOST_ONLY = -1
 
 
 class BoxT(ctypes.Structure):

@@ -12,6 +12,7 @@
 #include <array>
 #include <functional>
 #include <map>
+#include <set>
 #include <cmath>
 #include <stdexcept>
 #include <string>
@@ -379,8 +380,22 @@ void fuse_intervals(Program& prog, const std::function<int32_t(double)>& relax_c
     if (items[k].op.kind == OP_WINDOW && post_of[k] && k + 2 < n_items && pre_of[k + 2]) pre_of[k + 2] = 0;
   for (size_t k = 0; k < n_items; ++k)
     if (items[k].op.kind == OP_WINDOW && !items[k].interval) win_uses[win_key(k, pre_of[k], post_of[k])]++;
+  // absorbing keys reused often enough, most reused first, within the class cap: a window may only absorb
+  // its neighbours if its whole (pre, window, post) run gets a tabulated class
+  std::vector<std::pair<int64_t, RotKey>> absorbing;
+  for (const auto& kv : win_uses) {
+    const RotKey& key = kv.first;
+    const bool absorbs = std::any_of(key.begin(), key.begin() + 4, [](double v) { return v != 0.0; }) ||
+                         std::any_of(key.begin() + 9, key.end(), [](double v) { return v != 0.0; });
+    if (absorbs && kv.second >= kMinReuse) absorbing.push_back({-kv.second, key});
+  }
+  std::sort(absorbing.begin(), absorbing.end());
+  if (absorbing.size() > kMaxRotClasses) absorbing.resize(kMaxRotClasses);
+  std::set<RotKey> classed_absorbing;
+  for (const auto& a : absorbing) classed_absorbing.insert(a.second);
   for (size_t k = 0; k < n_items; ++k)
-    if (items[k].op.kind == OP_WINDOW && !items[k].interval && win_uses[win_key(k, pre_of[k], post_of[k])] < kMinReuse)
+    if (items[k].op.kind == OP_WINDOW && !items[k].interval && (pre_of[k] || post_of[k]) &&
+        !classed_absorbing.count(win_key(k, pre_of[k], post_of[k])))
       pre_of[k] = post_of[k] = 0;
   std::vector<bool> absorbed(n_items, false);
   for (size_t k = 0; k < n_items; ++k) {
@@ -413,7 +428,9 @@ void fuse_intervals(Program& prog, const std::function<int32_t(double)>& relax_c
     return c;
   };
 
-  // 3. emit; windows first claim classes in order of reuse (most reused first)
+  // 3. emit; the absorbing windows claim their classes first, then the remaining windows and the
+  // reused intervals in order of reuse (most reused first)
+  for (const auto& a : absorbing) rot_class(a.second);
   std::vector<std::pair<int64_t, RotKey>> order;
   for (const auto& kv : plain_win_uses) order.push_back({-kv.second, kv.first});
   for (const auto& kv : iv_uses)

@@ -116,3 +116,72 @@ def test_hahn_echo_amplitude(precision):
         assert rec.timestamps[mid] == pytest.approx(te, rel=1e-12)
         worst = max(worst, abs(abs(rec.values[mid]) / math.exp(-te / t2) - 1.0))
     assert worst <= 1e-4, f"worst rel deviation {worst:.2e}"
+
+
+# -- image-level criteria through run(Experiment) + GPU reconstruction ----------------------------
+# run() needs an explicit spacing here (the spacing analysis, mrsim.discretize, is out of scope); these are the
+# spacings the reference's analysis returns for the two setups (computed with the reference in the build container).
+C7_SPACING = (0.006349206349206349, 0.0063492063492063475, 0.002)
+C9_SPACING = (0.004761904761904762, 0.004761904761904762, 0.002)
+
+
+def _thin_box(x0, y0, sx, sy, **props):
+    return PhantomBox(origin=(x0, y0, -5e-4), size=(sx, sy, 1e-3), **props)
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+def test_tse_ghost(precision):
+    """Criterion 7 (tests/test_acceptance.py:382-416): TSE turbo factor 2 ghost half a matrix away, ghost/main
+    ratio (1 - q)/(1 + q), q = exp(-ESP/T2), within 20%."""
+    from paper_1305_6861_b200 import build_tse
+    from paper_1305_6861_b200.recon import assemble_kspace, reconstruct
+
+    fov, n, t2, esp = 0.5, 64, 0.2, 0.06
+    seq = build_tse(fov=fov, n=n, turbo_factor=2, echo_spacing=esp, tr=2.5, readout_grad=0.239e-3)
+    ph = Phantom([_thin_box(-0.08, -0.06, 0.16, 0.12, m0=1.0, t1=1.0, t2=t2)])
+    res = run(Experiment(sequence=seq, phantom=ph, spacing=C7_SPACING, precision=precision))
+    assert res.spin_count == 450
+    k = assemble_kspace(res.echo_matrix(), seq.trajectory_table(), n_rows=n, fov=fov)[0]
+    mag = reconstruct(k, device="cuda").magnitude
+    rolled = np.roll(mag, n // 2, axis=0)
+    rows = np.arange(n)
+    band = slice(n // 2 - 10, n // 2 + 10)
+    main_p, ghost_p = mag.sum(axis=1), rolled.sum(axis=1)
+    main_c = (rows[band] * main_p[band]).sum() / main_p[band].sum()
+    ghost_c = (rows[band] * ghost_p[band]).sum() / ghost_p[band].sum()
+    offset = (ghost_c + n // 2 - main_c) % n
+    q = math.exp(-esp / t2)
+    predicted = (1.0 - q) / (1.0 + q)
+    center = slice(n // 2 - 8, n // 2 + 8)
+    measured = rolled[center, center].max() / mag[center, center].max()
+    assert abs(offset - n / 2) <= 1.0
+    assert abs(measured / predicted - 1.0) <= 0.20
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+def test_cpmg_t2_mapping(precision):
+    """Criterion 9 (tests/test_acceptance.py:458-504): 12-echo CPMG, per-probe rho and T2 from the GPU
+    k-space -> assembly -> GPU reconstruction -> exponential fit, within 2%."""
+    from paper_1305_6861_b200 import build_cpmg
+    from paper_1305_6861_b200.recon import assemble_kspace, cpmg_fit, reconstruct
+
+    fov, n = 0.375, 64
+    seq = build_cpmg(fov=fov, n=n, n_echoes=12, dte=0.02, tr=2.0, readout_grad=readout_gradient(fov, n, 0.012))
+    probes = [((-0.09, -0.09), 0.9, 0.05), ((+0.09, -0.09), 0.7, 0.10), ((-0.09, +0.09), 0.5, 0.15),
+              ((+0.09, +0.09), 0.3, 0.20)]
+    size = 0.09
+    ph = Phantom([_thin_box(cx - size / 2, cy - size / 2, size, size, m0=m0, t1=0.3, t2=t2)
+                  for (cx, cy), m0, t2 in probes])
+    res = run(Experiment(sequence=seq, phantom=ph, spacing=C9_SPACING, precision=precision))
+    assert res.spin_count == 1296
+    vols = assemble_kspace(res.echo_matrix(), seq.trajectory_table(), n_rows=n, fov=fov)
+    images = [reconstruct(k, device="cuda") for k in vols]
+    scale = (fov * fov) / (n * n * res.spin_count * res.spacing[0] * res.spacing[1])
+    te = np.array(seq.meta["echo_times"])
+    xs, ys = images[0].axis_coords(1), images[0].axis_coords(0)
+    for (cx, cy), m0, t2 in probes:
+        mask = (np.abs(xs[None, :] - cx) <= 0.03) & (np.abs(ys[:, None] - cy) <= 0.03)
+        series = np.array([img.magnitude[mask].mean() for img in images])
+        fit = cpmg_fit(te, series)
+        assert abs(fit.rho / scale / m0 - 1.0) <= 0.02, (cx, cy, fit)
+        assert abs(fit.t2 / t2 - 1.0) <= 0.02, (cx, cy, fit)

@@ -179,3 +179,26 @@ def test_empty_and_single_sample_windows(host_engine):
     host_engine.set_tables(tables)
     st = host_engine.program_stats()
     assert st["samples"] == 1 and st["events"] == event_counts(tables)["events"]
+
+
+def test_compiler_class_cap_with_absorbing_windows():
+    """More reused (pre, window, post) runs than rotation-class slots: the windows beyond the cap must
+    keep their neighbouring intervals separate (regression: 'absorbing window without a class')."""
+    import ctypes
+
+    from paper_1305_6861_b200 import build_cpmg, readout_gradient
+    from paper_1305_6861_b200.engine import BlochEngine, precompute_sequence_tables
+
+    seq = build_cpmg(fov=0.375, n=64, n_echoes=12, dte=0.02, tr=2.0, readout_grad=readout_gradient(0.375, 64, 0.012))
+    eng = BlochEngine.__new__(BlochEngine)
+    lib = _capi.load()
+    eng._lib, eng.device, eng.precision, eng._tables_ref, eng._flat = lib, _capi.BLOCH_HOST_ONLY, 32, None, None
+    h = ctypes.c_void_p()
+    _capi.check(lib.bloch_create(_capi.BLOCH_HOST_ONLY, 32, ctypes.byref(h)), "bloch_create")
+    eng._h = h
+    try:
+        eng.set_tables(precompute_sequence_tables(seq))
+        st = eng.program_stats()
+    finally:
+        eng.close()
+    assert st["rot_classes"] == 64 and st["window_samples"] == 64 * 12 * 64
