@@ -185,3 +185,37 @@ def test_cpmg_t2_mapping(precision):
         fit = cpmg_fit(te, series)
         assert abs(fit.rho / scale / m0 - 1.0) <= 0.02, (cx, cy, fit)
         assert abs(fit.t2 / t2 - 1.0) <= 0.02, (cx, cy, fit)
+
+
+def _kt_case(g, i):
+    """Sequence i of tests/golden/kt_random.npz rebuilt with this package (make_golden_kt.py)."""
+    from paper_1305_6861_b200 import AcquisitionSpec
+
+    els = []
+    for alpha, phi, q, dt in g[f"seq{i}_rows"]:
+        els.append(ElementarySequence(pulse=HardPulse(alpha, phi),
+                                      gradient=GradientWaveform.constant(gx=q * 80.0 / (GAMMA_PROTON * dt)), duration=dt))
+    els.append(ElementarySequence(gradient=GradientWaveform.constant(gx=4 * 80.0 / (GAMMA_PROTON * 0.01)), duration=0.01,
+                                  acquisition=AcquisitionSpec(True, 33), kspace_row=0))
+    return Sequence(els, name="random")
+
+
+@pytest.mark.parametrize("precision,tol", [(64, 1e-6), (32, 2e-5)])
+def test_spin_engine_vs_kt_engine(precision, tol):
+    """Criterion 2 (tests/test_acceptance.py:127-184): the GPU spin engine against the reference's k-t
+    (configuration-population) engine on seeded random sequences, homogeneous field."""
+    import os
+
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "kt_random.npz"))
+    pos, m0 = g["pos"], g["m0"]
+    n = m0.size
+    blk = SpinBlock(index=0, pos=pos, mx=np.zeros(n), my=np.zeros(n), mz=m0.copy(), t1=np.full(n, float(g["t1"])),
+                    t2=np.full(n, float(g["t2"])), m0=m0.copy(), domega=np.zeros(n), weight=np.full(n, 1 + 0j))
+    worst = 0.0
+    for i in range(int(g["n_seq"])):
+        seq = _kt_case(g, i)
+        echoes, _ = compute_block(precompute_sequence_tables(seq), blk, precision=precision)
+        spin = np.asarray(echoes).ravel()[: g[f"seq{i}_kt"].size] / n
+        kt = g[f"seq{i}_kt"]
+        worst = max(worst, np.linalg.norm(spin - kt) / np.linalg.norm(spin))
+    assert worst <= tol, f"worst rel L2 {worst:.2e}"

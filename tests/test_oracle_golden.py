@@ -119,3 +119,29 @@ def test_delta_e_stoer_and_rel_l2():  # engine.py:603-616; test_engine.py:277-29
     assert O.delta_e_stoer(ref, ref * (1 + 1e-6)) == pytest.approx(-120.0, abs=0.5)
     assert O.delta_e_stoer(np.array([1.0, 2.0, 3.0]), np.zeros(3)) == pytest.approx(0.0, abs=1e-12)
     assert O.rel_l2(ref, ref * (1 + 1e-4)) == pytest.approx(1e-4, rel=1e-6)
+
+
+def test_oracle_vs_kt_engine():
+    """The float64 oracle against the reference's independent k-t engine (golden kt_random.npz,
+    criterion 2 of the reference's acceptance tests): a second, algorithmically different pin."""
+    import math
+    import os
+
+    from paper_1305_6861_b200 import (GAMMA_PROTON, AcquisitionSpec, ElementarySequence, GradientWaveform,
+                                      HardPulse, Sequence)
+
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "kt_random.npz"))
+    pos, m0 = g["pos"], g["m0"]
+    n = m0.size
+    worst = 0.0
+    for i in range(int(g["n_seq"])):
+        els = [ElementarySequence(pulse=HardPulse(a, p), gradient=GradientWaveform.constant(gx=q * 80.0 / (GAMMA_PROTON * dt)),
+                                  duration=dt) for a, p, q, dt in g[f"seq{i}_rows"]]
+        els.append(ElementarySequence(gradient=GradientWaveform.constant(gx=4 * 80.0 / (GAMMA_PROTON * 0.01)),
+                                      duration=0.01, acquisition=AcquisitionSpec(True, 33), kspace_row=0))
+        tabs = O.precompute_tables(Sequence(els, name="random"))
+        e, _ = O.compute_block(tabs, pos, np.zeros(n), np.zeros(n), m0.copy(), np.full(n, float(g["t1"])),
+                               np.full(n, float(g["t2"])), m0.copy(), np.zeros(n), np.full(n, 1 + 0j))
+        spin = np.asarray(e).ravel()[: g[f"seq{i}_kt"].size] / n
+        worst = max(worst, np.linalg.norm(spin - g[f"seq{i}_kt"]) / np.linalg.norm(spin))
+    assert worst <= 1e-6 and math.isfinite(worst)
