@@ -192,8 +192,26 @@ __device__ __forceinline__ void interval(const KParams& kp, Spins<S>& sp, int s,
 
 // the fused pulse on its own pass over the state (paths that do not load the state anyway)
 template <int S>
-__device__ __forceinline__ void apply_pre(const KParams& kp, Spins<S>& sp, int pre) {
+__device__ __forceinline__ void apply_pre(const KParams& kp, Spins<S>& sp, int pre, int mode) {
   const Mat3 m = load_mat(kp, pre);
+  if (mode == 1) {  // about x: (x, r4 y + r5 z, r7 y + r8 z)
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const double y = sp.my(s), z = sp.mz(s);
+      sp.my(s) = m.r[4] * y + m.r[5] * z;
+      sp.mz(s) = m.r[7] * y + m.r[8] * z;
+    }
+    return;
+  }
+  if (mode == 2) {  // about y: (r0 x + r2 z, y, r6 x + r8 z)
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const double x = sp.mx(s), z = sp.mz(s);
+      sp.mx(s) = m.r[0] * x + m.r[2] * z;
+      sp.mz(s) = m.r[6] * x + m.r[8] * z;
+    }
+    return;
+  }
 #pragma unroll
   for (int s = 0; s < S; ++s) {
     double x = sp.mx(s), y = sp.my(s), z = sp.mz(s);
@@ -596,7 +614,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
       const int flags = __ldg(&op->count), snap = __ldg(&op->aux), cls = __ldg(&op->cls), rc = __ldg(&op->rot),
                 pg = __ldg(&op->prg), pre = __ldg(&op->pre);
       if constexpr (!kFull) {  // a fused pulse (basic programs only): its own pass over the state
-        if (pre >= 0) apply_pre<S>(kp, sp, pre);
+        if (pre >= 0) apply_pre<S>(kp, sp, pre, __ldg(&op->tmode));
       }
       // Two-phase per group of G spins: issue every table load of the group
       // before any store, so the L2 round trips overlap instead of serialising
@@ -867,7 +885,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
       const int cnt = __ldg(&op->count), lead = __ldg(&op->aux), s0 = __ldg(&op->s0), rc = __ldg(&op->rot),
                 pre = __ldg(&op->pre);
       if constexpr (!kFull) {
-        if (pre >= 0) apply_pre<S>(kp, sp, pre);
+        if (pre >= 0) apply_pre<S>(kp, sp, pre, __ldg(&op->tmode));
       }
       if constexpr (sizeof(R) == 4 && NC >= 2) {
         if (cnt >= kMmaMinWindow && kp.w32 != nullptr) {  // tensor-core multi-coil window

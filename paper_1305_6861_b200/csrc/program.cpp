@@ -499,6 +499,15 @@ void fuse_pulses(Program& prog) {
       DevOp next = prog.ops[k + 1];
       next.pre = static_cast<int32_t>(prog.mats.size() / 9);
       prog.mats.insert(prog.mats.end(), op.p, op.p + 9);
+      // hard pulses about x (phi = 0) or y (phi = pi/2; cos(pi/2) leaves ~6e-17 terms): 4-entry rotation
+      const double* m = op.p;
+      auto tiny = [](double v) { return std::fabs(v) <= 1e-15; };
+      if (tiny(m[0] - 1.0) && tiny(m[1]) && tiny(m[2]) && tiny(m[3]) && tiny(m[6]))
+        next.tmode = 1;
+      else if (tiny(m[4] - 1.0) && tiny(m[1]) && tiny(m[3]) && tiny(m[5]) && tiny(m[7]))
+        next.tmode = 2;
+      else
+        next.tmode = 0;
       out.push_back(next);
       prog.n_fused_pulses++;
       ++k;

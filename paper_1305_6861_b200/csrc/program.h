@@ -54,7 +54,7 @@ struct alignas(16) DevOp {
   int32_t rot;    // rotation class (EVENT: repeated interval; WINDOW: reused run), -1 = none
   int32_t prg;    // EVENT: progression class (interval of an arithmetic series of moments), -1 = none
   int32_t pre;    // EVENT/WINDOW: hard pulse applied first (matrix index into mats, fused OP_ROT), -1 = none
-  int32_t tmode;  // RFTRAIN: 1 = every sub-pulse rotates about the x axis (real envelope), else general
+  int32_t tmode;  // RFTRAIN: 1 = every sub-pulse rotates about x (real envelope); EVENT/WINDOW: axis of `pre` (1 x, 2 y, 0 general)
   int32_t pad[4];
 };
 
