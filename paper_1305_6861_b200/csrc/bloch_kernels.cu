@@ -818,13 +818,16 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
             const double2 r0 = __ldg(tb), q = __ldg(tb + 1), ab = __ldg(tb + 3);
             rr = r0.x;
             ri = r0.y;
-            if (k0 > 0) {  // advance to event k0 by q^16 per block (chirps are a block or two long)
-              const double2 q8 = __ldg(tb + 2);
-              const double q16r = q8.x * q8.x - q8.y * q8.y, q16i = 2.0 * q8.x * q8.y;
-              for (int a16 = 0; a16 < k0; a16 += kBlk) {
-                const double a = rr;
-                rr = a * q16r - ri * q16i;
-                ri = a * q16i + ri * q16r;
+            if (k0 > 0) {  // advance to event k0 by q^kBlk per block (chirps are a block or two long)
+              // kBlk = 16 / NC events per block: q^kBlk from the tabulated q^8 (NC <= 2) or from q (NC >= 4)
+              double2 qb = kBlk >= 8 ? __ldg(tb + 2) : q;
+#pragma unroll
+              for (int m = kBlk >= 8 ? 8 : 1; m < kBlk; m <<= 1)
+                qb = make_double2(qb.x * qb.x - qb.y * qb.y, 2.0 * qb.x * qb.y);
+              for (int a = 0; a < k0; a += kBlk) {
+                const double r0r = rr;
+                rr = r0r * qb.x - ri * qb.y;
+                ri = r0r * qb.y + ri * qb.x;
               }
             }
             qc = q.x;

@@ -72,7 +72,14 @@ void compile_program(const TablesView& t, Program& prog) {
   }
   for (int64_t i = 0; i < E; ++i) {
     if (t.ev_snap[i] >= t.n_snap) throw std::invalid_argument("ev_snap out of range");
-    if (!(t.ev_dt[i] >= 0.0)) throw std::invalid_argument("negative or NaN event interval");
+    // The reference's own tables can hold a -1e-18 s interval: a snapshot at the sequence end that the
+    // running clock places a rounding step inside the last elementary sequence leaves a negative
+    // remainder, which compute_block applies as is.  Rejected: non-finite values and intervals more
+    // negative than such a rounding residue.
+    if (!std::isfinite(t.ev_dt[i]) || t.ev_dt[i] < -1e-12)
+      throw std::invalid_argument("negative (beyond rounding) or non-finite event interval");
+    for (int a = 0; a < 3; ++a)
+      if (!std::isfinite(t.ev_dmom[3 * i + a])) throw std::invalid_argument("non-finite event moment");
   }
 
   auto dm = [&](int64_t i) { return t.ev_dmom + 3 * i; };

@@ -1,0 +1,151 @@
+"""Seeded random sequences through the GPU engine vs the float64 oracle.
+
+The program compiler (csrc/program.cpp) turns the event stream into windows,
+chirps, RF trains, rotation/progression/chirp classes, fused intervals and
+fused pulses; each pass has its own conditions.  This fuzzer builds random
+sequences out of the structures that trigger them — repeated TR blocks with an
+arithmetic phase-encode series (progressions), constant/trapezoid/sampled
+readouts under the ADC (windows, chirps, generic samples), shaped pulses with
+real and complex envelopes (RF trains, general and x-axis), hard pulses about
+x/y/arbitrary axes (fused pulses), snapshots anywhere — and checks the k-space
+and every snapshot against the oracle (oracle/bloch_oracle.py) in both
+precision modes.  A separate CPU test compiles many more seeds on a host-only
+context (no GPU) to catch compiler exceptions.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import bloch_oracle as O
+from paper_1305_6861_b200 import (
+    GAMMA_PROTON,
+    AcquisitionSpec,
+    ElementarySequence,
+    GradientWaveform,
+    HardPulse,
+    Sequence,
+    SpinBlock,
+    compute_block,
+    expand_shaped_pulse,
+    precompute_sequence_tables,
+)
+
+
+def random_gradient(rng, dur):
+    kind = rng.integers(0, 4)
+    amp = lambda: float(rng.uniform(-2e-3, 2e-3)) * (rng.random() < 0.7)  # noqa: E731
+    if kind == 0:
+        return GradientWaveform.none()
+    if kind == 1:
+        return GradientWaveform.constant(gx=amp(), gy=amp(), gz=amp())
+    if kind == 2:
+        ramp = dur * float(rng.uniform(0.05, 0.3))
+        return GradientWaveform.trapezoid(gx=amp(), gy=amp(), ramp_s=ramp, flat_s=dur - 2 * ramp)
+    m = int(rng.integers(2, 9))
+    return GradientWaveform.from_samples(rng.uniform(-1e-3, 1e-3, size=(m, 3)), dur / m)
+
+
+def random_es(rng, row):
+    dur = float(rng.uniform(5e-5, 4e-3))
+    pulse = None
+    if rng.random() < 0.25:
+        phi = [0.0, math.pi / 2, float(rng.uniform(0, 2 * math.pi))][int(rng.integers(0, 3))]
+        pulse = HardPulse(float(rng.uniform(0.05, math.pi)), phi)
+    acq = AcquisitionSpec(True, int(rng.integers(1, 80))) if rng.random() < 0.3 else AcquisitionSpec(False, 0)
+    return ElementarySequence(pulse=pulse, gradient=random_gradient(rng, dur), duration=dur, acquisition=acq,
+                              kspace_row=row if acq.enabled else None)
+
+
+def random_sequence(seed):
+    rng = np.random.default_rng(seed)
+    els, row = [], 0
+    # a TR block repeated with an arithmetic phase-encode series (progressions, window and interval classes)
+    reps = int(rng.integers(1, 9))
+    n_read = int(rng.integers(8, 70))
+    read_dur = float(rng.uniform(2e-4, 2e-3))
+    g_read = float(rng.uniform(-3e-3, 3e-3))
+    trap = rng.random() < 0.4
+    pe_step = float(rng.uniform(-4e-4, 4e-4))
+    for r in range(reps):
+        els.append(ElementarySequence(pulse=HardPulse(math.pi / 2, 0.0), duration=float(rng.uniform(1e-4, 1e-3))))
+        els.append(ElementarySequence(gradient=GradientWaveform.constant(gy=(r - reps / 2) * pe_step, gx=-g_read / 2),
+                                      duration=5e-4))
+        if rng.random() < 0.5:
+            els.append(ElementarySequence(pulse=HardPulse(math.pi, math.pi / 2), duration=2e-4))
+        grad = (GradientWaveform.trapezoid(gx=g_read, ramp_s=read_dur * 0.2, flat_s=read_dur * 0.6) if trap
+                else GradientWaveform.constant(gx=g_read))
+        els.append(ElementarySequence(gradient=grad, duration=read_dur, acquisition=AcquisitionSpec(True, n_read),
+                                      kspace_row=row))
+        row += 1
+        els.append(ElementarySequence(duration=float(rng.uniform(1e-3, 5e-3))))
+    # a shaped pulse (RF train), real or complex envelope
+    if rng.random() < 0.6:
+        m = int(rng.integers(4, 40))
+        env = np.sinc(np.linspace(-2, 2, m)) * 2e-6
+        if rng.random() < 0.4:
+            env = env * np.exp(1j * np.linspace(0, float(rng.uniform(0, 3)), m))
+        els.extend(expand_shaped_pulse(env, 1e-5, GradientWaveform.constant(gz=float(rng.uniform(-5e-3, 5e-3)))))
+    # free-form tail
+    for _ in range(int(rng.integers(2, 12))):
+        es = random_es(rng, row)
+        if es.acquisition.enabled:
+            row += 1
+        els.append(es)
+    return Sequence(els, name=f"fuzz{seed}")
+
+
+def random_spins(seed, n=48):
+    """Spins of seed: uniform 1+0j receive weight, a non-uniform single-coil weight, or 3 coils (seed % 3)."""
+    rng = np.random.default_rng(seed + 1000)
+    m0 = rng.uniform(0.2, 1.0, n)
+    cplx = lambda *sh: rng.uniform(0.3, 1.0, sh) * np.exp(1j * rng.uniform(0, 2 * math.pi, sh))  # noqa: E731
+    w = [np.full(n, 1 + 0j), cplx(n), cplx(3, n)][seed % 3]
+    return SpinBlock(index=0, pos=rng.uniform(-0.05, 0.05, (n, 3)), mx=np.zeros(n), my=np.zeros(n), mz=m0.copy(),
+                     t1=rng.uniform(0.3, 1.5, n), t2=rng.uniform(0.02, 0.3, n), m0=m0,
+                     domega=rng.normal(0.0, 2 * math.pi * 30, n), weight=w)
+
+
+def test_compiler_accepts_random_sequences():
+    """Host-only compile of many random programs: no compiler exception, consistent statistics."""
+    import ctypes
+
+    from paper_1305_6861_b200 import _capi
+    from paper_1305_6861_b200.engine import BlochEngine
+
+    eng = BlochEngine.__new__(BlochEngine)
+    lib = _capi.load()
+    eng._lib, eng.device, eng.precision, eng._tables_ref, eng._flat = lib, _capi.BLOCH_HOST_ONLY, 32, None, None
+    h = ctypes.c_void_p()
+    _capi.check(lib.bloch_create(_capi.BLOCH_HOST_ONLY, 32, ctypes.byref(h)), "bloch_create")
+    eng._h = h
+    try:
+        for seed in range(200):
+            seq = random_sequence(seed)
+            t = precompute_sequence_tables(seq, snapshot_times=(0.0, seq.end_time * 0.37, seq.end_time))
+            eng.set_tables(t)
+            st = eng.program_stats()
+            assert st["events"] == O.event_count(t), seed
+            assert st["samples"] == sum(x.size for x in t.acq_times), seed
+    finally:
+        eng.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(64))
+def test_random_sequence_matches_oracle(seed):
+    seq = random_sequence(seed)
+    snaps_t = (0.0, seq.end_time * 0.37, seq.end_time)
+    b = random_spins(seed)
+    t = precompute_sequence_tables(seq, snapshot_times=snaps_t)
+    ot = O.precompute_tables(seq, snapshot_times=snaps_t)
+    ref_e, ref_s = O.compute_block(ot, b.pos, b.mx, b.my, b.mz, b.t1, b.t2, b.m0, b.domega, b.weight)
+    for precision, tol_k, tol_m in ((64, 1e-10, 1e-11), (32, 1e-4, 1e-9)):
+        e, s = compute_block(t, b, precision=precision)
+        if np.linalg.norm(ref_e) > 0:
+            assert O.rel_l2(ref_e, e) <= tol_k, (seed, precision, O.rel_l2(ref_e, e))
+        for k, (a, r) in enumerate(zip(s, ref_s)):
+            assert (a is None) == (r is None), (seed, k)
+            if r is not None:
+                assert O.rel_l2(r, a) <= tol_m, (seed, precision, k, O.rel_l2(r, a))
