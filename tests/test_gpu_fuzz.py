@@ -149,3 +149,27 @@ def test_random_sequence_matches_oracle(seed):
             assert (a is None) == (r is None), (seed, k)
             if r is not None:
                 assert O.rel_l2(r, a) <= tol_m, (seed, precision, k, O.rel_l2(r, a))
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+@pytest.mark.parametrize("seed,coils", [(100, 1), (101, 1), (102, 2), (103, 4), (104, 8), (105, 8)])
+def test_random_sequence_large_block(seed, coils):
+    """Blocks large enough for the production kernel variants (8 or 4 spins per thread, 2-8 coils, several
+    CTAs per SM), on a rasterisation-order subsample checked against the oracle."""
+    seq = random_sequence(seed)
+    n = 80_000
+    rng = np.random.default_rng(seed)
+    m0 = rng.uniform(0.2, 1.0, n)
+    w = (np.full(n, 1 + 0j) if coils == 1 else
+         rng.uniform(0.3, 1.0, (coils, n)) * np.exp(1j * rng.uniform(0, 2 * math.pi, (coils, n))))
+    b = SpinBlock(index=0, pos=rng.uniform(-0.05, 0.05, (n, 3)), mx=np.zeros(n), my=np.zeros(n), mz=m0.copy(),
+                  t1=rng.uniform(0.3, 1.5, n), t2=rng.uniform(0.02, 0.3, n), m0=m0,
+                  domega=rng.normal(0.0, 2 * math.pi * 30, n), weight=w)
+    snaps_t = (seq.end_time,)
+    t = precompute_sequence_tables(seq, snapshot_times=snaps_t)
+    e, s = compute_block(t, b, precision=32)
+    ot = O.precompute_tables(seq, snapshot_times=snaps_t)
+    ref_e, ref_s = O.compute_block(ot, b.pos, b.mx, b.my, b.mz, b.t1, b.t2, b.m0, b.domega, b.weight)
+    assert O.rel_l2(ref_e, e) <= 1e-4, O.rel_l2(ref_e, e)
+    assert O.rel_l2(ref_s[0], s[0]) <= 1e-9
