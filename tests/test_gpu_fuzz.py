@@ -173,3 +173,83 @@ def test_random_sequence_large_block(seed, coils):
     ref_e, ref_s = O.compute_block(ot, b.pos, b.mx, b.my, b.mz, b.t1, b.t2, b.m0, b.domega, b.weight)
     assert O.rel_l2(ref_e, e) <= 1e-4, O.rel_l2(ref_e, e)
     assert O.rel_l2(ref_s[0], s[0]) <= 1e-9
+
+
+def random_sequence_v2(seed):
+    """Second generator: long (multi-pass) and very short windows, EPI-style alternating trapezoid readouts,
+    repeated shaped pulses, zero-duration ES and pulses on acquiring ES."""
+    rng = np.random.default_rng(10_000 + seed)
+    els, row = [], 0
+    els.append(ElementarySequence(pulse=HardPulse(float(rng.uniform(0.3, 1.6)), float(rng.uniform(0, 6.28))),
+                                  duration=float(rng.uniform(1e-4, 2e-3))))
+    n_lines = int(rng.integers(2, 7))
+    n_read = int([rng.integers(2, 20), rng.integers(30, 90), rng.integers(250, 700)][int(rng.integers(0, 3))])
+    dur = float(rng.uniform(3e-4, 3e-3))
+    g = float(rng.uniform(5e-4, 3e-3))
+    for line in range(n_lines):
+        sign = 1.0 if line % 2 == 0 else -1.0
+        grad = (GradientWaveform.trapezoid(gx=sign * g, ramp_s=0.15 * dur, flat_s=0.7 * dur) if rng.random() < 0.5
+                else GradientWaveform.constant(gx=sign * g))
+        els.append(ElementarySequence(gradient=grad, duration=dur, acquisition=AcquisitionSpec(True, n_read),
+                                      kspace_row=row, kspace_reversed=bool(line % 2)))
+        row += 1
+        els.append(ElementarySequence(gradient=GradientWaveform.constant(gy=2e-4), duration=float(rng.uniform(2e-5, 1e-4))))
+        if rng.random() < 0.3:
+            els.append(ElementarySequence(duration=0.0))  # zero-duration ES
+    if rng.random() < 0.6:  # the same shaped pulse twice (RF-train reuse)
+        m = int(rng.integers(4, 24))
+        env = np.hanning(m + 2)[1:-1] * float(rng.uniform(5e-7, 4e-6))
+        for _ in range(2):
+            els.extend(expand_shaped_pulse(env, 1e-5, GradientWaveform.constant(gz=float(rng.uniform(-4e-3, 4e-3)))))
+            els.append(ElementarySequence(duration=float(rng.uniform(1e-4, 1e-3))))
+    # a pulse on an acquiring ES, then a long plain window
+    els.append(ElementarySequence(pulse=HardPulse(math.pi / 3, 0.7), gradient=GradientWaveform.constant(gy=-1e-3),
+                                  duration=float(rng.uniform(2e-4, 1e-3)), acquisition=AcquisitionSpec(True, 40),
+                                  kspace_row=row))
+    row += 1
+    els.append(ElementarySequence(gradient=GradientWaveform.constant(gx=float(rng.uniform(-1e-3, 1e-3))),
+                                  duration=float(rng.uniform(1e-3, 4e-3)),
+                                  acquisition=AcquisitionSpec(True, int(rng.integers(100, 600))), kspace_row=row))
+    return Sequence(els, name=f"fuzz2_{seed}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(48))
+def test_random_sequence_v2_matches_oracle(seed):
+    seq = random_sequence_v2(seed)
+    b = random_spins(seed)
+    t_acq = precompute_sequence_tables(seq).acq_times
+    # snapshots: one exactly on a sample instant, one mid-sequence, the end
+    snaps_t = (float(t_acq[0][len(t_acq[0]) // 2]), seq.end_time * 0.61, seq.end_time)
+    t = precompute_sequence_tables(seq, snapshot_times=snaps_t)
+    ot = O.precompute_tables(seq, snapshot_times=snaps_t)
+    ref_e, ref_s = O.compute_block(ot, b.pos, b.mx, b.my, b.mz, b.t1, b.t2, b.m0, b.domega, b.weight)
+    for precision, tol_k, tol_m in ((64, 1e-10, 1e-11), (32, 1e-4, 1e-9)):
+        e, s = compute_block(t, b, precision=precision)
+        assert O.rel_l2(ref_e, e) <= tol_k, (seed, precision, O.rel_l2(ref_e, e))
+        for k, (a, r) in enumerate(zip(s, ref_s)):
+            assert (a is None) == (r is None), (seed, k)
+            if r is not None:
+                assert O.rel_l2(r, a) <= tol_m, (seed, precision, k, O.rel_l2(r, a))
+
+
+def test_compiler_accepts_random_sequences_v2():
+    import ctypes
+
+    from paper_1305_6861_b200 import _capi
+    from paper_1305_6861_b200.engine import BlochEngine
+
+    eng = BlochEngine.__new__(BlochEngine)
+    lib = _capi.load()
+    eng._lib, eng.device, eng.precision, eng._tables_ref, eng._flat = lib, _capi.BLOCH_HOST_ONLY, 32, None, None
+    h = ctypes.c_void_p()
+    _capi.check(lib.bloch_create(_capi.BLOCH_HOST_ONLY, 32, ctypes.byref(h)), "bloch_create")
+    eng._h = h
+    try:
+        for seed in range(200):
+            seq = random_sequence_v2(seed)
+            t = precompute_sequence_tables(seq, snapshot_times=(seq.end_time * 0.5,))
+            eng.set_tables(t)
+            assert eng.program_stats()["events"] == O.event_count(t), seed
+    finally:
+        eng.close()
