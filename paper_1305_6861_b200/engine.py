@@ -637,7 +637,7 @@ def _run_device_scene(exp: Experiment, spacing, wall_start: float) -> RunResult:
                        snaps.data_ptr() if snaps is not None else 0, sync=True, present=present)
     busy = time.perf_counter() - t_k
     echo_sum = echo.cpu().numpy()
-    if spins.n_coils == 1:
+    if spins.n_coils == 1 and not spins.coil_array:  # a CoilArray keeps its coil axis, as on the host path
         echo_sum = echo_sum[0]
     n_spins = spins.n
     records = []

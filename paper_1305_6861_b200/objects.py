@@ -182,6 +182,7 @@ class DeviceSpins:
     domega: object
     weight: object  # float64 (C, n, 2) interleaved complex, or None for the uniform 1+0j
     device: int = 0
+    coil_array: bool = False  # receive model is a CoilArray: weights keep the coil axis even for one coil
 
     def pointers(self) -> dict:
         d = {k: getattr(self, k).data_ptr() for k in ("pos", "mx", "my", "mz", "t1", "t2", "m0", "domega")}
@@ -194,7 +195,7 @@ class DeviceSpins:
         wc = w[..., 0] + 1j * w[..., 1]
         out = {k: getattr(self, k).cpu().numpy() for k in ("pos", "mx", "my", "mz", "t1", "t2", "m0")}
         out["delta_omega"] = self.domega.cpu().numpy()
-        out["weight"] = wc if self.n_coils > 1 else wc[0]
+        out["weight"] = wc if (self.n_coils > 1 or self.coil_array) else wc[0]
         return out
 
 
@@ -297,6 +298,7 @@ def rasterize_device(scene: DeviceScene, spacing, engine=None, cap: int = DEFAUL
         n=n, n_coils=ncw, pos=views["pos"][: 3 * n].view(n, 3), mx=views["mx"][:n], my=views["my"][:n],
         mz=views["mz"][:n], t1=views["t1"][:n], t2=views["t2"][:n], m0=views["m0"][:n],
         domega=views["domega"][:n], weight=views["weight"][: 2 * ncw * n].view(ncw, n, 2), device=eng.device,
+        coil_array=isinstance(scene.receive, CoilArray),
     )
     if extra_dw is not None:
         extra = np.asarray(extra_dw, dtype=float)

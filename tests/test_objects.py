@@ -175,3 +175,59 @@ def test_device_rasterize_errors_and_general_scene():
     np.testing.assert_allclose(dev["weight"], receive_weights(type("S", (), {"receive": sc.receive})(),
                                                               host["pos"]), rtol=0, atol=1e-14)
     assert math.isclose(float(np.sum(dev["m0"])), float(np.sum(host["m0"])), rel_tol=0, abs_tol=0)
+
+
+def _random_scene(seed):
+    from paper_1305_6861_b200.system import CoilArray, GaussianCoil, UniformSensitivity
+
+    rng = np.random.default_rng(seed)
+    boxes = []
+    for _ in range(int(rng.integers(1, 4))):
+        origin = tuple(rng.uniform(-0.05, 0.03, 3))
+        size = tuple(rng.uniform(0.005, 0.04, 3))
+        shapes = []
+        for _ in range(int(rng.integers(0, 6))):
+            dim = int(rng.integers(2, 4))
+            c = tuple(np.add(origin, rng.uniform(0, 1, 3) * size)[:dim])
+            ax = tuple(rng.uniform(0.002, 0.02, dim))
+            shapes.append(Ellipse(c, ax, angle=float(rng.uniform(0, math.pi)), m0=float(rng.choice([0.0, rng.uniform(0.1, 1)])),
+                                  t1=float(rng.uniform(0.3, 2)), t2=float(rng.uniform(0.02, 0.3)),
+                                  delta_omega=float(rng.normal(0, 50))))
+        boxes.append(LabelBox(origin, size, m0=float(rng.choice([0.0, 0.5])), t1=1.0, t2=0.1,
+                              delta_omega=float(rng.normal(0, 10)), shapes=tuple(shapes)))
+    poly = None
+    if rng.random() < 0.5:
+        k = int(rng.integers(1, 6))
+        poly = PolynomialField(tuple(rng.normal(0, 1, k)), tuple(tuple(int(v) for v in rng.integers(0, 3, 3)) for _ in range(k)),
+                               0.05, scale=float(rng.uniform(1, 50)), peak=(None if rng.random() < 0.5 else 300.0))
+    bumps = None
+    if rng.random() < 0.5:
+        k = int(rng.integers(1, 4))
+        bumps = GaussianBumps(tuple(tuple(rng.uniform(-0.05, 0.05, int(rng.integers(2, 4)))) for _ in range(k)),
+                              tuple(rng.uniform(0.005, 0.03, k)), tuple(rng.normal(0, 100, k)))
+    rx = [UniformSensitivity(), CoilArray([GaussianCoil(tuple(rng.uniform(-0.1, 0.1, 3)), 0.05, float(rng.uniform(0, 6)))
+                                           for _ in range(int(rng.integers(1, 5)))])][int(rng.integers(0, 2))]
+    spacing = tuple(rng.uniform(0.0015, 0.004, 3))
+    return DeviceScene(boxes, const_dw=float(rng.normal(0, 5)), polynomial=poly, bumps=bumps, receive=rx), spacing
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(24))
+def test_device_rasterize_random_scenes(seed):
+    from paper_1305_6861_b200.engine import get_engine
+    from paper_1305_6861_b200.objects import rasterize_device
+    from paper_1305_6861_b200.system import receive_weights
+
+    scene, spacing = _random_scene(seed)
+    host = rasterize_arrays(scene.host_phantom(), spacing)
+    if host["m0"].size == 0:
+        with pytest.raises(InvalidParameter):
+            rasterize_device(scene, spacing, get_engine(0, 32))
+        return
+    dev = rasterize_device(scene, spacing, get_engine(0, 32)).to_host()
+    for k in ("pos", "m0", "t1", "t2"):
+        assert np.array_equal(dev[k], host[k]), (seed, k)
+    dw = scene.host_field(host["pos"], host["delta_omega"])
+    np.testing.assert_allclose(dev["delta_omega"], dw, rtol=1e-12, atol=1e-9)
+    w = receive_weights(type("S", (), {"receive": scene.receive})(), host["pos"])
+    np.testing.assert_allclose(dev["weight"], w, rtol=0, atol=1e-13)
