@@ -87,6 +87,31 @@ struct bloch_ctx {
   std::vector<unsigned char> raster_staging;
   float kernel_ms = 0.f, device_ms = 0.f;
   int launches = 0;
+  // CUDA graph of the device work of a device-resident call (prep, tables, integrator, fold),
+  // captured on the second identical call and replayed while the arguments stay the same
+  uint64_t prog_gen = 0;
+  struct GraphKey {
+    int64_t n = -1;
+    const void* p[12] = {};
+    int32_t n_coils = 0;
+    uint32_t flags = 0;
+    uint64_t gen = 0;
+    cudaStream_t st = nullptr;
+    bool operator==(const GraphKey& o) const {
+      if (n != o.n || n_coils != o.n_coils || flags != o.flags || gen != o.gen || st != o.st) return false;
+      for (int i = 0; i < 12; ++i)
+        if (p[i] != o.p[i]) return false;
+      return true;
+    }
+  } last_key, graph_key;
+  cudaGraphExec_t graph_exec = nullptr;
+  int graph_launches = 0;
+  void drop_graph() {
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    graph_exec = nullptr;
+    graph_key = GraphKey{};
+    last_key = GraphKey{};
+  }
 };
 
 namespace {
@@ -171,6 +196,17 @@ void upload(DevBuf& b, const void* src, size_t bytes, cudaStream_t st) {
 
 }  // namespace
 
+namespace {
+// an error during capture: end it (discarding the partial graph) so the stream is usable again
+void abandon_capture(bloch_ctx* c) {
+  cudaGraph_t g = nullptr;
+  cudaStreamEndCapture(c->stream, &g);
+  if (g) cudaGraphDestroy(g);
+  cudaGetLastError();
+  c->drop_graph();
+}
+}  // namespace
+
 extern "C" {
 
 const char* bloch_version(void) { return BLOCH_VERSION_STRING; }
@@ -240,6 +276,7 @@ int bloch_destroy(bloch_ctx* c) {
   }
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  c->drop_graph();
   for (DevBuf* b : {&c->d_ops, &c->d_gev, &c->d_mats, &c->d_sample_g, &c->d_relax_t, &c->relax, &c->d_rot_cls, &c->rot, &c->in_pos, &c->in_mx, &c->in_my, &c->in_mz,
                     &c->in_t1, &c->in_t2, &c->in_m0, &c->in_dw, &c->in_w, &c->sc, &c->wpad, &c->w32, &c->partial,
                     &c->echo, &c->snaps, &c->d_prog_cls, &c->progtab, &c->d_chirp_cls, &c->chirptab,
@@ -256,6 +293,7 @@ int bloch_set_stream(bloch_ctx* c, void* stream) {
   if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
   if (c->device == BLOCH_HOST_ONLY) return fail(BLOCH_E_STATE, "host-only context has no stream");
   cudaSetDevice(c->device);
+  c->drop_graph();
   if (c->own_stream && c->stream) {
     cudaStreamSynchronize(c->stream);
     cudaStreamDestroy(c->stream);
@@ -306,6 +344,7 @@ int bloch_set_tables(bloch_ctx* c, int32_t n_es, const int64_t* es_ev_offset,
       if (op.kind == bloch::OP_EVENT && op.aux >= 0) c->snap_present[op.aux] = 1;
     c->prog = std::move(prog);
     c->has_prog = true;
+    c->prog_gen++;
   } catch (const std::invalid_argument& ex) {
     c->has_prog = false;
     return fail(BLOCH_E_INVALID, std::string("invalid tables: ") + ex.what());
@@ -363,11 +402,41 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
   const int64_t G = static_cast<int64_t>(P.n_acq) * P.max_samples;
   if (G > 0 && !echoes_out) return fail(BLOCH_E_INVALID, "echoes_out is NULL");
   const bool in_dev = flags & BLOCH_IN_DEVICE, out_dev = flags & BLOCH_OUT_DEVICE;
+  static const bool no_graph = getenv("BLOCH_NO_GRAPH") != nullptr;
+  const bool graphable = in_dev && out_dev && !no_graph;
+  bloch_ctx::GraphKey key;
+  if (graphable) {
+    const void* ptrs[12] = {pos, mx, my, mz, t1, t2, m0, domega, weight, echoes_out, snaps_out, nullptr};
+    key.n = n;
+    for (int i = 0; i < 12; ++i) key.p[i] = ptrs[i];
+    key.n_coils = n_coils;
+    key.flags = flags & ~BLOCH_NO_SYNC;
+    key.gen = c->prog_gen;
+    key.st = c->stream;
+  }
+  bool capturing = false;
   try {
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     cudaStream_t st = c->stream;
+    if (graphable && c->graph_exec && key == c->graph_key) {  // replay the captured device work
+      ck(cudaGraphLaunch(c->graph_exec, st), "graph launch");
+      c->launches = c->graph_launches;
+      if (!(flags & BLOCH_NO_SYNC)) {
+        ck(cudaStreamSynchronize(st), "stream sync");
+        ck(cudaEventElapsedTime(&c->kernel_ms, c->ev[1], c->ev[2]), "elapsed");
+        ck(cudaEventElapsedTime(&c->device_ms, c->ev[0], c->ev[3]), "elapsed");
+      }
+      if (snap_present)
+        for (int32_t i = 0; i < P.n_snap; ++i) snap_present[i] = c->snap_present[i];
+      return BLOCH_OK;
+    }
+    // the second identical call is captured (the first sized every buffer: no allocation below)
+    if (graphable && key == c->last_key) {
+      ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+      capturing = true;
+    }
     c->launches = 0;
-    ck(cudaEventRecord(c->ev[0], st), "event");
+    ck(cudaEventRecordWithFlags(c->ev[0], st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault), "event");
     const int ncp = n_coils <= 1 ? 1 : n_coils <= 2 ? 2 : n_coils <= 4 ? 4 : 8;
     const size_t nd = static_cast<size_t>(n) * sizeof(double);
 
@@ -499,9 +568,9 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       kp.rot = c->rot.as<double>();
       kp.prog = c->progtab.as<double>();
       kp.chirp = c->chirptab.as<double>();
-      ck(cudaEventRecord(c->ev[1], st), "event");
+      ck(cudaEventRecordWithFlags(c->ev[1], st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault), "event");
       ck(dispatch(v, kp, static_cast<int>(grid), static_cast<int>(threads), st), "integrate kernel");
-      ck(cudaEventRecord(c->ev[2], st), "event");
+      ck(cudaEventRecordWithFlags(c->ev[2], st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault), "event");
       c->launches++;
       if (n_slots > 0) {
         if (v.prec == 32)
@@ -515,15 +584,29 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
         c->launches++;
       }
     } else {
-      ck(cudaEventRecord(c->ev[1], st), "event");
-      ck(cudaEventRecord(c->ev[2], st), "event");
+      ck(cudaEventRecordWithFlags(c->ev[1], st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault), "event");
+      ck(cudaEventRecordWithFlags(c->ev[2], st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault), "event");
     }
     // 5. outputs to the host
     if (!out_dev) {
       if (echo_bytes) ck(cudaMemcpyAsync(echoes_out, d_echo, echo_bytes, cudaMemcpyDeviceToHost, st), "D2H echoes");
       if (d_snap) ck(cudaMemcpyAsync(snaps_out, d_snap, snap_bytes, cudaMemcpyDeviceToHost, st), "D2H snapshots");
     }
-    ck(cudaEventRecord(c->ev[3], st), "event");
+    ck(cudaEventRecordWithFlags(c->ev[3], st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault), "event");
+    if (capturing) {
+      cudaGraph_t g = nullptr;
+      capturing = false;
+      ck(cudaStreamEndCapture(st, &g), "end capture");
+      if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+      c->graph_exec = nullptr;
+      const cudaError_t e = cudaGraphInstantiate(&c->graph_exec, g, 0);
+      cudaGraphDestroy(g);
+      ck(e, "graph instantiate");
+      c->graph_key = key;
+      c->graph_launches = c->launches;
+      ck(cudaGraphLaunch(c->graph_exec, st), "graph launch");
+    }
+    if (graphable) c->last_key = key;
     if (!out_dev || !(flags & BLOCH_NO_SYNC)) {
       ck(cudaStreamSynchronize(st), "stream sync");
       ck(cudaEventElapsedTime(&kms, c->ev[1], c->ev[2]), "elapsed");
@@ -533,8 +616,10 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
     if (snap_present)
       for (int32_t i = 0; i < P.n_snap; ++i) snap_present[i] = c->snap_present[i];
   } catch (const InvalidArg& ex) {
+    if (capturing) abandon_capture(c);
     return fail(BLOCH_E_INVALID, ex.what());
   } catch (const std::exception& ex) {
+    if (capturing) abandon_capture(c);
     return fail(BLOCH_E_CUDA, ex.what());
   }
   return BLOCH_OK;

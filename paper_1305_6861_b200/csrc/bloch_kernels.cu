@@ -1423,10 +1423,12 @@ size_t integrate_smem_bytes(int threads) {
 template <typename R, int S, int NC, bool kFull>
 static cudaError_t launch_one(const KParams& kp, int grid, int threads, cudaStream_t stream) {
   const size_t smem = integrate_smem_bytes<R, S, NC>(threads);
-  if (smem > 48 * 1024) {
+  static size_t smem_set = 48 * 1024;  // raise the opt-in limit only when needed (not inside a graph capture)
+  if (smem > smem_set) {
     cudaError_t e = cudaFuncSetAttribute(integrate_kernel<R, S, NC, kFull>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
+    smem_set = smem;
   }
   integrate_kernel<R, S, NC, kFull><<<grid, threads, smem, stream>>>(kp);
   return cudaGetLastError();
