@@ -55,7 +55,8 @@ extern "C" {
 /* bloch_compute_block flags */
 #define BLOCH_IN_DEVICE 1u  /* spin arrays are device pointers (else host)          */
 #define BLOCH_OUT_DEVICE 2u /* echoes/snapshot outputs are device pointers (else host) */
-#define BLOCH_NO_SYNC 4u    /* device outputs only: do not synchronise the stream   */
+#define BLOCH_NO_SYNC 4u    /* return without synchronising the stream; with host buffers they must be
+                               pinned and stay untouched until bloch_synchronize (pipelined callers) */
 
 typedef struct bloch_ctx bloch_ctx;
 
@@ -196,6 +197,14 @@ int bloch_rasterize(bloch_ctx* ctx, const bloch_box_t* boxes, int32_t n_boxes,
                     const bloch_coil_t* coils, int32_t n_coils, double uniform_s, int64_t capacity,
                     double* pos, double* mx, double* my, double* mz, double* t1, double* t2,
                     double* m0, double* domega, double* weight, int64_t* n_out);
+
+/* Wait for all work of this context (e.g. a BLOCH_NO_SYNC call's host outputs). */
+int bloch_synchronize(bloch_ctx* ctx);
+
+/* Order this context's integrator after another context's (pipelined callers): before its
+ * integrator kernel the context waits on `wait_event` (a cudaEvent_t, or NULL), after it it records
+ * `signal_event` (or NULL).  Uploads and downloads stay free to overlap; the kernels serialise. */
+int bloch_set_kernel_gate(bloch_ctx* ctx, void* wait_event, void* signal_event);
 
 /* Device time (ms, CUDA events on the context stream) of the last
  * bloch_compute_block: the integrator kernel alone, and all device work of the

@@ -106,6 +106,7 @@ struct bloch_ctx {
   } last_key, graph_key;
   cudaGraphExec_t graph_exec = nullptr;
   int graph_launches = 0;
+  cudaEvent_t gate_wait = nullptr, gate_signal = nullptr;  // bloch_set_kernel_gate
   void drop_graph() {
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
     graph_exec = nullptr;
@@ -403,7 +404,7 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
   if (G > 0 && !echoes_out) return fail(BLOCH_E_INVALID, "echoes_out is NULL");
   const bool in_dev = flags & BLOCH_IN_DEVICE, out_dev = flags & BLOCH_OUT_DEVICE;
   static const bool no_graph = getenv("BLOCH_NO_GRAPH") != nullptr;
-  const bool graphable = in_dev && out_dev && !no_graph;
+  const bool graphable = in_dev && out_dev && !no_graph && !c->gate_wait && !c->gate_signal;
   bloch_ctx::GraphKey key;
   if (graphable) {
     const void* ptrs[12] = {pos, mx, my, mz, t1, t2, m0, domega, weight, echoes_out, snaps_out, nullptr};
@@ -568,8 +569,10 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       kp.rot = c->rot.as<double>();
       kp.prog = c->progtab.as<double>();
       kp.chirp = c->chirptab.as<double>();
+      if (c->gate_wait) ck(cudaStreamWaitEvent(st, c->gate_wait, 0), "gate wait");
       ck(cudaEventRecordWithFlags(c->ev[1], st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault), "event");
       ck(dispatch(v, kp, static_cast<int>(grid), static_cast<int>(threads), st), "integrate kernel");
+      if (c->gate_signal) ck(cudaEventRecord(c->gate_signal, st), "gate signal");
       ck(cudaEventRecordWithFlags(c->ev[2], st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault), "event");
       c->launches++;
       if (n_slots > 0) {
@@ -607,7 +610,7 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       ck(cudaGraphLaunch(c->graph_exec, st), "graph launch");
     }
     if (graphable) c->last_key = key;
-    if (!out_dev || !(flags & BLOCH_NO_SYNC)) {
+    if (!(flags & BLOCH_NO_SYNC)) {
       ck(cudaStreamSynchronize(st), "stream sync");
       ck(cudaEventElapsedTime(&kms, c->ev[1], c->ev[2]), "elapsed");
       c->kernel_ms = kms;
@@ -694,6 +697,23 @@ int bloch_rasterize(bloch_ctx* c, const bloch_box_t* boxes, int32_t n_boxes, con
   } catch (const std::exception& ex) {
     return fail(BLOCH_E_CUDA, ex.what());
   }
+  return BLOCH_OK;
+}
+
+int bloch_set_kernel_gate(bloch_ctx* c, void* wait_event, void* signal_event) {
+  if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
+  c->gate_wait = static_cast<cudaEvent_t>(wait_event);
+  c->gate_signal = static_cast<cudaEvent_t>(signal_event);
+  c->drop_graph();
+  return BLOCH_OK;
+}
+
+int bloch_synchronize(bloch_ctx* c) {
+  if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
+  if (c->device == BLOCH_HOST_ONLY) return BLOCH_OK;
+  cudaSetDevice(c->device);
+  const cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return fail(BLOCH_E_CUDA, std::string("stream sync: ") + cudaGetErrorString(e));
   return BLOCH_OK;
 }
 

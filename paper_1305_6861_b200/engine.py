@@ -393,6 +393,20 @@ class BlochEngine:
 
         ``out_echoes`` (complex128 (C, n_acq, max_ns)) and ``out_snaps`` (float64
         (n_snap, n, 3)) may be preallocated (e.g. pinned) buffers."""
+        return self._submit(tables, pos, mx, my, mz, t1, t2, m0, domega, weight, block_index, out_echoes,
+                            out_snaps, sync=True).wait()
+
+    def submit(self, tables, pos, mx, my, mz, t1, t2, m0, domega, weight, block_index=0,
+               out_echoes: Optional[np.ndarray] = None, out_snaps: Optional[np.ndarray] = None) -> "Pending":
+        """compute without waiting: returns a :class:`Pending` whose ``wait()`` gives (echoes, snapshots).
+
+        The host inputs and the (pinned) output buffers must stay untouched until ``wait()``.  With
+        two engines (:class:`Pipeline`) the uploads of one block overlap the kernels of the other."""
+        return self._submit(tables, pos, mx, my, mz, t1, t2, m0, domega, weight, block_index, out_echoes,
+                            out_snaps, sync=False)
+
+    def _submit(self, tables, pos, mx, my, mz, t1, t2, m0, domega, weight, block_index, out_echoes, out_snaps,
+                sync):
         f = self.set_tables(tables)
         n = int(np.asarray(mx).size)
         pos = _f64(np.asarray(pos, dtype=float).reshape(n, 3))
@@ -425,11 +439,71 @@ class BlochEngine:
             self._h, n, _capi.dptr(pos), *[_capi.dptr(a) for a in arrs],
             wptr, n_coils, _capi.dptr(echoes.view(np.float64)),
             _capi.dptr(snaps) if snaps is not None else None,
-            present.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), 0,
+            present.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), 0 if sync else _capi.BLOCH_NO_SYNC,
         )
         _capi.check(st, "bloch_compute_block", block_index)
-        snap_list = [snaps[i] if present[i] else None for i in range(n_snap)]
-        return (echoes if multi else echoes[0]), snap_list
+        return Pending(self, echoes if multi else echoes[0], snaps, present, n_snap, keep=(pos, arrs, wc),
+                       done=sync, block_index=block_index)
+
+
+class Pending:
+    """A submitted compute_block (BlochEngine.submit); wait() synchronises and returns its outputs."""
+
+    def __init__(self, eng, echoes, snaps, present, n_snap, keep, done, block_index=0):
+        self._eng, self._echoes, self._snaps, self._present = eng, echoes, snaps, present
+        self._n_snap, self._keep, self._done, self._block = n_snap, keep, done, block_index
+
+    def wait(self):
+        if not self._done:
+            _capi.check(self._eng._lib.bloch_synchronize(self._eng._h), "bloch_synchronize", self._block)
+            self._done = True
+            self._keep = None
+        snaps = [self._snaps[i] if self._present[i] else None for i in range(self._n_snap)]
+        return self._echoes, snaps
+
+
+class Pipeline:
+    """Double-buffered host-to-host compute_block: ``depth`` engine contexts (own stream, own device
+    buffers) take successive blocks in turn, so the uploads and downloads of one block overlap the
+    kernels of the other.  ``submit`` waits only for the block that last used the same context."""
+
+    def __init__(self, device: Optional[int] = None, precision: Optional[int] = None, depth: int = 2):
+        import torch
+
+        dev = default_device() if device is None else int(device)
+        prec = int(os.environ.get("BLOCH_PRECISION", "32")) if precision is None else int(precision)
+        self.engines = [BlochEngine(dev, prec) for _ in range(depth)]
+        self._pending: List[Optional[Pending]] = [None] * depth
+        self._k = 0
+        # the integrators run in submission order: context i waits on context i-1's kernel
+        with torch.cuda.device(dev):
+            self._events = [torch.cuda.Event() for _ in range(depth)]
+            for ev in self._events:  # torch creates the CUDA event lazily: record once (it then counts as done)
+                ev.record()
+            torch.cuda.synchronize(dev)
+        for i, e in enumerate(self.engines):
+            _capi.check(e._lib.bloch_set_kernel_gate(e._h, ctypes.c_void_p(self._events[i - 1].cuda_event),
+                                                     ctypes.c_void_p(self._events[i].cuda_event)),
+                        "bloch_set_kernel_gate")
+
+    def submit(self, tables, *arrays, out_echoes=None, out_snaps=None, block_index=0) -> Pending:
+        i = self._k % len(self.engines)
+        self._k += 1
+        if self._pending[i] is not None:
+            self._pending[i].wait()
+        self._pending[i] = self.engines[i].submit(tables, *arrays, block_index=block_index, out_echoes=out_echoes,
+                                                  out_snaps=out_snaps)
+        return self._pending[i]
+
+    def drain(self) -> None:
+        for p in self._pending:
+            if p is not None:
+                p.wait()
+
+    def close(self) -> None:
+        self.drain()
+        for e in self.engines:
+            e.close()
 
 
 def _unit_weight(wc: np.ndarray, chunk: int = 1 << 15) -> bool:
