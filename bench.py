@@ -281,6 +281,7 @@ def main():
         dist.barrier()
     clocks.mark()
     clocks.stop()
+    launch_shape = eng.last_launch()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = torch.tensor([sum(step_ms), sum(kernel_ms)], dtype=torch.float64, device=dev)
     if world > 1:
@@ -425,6 +426,7 @@ def main():
                    "events_per_spin": E, "coils": C, "event_classes": counts, "program": pstats,
                    "l2": "flushed between timed steps (256 MiB write)", "parallelism": f"spin-shards x{world}"},
         "roofline": roofline,
+        "integrator_launch": launch_shape,
         "e2e": {"value": e2e_value, "unit": metric, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "steps": e2e_steps, "path": e2e_path},
         "gpu_launches": launches,

@@ -212,6 +212,12 @@ int bloch_set_kernel_gate(bloch_ctx* ctx, void* wait_event, void* signal_event);
 int bloch_last_timing(const bloch_ctx* ctx, float* kernel_ms, float* device_ms,
                       int32_t* kernel_launches);
 
+/* Shape of the last integrator launch (all 0 before the first): arithmetic precision (32 / 64 bits),
+ * spins per thread, coil-group width, grid (CTAs) and threads per CTA.  Chosen per call from the block
+ * size, the coil count and the program (>= 16 warps per SM when the block allows). */
+int bloch_last_launch(const bloch_ctx* ctx, int32_t* prec, int32_t* spins_per_thread, int32_t* coils,
+                      int32_t* grid, int32_t* threads);
+
 #ifdef __cplusplus
 }
 #endif

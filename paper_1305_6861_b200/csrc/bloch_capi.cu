@@ -87,6 +87,7 @@ struct bloch_ctx {
   std::vector<unsigned char> raster_staging;
   float kernel_ms = 0.f, device_ms = 0.f;
   int launches = 0;
+  int last_launch[5] = {0, 0, 0, 0, 0};  // prec, spins per thread, coils, grid, threads of the last integrator
   // CUDA graph of the device work of a device-resident call (prep, tables, integrator, fold),
   // captured on the second identical call and replayed while the arguments stay the same
   uint64_t prog_gen = 0;
@@ -126,22 +127,28 @@ struct Variant {
 // uniform ADC window of the program (samples)
 Variant pick_variant(int prec, int64_t n, int ncp, int n_sm, int max_window) {
   if (prec == BLOCH_PREC_F32) {
-    switch (ncp) {
-      case 1: {
-        static const int force_s = [] {  // experiment hook: BLOCH_F32_SPINS=4|8
-          const char* e = getenv("BLOCH_F32_SPINS");
-          return e ? atoi(e) : 0;
-        }();
-        if (force_s == 4 || force_s == 8) return {32, force_s, 1};
-        if (n < int64_t(n_sm) * 8 * 64) return {32, 2, 1};
-        // measured (B200): 256-sample windows run fastest with 8 spins per thread (config 1:
-        // 10.25 vs 10.90 ms), 512-sample windows with 4 (config 2: 35.0 vs 38.1 ms)
-        return {32, max_window >= 384 ? 4 : 8, 1};
-      }
-      case 2: return {32, 4, 2};
-      case 4: return {32, 4, 4};
-      default: return {32, 4, 8};
+    static const int force_s = [] {  // experiment hook: BLOCH_F32_SPINS=2|4|8
+      const char* e = getenv("BLOCH_F32_SPINS");
+      return e ? atoi(e) : 0;
+    }();
+    // the largest spins-per-thread that still keeps >= 16 warps per SM busy: a spin shard of a
+    // multi-GPU run (n / world) must not trade occupancy for per-thread reuse. Measured (B200):
+    // config 1 / 8 (87k spins) S=8 4.13 ms, S=4 3.00, S=2 1.95; config 1 / 4 S=8 5.23, S=4 3.68,
+    // S=2 3.63; the full config 1 (697k) S=8 10.25 vs S=4 10.90
+    auto fits = [&](int s) { return n >= int64_t(n_sm) * 16 * 32 * s; };
+    if (ncp == 1) {
+      if (force_s == 2 || force_s == 4 || force_s == 8) return {32, force_s, 1};
+      // 512-sample windows run fastest with 4 spins per thread (config 2: 35.0 vs 38.1 ms)
+      if (fits(8) && max_window < 384) return {32, 8, 1};
+      return {32, fits(4) ? 4 : 2, 1};
     }
+    if (ncp == 8) {
+      // eight coils carry 4x the accumulators per spin, so fewer warps already saturate: measured
+      // config 4 (274k) S=4 63.7 vs S=2 71.3 ms; config 4 / 2 S=4 42.2 vs S=2 37.0; / 8 33.1 vs 20.6
+      if (force_s == 2 || force_s == 4) return {32, force_s, 8};
+      return {32, n >= int64_t(n_sm) * 8 * 32 * 4 ? 4 : 2, 8};
+    }
+    return {32, 4, ncp};
   }
   switch (ncp) {
     case 1: return {64, n >= int64_t(n_sm) * 4 * 64 ? 4 : 1, 1};
@@ -545,6 +552,11 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       threads = std::max<int64_t>(32, std::min<int64_t>(max_t, threads));
       const int64_t spc = threads * v.S;
       const int64_t grid = (n + spc - 1) / spc;
+      c->last_launch[0] = v.prec;
+      c->last_launch[1] = v.S;
+      c->last_launch[2] = v.NC;
+      c->last_launch[3] = static_cast<int>(grid);
+      c->last_launch[4] = static_cast<int>(threads);
       const int64_t n_slots = P.n_samples * ncp;
       const size_t rsz = v.prec == 32 ? sizeof(float) : sizeof(double);
       const int64_t rows = grid * (threads / 32);  // one partial row per warp
@@ -731,6 +743,15 @@ int bloch_last_timing(const bloch_ctx* c, float* kernel_ms, float* device_ms, in
   if (kernel_ms) *kernel_ms = c->kernel_ms;
   if (device_ms) *device_ms = c->device_ms;
   if (launches) *launches = c->launches;
+  return BLOCH_OK;
+}
+
+int bloch_last_launch(const bloch_ctx* c, int32_t* prec, int32_t* spins_per_thread, int32_t* coils,
+                      int32_t* grid, int32_t* threads) {
+  if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
+  int32_t* out[5] = {prec, spins_per_thread, coils, grid, threads};
+  for (int i = 0; i < 5; ++i)
+    if (out[i]) *out[i] = c->last_launch[i];
   return BLOCH_OK;
 }
 

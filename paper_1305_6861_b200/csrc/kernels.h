@@ -55,6 +55,7 @@ struct KernelTraits<float, 8, 1> {  // the fp32 single-coil workhorse: 2 CTAs x 
   X(float, 4, 2)                  \
   X(float, 4, 4)                  \
   X(float, 4, 8)                  \
+  X(float, 2, 8)                  \
   X(double, 4, 1)                 \
   X(double, 1, 1)                 \
   X(double, 2, 2)                 \

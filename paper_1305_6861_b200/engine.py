@@ -359,6 +359,13 @@ class BlochEngine:
         _capi.check(self._lib.bloch_last_timing(self._h, ctypes.byref(k), ctypes.byref(d), ctypes.byref(n)), "timing")
         return {"kernel_ms": k.value, "device_ms": d.value, "launches": n.value}
 
+    def last_launch(self) -> Dict[str, int]:
+        """Shape of the last integrator launch: precision bits, spins per thread, coil-group width,
+        grid (CTAs) and threads per CTA (bloch_last_launch)."""
+        v = [ctypes.c_int32() for _ in range(5)]
+        _capi.check(self._lib.bloch_last_launch(self._h, *[ctypes.byref(x) for x in v]), "bloch_last_launch")
+        return dict(zip(("precision", "spins_per_thread", "coils", "grid", "threads"), (x.value for x in v)))
+
     def set_stream(self, stream_ptr: int) -> None:
         """Run on an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream); 0 = own stream."""
         _capi.check(self._lib.bloch_set_stream(self._h, ctypes.c_void_p(int(stream_ptr) or None)), "bloch_set_stream")

@@ -19,6 +19,7 @@ import numpy as np
 import pytest
 
 from oracle import bloch_oracle as O
+from paper_1305_6861_b200.engine import get_engine
 from paper_1305_6861_b200 import (
     GAMMA_PROTON,
     AcquisitionSpec,
@@ -153,12 +154,13 @@ def test_random_sequence_matches_oracle(seed):
 
 @pytest.mark.gpu
 @pytest.mark.slow
-@pytest.mark.parametrize("seed,coils", [(100, 1), (101, 1), (102, 2), (103, 4), (104, 8), (105, 8)])
-def test_random_sequence_large_block(seed, coils):
-    """Blocks large enough for the production kernel variants (8 or 4 spins per thread, 2-8 coils, several
-    CTAs per SM), on a rasterisation-order subsample checked against the oracle."""
+@pytest.mark.parametrize("seed,coils,n", [(100, 1, 80_000), (101, 1, 320_000), (106, 1, 620_000), (102, 2, 80_000),
+                                          (103, 4, 80_000), (104, 8, 80_000), (105, 8, 160_000)])
+def test_random_sequence_large_block(seed, coils, n):
+    """Blocks large enough for every production kernel variant: the host picks spins per thread from the
+    block size (>= 16 warps per SM), so 80k / 320k / 620k single-coil spins select 2 / 4 / 8 spins per
+    thread and 80k / 160k eight-coil spins select 2 / 4 (bloch_capi.cu pick_variant)."""
     seq = random_sequence(seed)
-    n = 80_000
     rng = np.random.default_rng(seed)
     m0 = rng.uniform(0.2, 1.0, n)
     w = (np.full(n, 1 + 0j) if coils == 1 else
@@ -169,6 +171,9 @@ def test_random_sequence_large_block(seed, coils):
     snaps_t = (seq.end_time,)
     t = precompute_sequence_tables(seq, snapshot_times=snaps_t)
     e, s = compute_block(t, b, precision=32)
+    launch = get_engine(0, 32).last_launch()
+    want_s = {(1, 80_000): 2, (1, 320_000): 4, (1, 620_000): 8, (8, 80_000): 2, (8, 160_000): 4}.get((coils, n))
+    assert launch["precision"] == 32 and (want_s is None or launch["spins_per_thread"] == want_s), launch
     ot = O.precompute_tables(seq, snapshot_times=snaps_t)
     ref_e, ref_s = O.compute_block(ot, b.pos, b.mx, b.my, b.mz, b.t1, b.t2, b.m0, b.domega, b.weight)
     assert O.rel_l2(ref_e, e) <= 1e-4, O.rel_l2(ref_e, e)
