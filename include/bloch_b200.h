@@ -108,6 +108,14 @@ int bloch_program_stats(const bloch_ctx* ctx, int64_t* n_events, int64_t* n_samp
 int bloch_program_layout(const bloch_ctx* ctx, int64_t* n_ops, int64_t* n_rot_classes,
                          int64_t* n_relax_classes, int64_t* n_onthefly_intervals);
 
+/* Per-spin class tables of the compiled program (all tabulated once per call by
+ * small fp64 kernels before the integrator): progression classes (arithmetic
+ * series of interval moments), chirp classes (reused trapezoid ramps under the
+ * ADC), train classes (reused RF trains, composed into one affine propagator per
+ * spin) and the RF-train ops that use them.  Any pointer may be NULL. */
+int bloch_program_classes(const bloch_ctx* ctx, int64_t* n_prog_classes, int64_t* n_chirp_classes,
+                          int64_t* n_train_classes, int64_t* n_train_class_ops);
+
 /*
  * Evolve one spin block through the uploaded tables — compute_block.
  *

@@ -73,6 +73,8 @@ SIGNATURES = {
     ),
     "bloch_program_layout": (
         c_int, [c_void_p, POINTER(c_int64), POINTER(c_int64), POINTER(c_int64), POINTER(c_int64)]),
+    "bloch_program_classes": (
+        c_int, [c_void_p, POINTER(c_int64), POINTER(c_int64), POINTER(c_int64), POINTER(c_int64)]),
     "bloch_compute_block": (
         c_int,
         [c_void_p, c_int64, _PD, _PD, _PD, _PD, _PD, _PD, _PD, _PD, _PD, c_int32, _PD, _PD,

@@ -79,10 +79,10 @@ struct bloch_ctx {
   bloch::Program prog;
   bool has_prog = false;
   std::vector<uint8_t> snap_present;
-  DevBuf d_ops, d_gev, d_mats, d_sample_g, d_relax_t, d_rot_cls, d_prog_cls, d_chirp_cls;
+  DevBuf d_ops, d_gev, d_mats, d_sample_g, d_relax_t, d_rot_cls, d_prog_cls, d_chirp_cls, d_train_cls;
   DevBuf in_pos, in_mx, in_my, in_mz, in_t1, in_t2, in_m0, in_dw, in_w;
   DevBuf sc, wpad, w32;
-  DevBuf partial, echo, snaps, relax, rot, progtab, chirptab;
+  DevBuf partial, echo, snaps, relax, rot, progtab, chirptab, traintab;
   DevBuf raster_scratch;
   std::vector<unsigned char> raster_staging;
   float kernel_ms = 0.f, device_ms = 0.f;
@@ -287,7 +287,7 @@ int bloch_destroy(bloch_ctx* c) {
   c->drop_graph();
   for (DevBuf* b : {&c->d_ops, &c->d_gev, &c->d_mats, &c->d_sample_g, &c->d_relax_t, &c->relax, &c->d_rot_cls, &c->rot, &c->in_pos, &c->in_mx, &c->in_my, &c->in_mz,
                     &c->in_t1, &c->in_t2, &c->in_m0, &c->in_dw, &c->in_w, &c->sc, &c->wpad, &c->w32, &c->partial,
-                    &c->echo, &c->snaps, &c->d_prog_cls, &c->progtab, &c->d_chirp_cls, &c->chirptab,
+                    &c->echo, &c->snaps, &c->d_prog_cls, &c->progtab, &c->d_chirp_cls, &c->chirptab, &c->d_train_cls, &c->traintab,
                     &c->raster_scratch})
     b->release();
   for (auto& ev : c->ev)
@@ -344,6 +344,8 @@ int bloch_set_tables(bloch_ctx* c, int32_t n_es, const int64_t* es_ev_offset,
              c->stream);
       upload(c->d_chirp_cls, prog.chirp_classes.data(), prog.chirp_classes.size() * sizeof(bloch::ChirpClass),
              c->stream);
+      upload(c->d_train_cls, prog.train_classes.data(), prog.train_classes.size() * sizeof(bloch::TrainClass),
+             c->stream);
       upload(c->d_sample_g, prog.sample_g.data(), prog.sample_g.size() * sizeof(int64_t), c->stream);
       ck(cudaStreamSynchronize(c->stream), "set_tables sync");
     }
@@ -390,6 +392,17 @@ int bloch_program_layout(const bloch_ctx* c, int64_t* n_ops, int64_t* n_rot_clas
   if (n_rot_classes) *n_rot_classes = static_cast<int64_t>(c->prog.rot_classes.size());
   if (n_relax_classes) *n_relax_classes = static_cast<int64_t>(c->prog.relax_t.size());
   if (n_onthefly_intervals) *n_onthefly_intervals = otf;
+  return BLOCH_OK;
+}
+
+int bloch_program_classes(const bloch_ctx* c, int64_t* n_prog_classes, int64_t* n_chirp_classes,
+                          int64_t* n_train_classes, int64_t* n_train_class_ops) {
+  if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
+  if (!c->has_prog) return fail(BLOCH_E_STATE, "no tables uploaded");
+  if (n_prog_classes) *n_prog_classes = static_cast<int64_t>(c->prog.prog_classes.size());
+  if (n_chirp_classes) *n_chirp_classes = static_cast<int64_t>(c->prog.chirp_classes.size());
+  if (n_train_classes) *n_train_classes = static_cast<int64_t>(c->prog.train_classes.size());
+  if (n_train_class_ops) *n_train_class_ops = c->prog.n_train_class_ops;
   return BLOCH_OK;
 }
 
@@ -510,6 +523,14 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
            "chirp table kernel");
         c->launches++;
       }
+      const int n_train = static_cast<int>(P.train_classes.size());
+      if (n_train > 0) {
+        c->traintab.ensure(bloch::kTrainRow * nd * n_train);
+        ck(bloch::launch_train_table(n, n_train, c->d_train_cls.as<bloch::TrainClass>(), c->d_mats.as<double>(), d_sc,
+                                     c->traintab.as<double>(), st),
+           "train table kernel");
+        c->launches++;
+      }
       if (d_w && ncp != n_coils) {
         c->wpad.ensure(2 * nd * ncp);
         ck(bloch::launch_pad_weights(n, n_coils, ncp, d_w, c->wpad.as<double>(), st), "pad kernel");
@@ -581,6 +602,7 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       kp.rot = c->rot.as<double>();
       kp.prog = c->progtab.as<double>();
       kp.chirp = c->chirptab.as<double>();
+      kp.train = c->traintab.as<double>();
       if (c->gate_wait) ck(cudaStreamWaitEvent(st, c->gate_wait, 0), "gate wait");
       ck(cudaEventRecordWithFlags(c->ev[1], st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault), "event");
       ck(dispatch(v, kp, static_cast<int>(grid), static_cast<int>(threads), st), "integrate kernel");

@@ -689,6 +689,29 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
       const double dt = __ldg(&op->p[0]), dmx = __ldg(&op->p[1]), dmy = __ldg(&op->p[2]), dmz = __ldg(&op->p[3]);
       const double* mats = kp.mats + static_cast<int64_t>(m0i) * 9;
       constexpr int G = S < 4 ? S : 4;  // spins per register group
+      const int tcl = __ldg(&op->rot);
+      if (tcl >= 0) {  // reused train: its tabulated affine propagator m -> A m + b (train_table_kernel)
+        const double2* tb = reinterpret_cast<const double2*>(kp.train) + static_cast<int64_t>(tcl) * kp.n * 6;
+#pragma unroll
+        for (int g0 = 0; g0 < S; g0 += G) {
+          double2 a[G][6];
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const int64_t i = sp.act(g0 + g) ? sp.idx(g0 + g) : 0;
+#pragma unroll
+            for (int k = 0; k < 6; ++k) a[g][k] = __ldg(tb + i * 6 + k);
+          }
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const int s = g0 + g;
+            const double x = sp.mx(s), y = sp.my(s), z = sp.mz(s);
+            sp.mx(s) = fma(a[g][0].x, x, fma(a[g][0].y, y, fma(a[g][1].x, z, a[g][4].y)));
+            sp.my(s) = fma(a[g][1].y, x, fma(a[g][2].x, y, fma(a[g][2].y, z, a[g][5].x)));
+            sp.mz(s) = fma(a[g][3].x, x, fma(a[g][3].y, y, fma(a[g][4].x, z, a[g][5].y)));
+          }
+        }
+        continue;
+      }
 #pragma unroll 1
       for (int g0 = 0; g0 < S; g0 += G) {
         double x[G], y[G], z[G], zr[G], zi[G], e1[G], rg[G];
@@ -1371,6 +1394,60 @@ __global__ void chirp_table_kernel(int64_t n, int n_cls, const ChirpClass* __res
   }
 }
 
+// train classes (program.h TrainClass): per (class, spin) the affine propagator of the
+// whole run, m -> A m + b, composed in fp64 in the order the on-the-fly path applies
+// it (engine.py:277-302 per elementary sequence): pulse j, then the shared interval
+// (precession by th, transverse decay e2, longitudinal e1 and regrowth m0 (1 - e1)).
+// The three columns of A and the vector b are pushed through the pairs together.
+// Output row: A (row-major, 9), b (3).
+__global__ void train_table_kernel(int64_t n, int n_cls, const TrainClass* __restrict__ tc,
+                                   const double* __restrict__ mats, const SpinConst* __restrict__ sc,
+                                   double* __restrict__ out) {
+  const int64_t total = static_cast<int64_t>(n_cls) * n;
+  for (int64_t t = gtid(); t < total; t += gstride()) {
+    const int64_t c = t / n, i = t - c * n;
+    const TrainClass& k = tc[c];
+    const SpinConst s = sc[i];
+    double zr = 1.0, zi = 0.0, e1 = 1.0, rg = 0.0;
+    if (k.flags & EV_MOVE) {
+      const double th = fma(s.z, k.p[3], fma(s.y, k.p[2], s.x * k.p[1])) + s.dw * k.p[0];
+      phase_factor(th, zr, zi);
+      if (k.flags & EV_RELAX) {
+        const double e2 = exp(-k.p[0] * s.r2);
+        e1 = exp(-k.p[0] * s.r1);
+        zr *= e2;
+        zi *= e2;
+        rg = s.m0 * (1.0 - e1);
+      }
+    }
+    // v[col][row]: columns 0..2 of A, column 3 = b
+    double v[4][3] = {{1.0, 0.0, 0.0}, {0.0, 1.0, 0.0}, {0.0, 0.0, 1.0}, {0.0, 0.0, 0.0}};
+    const double* m = mats + 9 * static_cast<int64_t>(k.aux);
+    for (int j = 0; j < k.count; ++j, m += 9) {
+      double r[9];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) r[q] = __ldg(m + q);
+#pragma unroll
+      for (int col = 0; col < 4; ++col) {
+        const double x = v[col][0], y = v[col][1], z = v[col][2];
+        const double nx = r[0] * x + r[1] * y + r[2] * z;
+        const double ny = r[3] * x + r[4] * y + r[5] * z;
+        const double nz = r[6] * x + r[7] * y + r[8] * z;
+        v[col][0] = nx * zr - ny * zi;
+        v[col][1] = nx * zi + ny * zr;
+        v[col][2] = col == 3 ? fma(nz, e1, rg) : nz * e1;
+      }
+    }
+    double* o = out + t * kTrainRow;
+#pragma unroll
+    for (int row = 0; row < 3; ++row)
+#pragma unroll
+      for (int col = 0; col < 3; ++col) o[row * 3 + col] = v[col][row];
+#pragma unroll
+    for (int row = 0; row < 3; ++row) o[9 + row] = v[3][row];
+  }
+}
+
 // pad [nc][n][2] weights to [ncp][n][2] (zero coils beyond nc)
 __global__ void pad_weights_kernel(int64_t n, int nc, int ncp, const double* __restrict__ w, double* __restrict__ out) {
   const int64_t total = static_cast<int64_t>(ncp) * n * 2;
@@ -1481,6 +1558,13 @@ cudaError_t launch_chirp_table(int64_t n, int n_cls, const ChirpClass* cc, const
   if (n == 0 || n_cls == 0) return cudaSuccess;
   chirp_table_kernel<<<grid_for(static_cast<int64_t>(n_cls) * n, 256), 256, 0, stream>>>(
       n, n_cls, cc, sc, reinterpret_cast<double2*>(out));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_train_table(int64_t n, int n_cls, const TrainClass* tc, const double* mats, const SpinConst* sc,
+                               double* out, cudaStream_t stream) {
+  if (n == 0 || n_cls == 0) return cudaSuccess;
+  train_table_kernel<<<grid_for(static_cast<int64_t>(n_cls) * n, 128), 128, 0, stream>>>(n, n_cls, tc, mats, sc, out);
   return cudaGetLastError();
 }
 

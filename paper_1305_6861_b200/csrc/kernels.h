@@ -31,6 +31,7 @@ struct KParams {
   const double* rot;             // [n_rot][n][8]: rotation-class propagators (rot_table_kernel)
   double* prog;                  // [n_prog][n][8]: progression running factors (updated in place)
   const double* chirp;           // [n_chirp][n][8]: chirp-class factors (chirp_table_kernel)
+  const double* train;           // [n_train][n][12]: train-class affine propagators (train_table_kernel)
   const float2* w32;             // fp32 multi-coil weights, spin-major [n][NC] (tensor-core windows), or nullptr
 };
 
@@ -84,6 +85,8 @@ cudaError_t launch_prog_table(int64_t n, int n_cls, const ProgClass* pc, const S
                               cudaStream_t stream);
 cudaError_t launch_chirp_table(int64_t n, int n_cls, const ChirpClass* cc, const SpinConst* sc, double* out,
                                cudaStream_t stream);
+cudaError_t launch_train_table(int64_t n, int n_cls, const TrainClass* tc, const double* mats, const SpinConst* sc,
+                               double* out, cudaStream_t stream);
 cudaError_t launch_pad_weights(int64_t n, int nc, int ncp, const double* w, double* out,
                                cudaStream_t stream);
 cudaError_t launch_weights_f32(int64_t n, int ncp, const double* w, float2* out, cudaStream_t stream);

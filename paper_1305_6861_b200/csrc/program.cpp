@@ -54,6 +54,7 @@ void fuse_intervals(Program& prog, const std::function<int32_t(double)>& relax_c
 void find_progressions(Program& prog);
 void find_chirp_classes(Program& prog);
 void fuse_pulses(Program& prog);
+void find_train_classes(Program& prog);
 
 void compile_program(const TablesView& t, Program& prog) {
   prog = Program();
@@ -482,6 +483,7 @@ void fuse_intervals(Program& prog, const std::function<int32_t(double)>& relax_c
   prog.ops.swap(out);
   find_progressions(prog);
   find_chirp_classes(prog);
+  find_train_classes(prog);
   fuse_pulses(prog);
 }
 
@@ -553,6 +555,47 @@ void find_chirp_classes(Program& prog) {
       prog.chirp_classes.push_back(cc);
     }
     op.rot = f->second;
+  }
+}
+
+// Train classes (program.h TrainClass): an RF train that recurs with bit-identical
+// sub-pulse matrices and interval (the same shaped pulse under the same gradient,
+// sequence.py:650-674, repeated every line) is composed once per spin into its
+// affine propagator; OP_RFTRAIN.rot then indexes the train table.  A run that
+// occurs once stays on the fly (composing costs ~4 passes of the train).
+void find_train_classes(Program& prog) {
+  constexpr size_t kMaxTrain = 8;
+  using Key = std::vector<double>;
+  auto key_of = [&](const DevOp& op) {
+    Key k(op.p, op.p + 4);
+    k.push_back(static_cast<double>(op.count));
+    k.push_back(static_cast<double>(op.flags));
+    const double* m = prog.mats.data() + 9 * static_cast<size_t>(op.aux);
+    k.insert(k.end(), m, m + 9 * static_cast<size_t>(op.count));
+    return k;
+  };
+  std::map<Key, int64_t> uses;
+  for (const DevOp& op : prog.ops)
+    if (op.kind == OP_RFTRAIN) uses[key_of(op)]++;
+  std::map<Key, int32_t> ids;
+  for (DevOp& op : prog.ops) {
+    if (op.kind != OP_RFTRAIN) continue;
+    const Key k = key_of(op);
+    op.rot = -1;
+    if (uses[k] < 2) continue;
+    auto f = ids.find(k);
+    if (f == ids.end()) {
+      if (prog.train_classes.size() >= kMaxTrain) continue;
+      TrainClass tc{};
+      tc.aux = op.aux;
+      tc.count = op.count;
+      tc.flags = op.flags;
+      for (int a = 0; a < 4; ++a) tc.p[a] = op.p[a];
+      f = ids.emplace(k, static_cast<int32_t>(prog.train_classes.size())).first;
+      prog.train_classes.push_back(tc);
+    }
+    op.rot = f->second;
+    prog.n_train_class_ops++;
   }
 }
 

@@ -51,7 +51,8 @@ struct alignas(16) DevOp {
                   // CHIRP: dt, dmom_0 (3), dd (3)
   int32_t flags;  // RFTRAIN: EV_* flags of the shared interval
   int32_t cls;    // relax class of dt (EVENT/CHIRP/RFTRAIN on-the-fly path), -1 = no relaxation
-  int32_t rot;    // rotation class (EVENT: repeated interval; WINDOW: reused run), -1 = none
+  int32_t rot;    // rotation class (EVENT: repeated interval; WINDOW: reused run), chirp class (CHIRP),
+                  // train class (RFTRAIN), -1 = none
   int32_t prg;    // EVENT: progression class (interval of an arithmetic series of moments), -1 = none
   int32_t pre;    // EVENT/WINDOW: hard pulse applied first (matrix index into mats, fused OP_ROT), -1 = none
   int32_t tmode;  // RFTRAIN: 1 = every sub-pulse rotates about x (real envelope); EVENT/WINDOW: axis of `pre` (1 x, 2 y, 0 general)
@@ -92,6 +93,22 @@ struct alignas(16) ChirpClass {
   double pad;
 };
 static_assert(sizeof(ChirpClass) == 64, "ChirpClass must be 64 bytes");
+
+// A train class: a reused OP_RFTRAIN run (the same shaped pulse under the same
+// gradient, e.g. every line's slice-selective excitation).  Per spin the table
+// holds the whole train's affine propagator m -> A m + b (A row-major 3x3, then
+// b): 12 doubles, composed in fp64 by train_table_kernel from the same sub-pulse
+// matrices and interval the on-the-fly path applies one by one.
+struct alignas(16) TrainClass {
+  int32_t aux;    // first matrix of the run in the side table
+  int32_t count;  // sub-pulse + interval pairs
+  int32_t flags;  // EV_* flags of the shared interval
+  int32_t pad0;
+  double p[4];    // dt, dmx, dmy, dmz of the shared interval
+  double pad[2];
+};
+static_assert(sizeof(TrainClass) == 64, "TrainClass must be 64 bytes");
+constexpr int kTrainRow = 12;  // doubles per (train class, spin)
 
 struct alignas(16) GEv {  // one generic sampled interval
   double dt, dmx, dmy, dmz;

@@ -30,12 +30,14 @@ struct Program {
   std::vector<RotClass> rot_classes;
   std::vector<ProgClass> prog_classes;
   std::vector<ChirpClass> chirp_classes;
+  std::vector<TrainClass> train_classes;
   int32_t n_acq = 0, max_samples = 0, n_snap = 0;
   int64_t n_events = 0;  // reference table size incl. pulses
   int64_t n_samples = 0;
   int64_t n_rot = 0, n_interval = 0, n_window_ops = 0, n_window_samples = 0, n_gsamp_events = 0;
   int64_t n_chirp_ops = 0, n_chirp_samples = 0, n_train_ops = 0, n_train_pairs = 0;
   int64_t n_fused_windows = 0, n_fused_intervals = 0, n_prog_intervals = 0, n_fused_pulses = 0;
+  int64_t n_train_class_ops = 0;  // RF trains applied from the train table
 };
 
 // Throws std::invalid_argument on malformed tables.

@@ -86,7 +86,10 @@ def test_compile_detects_structure(host_engine):
     host_engine.set_tables(precompute_sequence_tables(configs.make(3).sequence))
     assert host_engine.program_stats()["chirp_samples"] > 2000  # trapezoid ramps under the ADC
     host_engine.set_tables(precompute_sequence_tables(configs.make(4).sequence))
-    assert host_engine.program_stats()["train_pairs"] == 3 * 256 * 128  # sinc sub-pulses
+    st = host_engine.program_stats()
+    assert st["train_pairs"] == 3 * 256 * 128  # sinc sub-pulses
+    # the three pulses of every line are the same sinc under the same slice gradient: one train class
+    assert st["train_classes"] == 1 and st["train_class_ops"] == 3 * 128
 
 
 def test_malformed_tables_rejected(host_engine):
