@@ -37,14 +37,16 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Compile the library; ``out``/``defines`` build variants for A/B timing (tools/ab.sh)."""
+    target = out or LIB_PATH
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     deps = srcs + [os.path.join(CSRC, h) for h in HEADERS] + [
         os.path.join(ROOT, "include", "bloch_b200.h"),
         os.path.abspath(__file__),
     ]
-    if not force and not _stale(LIB_PATH, deps):
-        return LIB_PATH
+    if not force and not defines and not _stale(target, deps):
+        return target
     cmd = [
         nvcc_path(),
         *ARCH,
@@ -58,8 +60,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         "-v" if verbose else "-O3",
         "-I",
         os.path.join(ROOT, "include"),
+        *[f"-D{d}" for d in defines],
         "-o",
-        LIB_PATH + ".tmp",
+        target + ".tmp",
         *srcs,
     ]
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -67,9 +70,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
     if verbose:
         sys.stderr.write(res.stdout + res.stderr)
-    os.replace(LIB_PATH + ".tmp", LIB_PATH)
-    return LIB_PATH
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python -m paper_1305_6861_b200.build [--force] [-v] [--out PATH] [-DNAME=VALUE ...]
+    args = sys.argv[1:]
+    out = args[args.index("--out") + 1] if "--out" in args else None
+    print(build(force="--force" in args, verbose="-v" in args, out=out,
+                defines=[a[2:] for a in args if a.startswith("-D")]))

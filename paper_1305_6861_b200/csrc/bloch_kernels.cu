@@ -418,9 +418,34 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
+// Window products: x = hi + lo with hi exact in tf32.  BLOCH_MMA_SPLIT 3: three tf32
+// passes (hi hi + hi lo + lo hi, lo masked to tf32).  BLOCH_MMA_SPLIT 2 (default): the
+// hi hi pass in tf32, and both cross terms in ONE bf16 m16n8k16 whose K concatenates
+// (A_hi | A_lo) against (B_lo ; B_hi).  The bf16 operands are the top 16 bits of the
+// fp32 words (one PRMT per pair, no F2FP conversion): the cross terms are ~2^-11 of
+// the product and carry 2^-8 relative truncation, ~2^-19 overall — the same order as
+// the fp32 recurrence.  The bf16 pipe runs twice the tf32 MAC rate, so the two cross
+// terms cost one tf32 pass: 2 instead of 3 tensor-pipe units per product.
+#ifndef BLOCH_MMA_SPLIT
+#define BLOCH_MMA_SPLIT 2
+#endif
 __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
   hi = __float_as_uint(x) & 0xffffe000u;
+#if BLOCH_MMA_SPLIT == 3
   lo = __float_as_uint(x - __uint_as_float(hi)) & 0xffffe000u;
+#else
+  lo = __float_as_uint(x - __uint_as_float(hi));  // exact; the bf16 pack keeps its top 16 bits
+#endif
+}
+
+// {x, y} -> bf16x2 (x in the low half) by truncation: the high halves of the fp32 words
+__device__ __forceinline__ uint32_t pack_bf16(uint32_t x, uint32_t y) { return __byte_perm(x, y, 0x7632); }
+
+__device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
 __device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
@@ -480,10 +505,18 @@ __device__ __forceinline__ void mma_round_t(const float4* __restrict__ st, const
     }
 #pragma unroll
     for (int j = 0; j < NT; ++j) mma_tf32(acc[j], arh, aih, naih, arh, brh[j], bih[j]);
+#if BLOCH_MMA_SPLIT == 3
 #pragma unroll
     for (int j = 0; j < NT; ++j) mma_tf32(acc[j], arh, aih, naih, arh, brl[j], bil[j]);
 #pragma unroll
     for (int j = 0; j < NT; ++j) mma_tf32(acc[j], arl, ail, nail, arl, brh[j], bih[j]);
+#else
+    // k16 slots of lane t: 2t, 2t+1 = (re, im) of its spin against (A_hi, B_lo); 2t+8, 2t+9 against (A_lo, B_hi)
+    const uint32_t c0 = pack_bf16(arh, naih), c1 = pack_bf16(aih, arh), c2 = pack_bf16(arl, nail),
+                   c3 = pack_bf16(ail, arl);
+#pragma unroll
+    for (int j = 0; j < NT; ++j) mma_bf16(acc[j], c0, c1, c2, c3, pack_bf16(brl[j], bil[j]), pack_bf16(brh[j], bih[j]));
+#endif
   }
 }
 
@@ -551,10 +584,17 @@ __device__ __forceinline__ void mma_round_mc(const float4* __restrict__ st, cons
     }
 #pragma unroll
     for (int c = 0; c < NC; ++c) mma_tf32(acc[c], arh, aih, naih, arh, brh[c], bih[c]);
+#if BLOCH_MMA_SPLIT == 3
 #pragma unroll
     for (int c = 0; c < NC; ++c) mma_tf32(acc[c], arh, aih, naih, arh, brl[c], bil[c]);
 #pragma unroll
     for (int c = 0; c < NC; ++c) mma_tf32(acc[c], arl, ail, nail, arl, brh[c], bih[c]);
+#else
+    const uint32_t c0 = pack_bf16(arh, naih), c1 = pack_bf16(aih, arh), c2 = pack_bf16(arl, nail),
+                   c3 = pack_bf16(ail, arl);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) mma_bf16(acc[c], c0, c1, c2, c3, pack_bf16(brl[c], bil[c]), pack_bf16(brh[c], bih[c]));
+#endif
   }
 }
 
