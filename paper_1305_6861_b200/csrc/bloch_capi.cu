@@ -79,10 +79,10 @@ struct bloch_ctx {
   bloch::Program prog;
   bool has_prog = false;
   std::vector<uint8_t> snap_present;
-  DevBuf d_ops, d_gev, d_mats, d_sample_g, d_relax_t, d_rot_cls, d_prog_cls, d_chirp_cls, d_train_cls;
+  DevBuf d_ops, d_gev, d_mats, d_sample_g, d_relax_t, d_planes, d_train_cls;
   DevBuf in_pos, in_mx, in_my, in_mz, in_t1, in_t2, in_m0, in_dw, in_w;
   DevBuf sc, wpad, w32;
-  DevBuf partial, echo, snaps, relax, rot, progtab, chirptab, traintab;
+  DevBuf partial, echo, snaps, relax, planetab, traintab;
   DevBuf raster_scratch;
   std::vector<unsigned char> raster_staging;
   float kernel_ms = 0.f, device_ms = 0.f;
@@ -285,9 +285,9 @@ int bloch_destroy(bloch_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   c->drop_graph();
-  for (DevBuf* b : {&c->d_ops, &c->d_gev, &c->d_mats, &c->d_sample_g, &c->d_relax_t, &c->relax, &c->d_rot_cls, &c->rot, &c->in_pos, &c->in_mx, &c->in_my, &c->in_mz,
+  for (DevBuf* b : {&c->d_ops, &c->d_gev, &c->d_mats, &c->d_sample_g, &c->d_relax_t, &c->relax, &c->d_planes, &c->planetab, &c->in_pos, &c->in_mx, &c->in_my, &c->in_mz,
                     &c->in_t1, &c->in_t2, &c->in_m0, &c->in_dw, &c->in_w, &c->sc, &c->wpad, &c->w32, &c->partial,
-                    &c->echo, &c->snaps, &c->d_prog_cls, &c->progtab, &c->d_chirp_cls, &c->chirptab, &c->d_train_cls, &c->traintab,
+                    &c->echo, &c->snaps, &c->d_train_cls, &c->traintab,
                     &c->raster_scratch})
     b->release();
   for (auto& ev : c->ev)
@@ -339,11 +339,7 @@ int bloch_set_tables(bloch_ctx* c, int32_t n_es, const int64_t* es_ev_offset,
       upload(c->d_gev, prog.gev.data(), prog.gev.size() * sizeof(bloch::GEv), c->stream);
       upload(c->d_mats, prog.mats.data(), prog.mats.size() * sizeof(double), c->stream);
       upload(c->d_relax_t, prog.relax_t.data(), prog.relax_t.size() * sizeof(double), c->stream);
-      upload(c->d_rot_cls, prog.rot_classes.data(), prog.rot_classes.size() * sizeof(bloch::RotClass), c->stream);
-      upload(c->d_prog_cls, prog.prog_classes.data(), prog.prog_classes.size() * sizeof(bloch::ProgClass),
-             c->stream);
-      upload(c->d_chirp_cls, prog.chirp_classes.data(), prog.chirp_classes.size() * sizeof(bloch::ChirpClass),
-             c->stream);
+      upload(c->d_planes, prog.planes.data(), prog.planes.size() * sizeof(bloch::PlaneDesc), c->stream);
       upload(c->d_train_cls, prog.train_classes.data(), prog.train_classes.size() * sizeof(bloch::TrainClass),
              c->stream);
       upload(c->d_sample_g, prog.sample_g.data(), prog.sample_g.size() * sizeof(int64_t), c->stream);
@@ -499,28 +495,12 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
            "relax table kernel");
         c->launches++;
       }
-      const int n_rot = static_cast<int>(P.rot_classes.size());
-      if (n_rot > 0) {
-        c->rot.ensure(8 * nd * n_rot);
-        ck(bloch::launch_rot_table(n, n_rot, c->d_rot_cls.as<bloch::RotClass>(), d_sc, n_coils == 1 ? d_w : nullptr,
-                                   c->rot.as<double>(), st),
-           "rotation table kernel");
-        c->launches++;
-      }
-      const int n_prog = static_cast<int>(P.prog_classes.size());
-      if (n_prog > 0) {
-        c->progtab.ensure(8 * nd * n_prog);
-        ck(bloch::launch_prog_table(n, n_prog, c->d_prog_cls.as<bloch::ProgClass>(), d_sc, c->progtab.as<double>(),
-                                    st),
-           "progression table kernel");
-        c->launches++;
-      }
-      const int n_chirp = static_cast<int>(P.chirp_classes.size());
-      if (n_chirp > 0) {
-        c->chirptab.ensure(8 * nd * n_chirp);
-        ck(bloch::launch_chirp_table(n, n_chirp, c->d_chirp_cls.as<bloch::ChirpClass>(), d_sc,
-                                     c->chirptab.as<double>(), st),
-           "chirp table kernel");
+      const int n_planes = static_cast<int>(P.planes.size());
+      if (n_planes > 0) {
+        c->planetab.ensure(2 * nd * n_planes);
+        ck(bloch::launch_planes(n, n_planes, c->d_planes.as<bloch::PlaneDesc>(), d_sc, n_coils == 1 ? d_w : nullptr,
+                                c->planetab.as<double>(), st),
+           "plane kernel");
         c->launches++;
       }
       const int n_train = static_cast<int>(P.train_classes.size());
@@ -599,9 +579,7 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       kp.part_stride = n_slots * 2;
       kp.snaps = d_snap;
       kp.relax = c->relax.as<double>();
-      kp.rot = c->rot.as<double>();
-      kp.prog = c->progtab.as<double>();
-      kp.chirp = c->chirptab.as<double>();
+      kp.planes = c->planetab.as<double2>();
       kp.train = c->traintab.as<double>();
       if (c->gate_wait) ck(cudaStreamWaitEvent(st, c->gate_wait, 0), "gate wait");
       ck(cudaEventRecordWithFlags(c->ev[1], st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault), "event");

@@ -144,13 +144,20 @@ __device__ __forceinline__ double theta_of(const SC& c, double dt, double dmx, d
 __device__ __forceinline__ double2 relax_pair(const KParams& kp, int c, int64_t i) {
   return __ldg(reinterpret_cast<const double2*>(kp.relax) + static_cast<int64_t>(c) * kp.n + i);
 }
-// rotation-class table, AoS [c][i][8]: Cpre (2), C (2), A, B, z (2)
+// plane `id` of the op (program.h PlaneDesc): [n] double2, one value per spin
+__device__ __forceinline__ const double2* plane(const KParams& kp, const DevOp* op, int k) {
+  return kp.planes + static_cast<int64_t>(__ldg(&op->pl[k])) * kp.n;
+}
+__device__ __forceinline__ const double2* plane_at(const KParams& kp, int id, int64_t i) {
+  return kp.planes + (static_cast<int64_t>(id) * kp.n + i);
+}
+// rotation-class quantities of a window: Cpre, C, (A, B), z
 struct RotCoef {
   double pr, pi, cr, ci, a, b, zr, zi;
 };
-__device__ __forceinline__ RotCoef load_rot(const KParams& kp, int c, int64_t i) {
-  const double2* p = reinterpret_cast<const double2*>(kp.rot) + (static_cast<int64_t>(c) * kp.n + i) * 4;
-  const double2 a = __ldg(p), b = __ldg(p + 1), d = __ldg(p + 2), e = __ldg(p + 3);
+__device__ __forceinline__ RotCoef load_rot(const KParams& kp, const DevOp* op, int64_t i) {
+  const double2 a = __ldg(plane(kp, op, 0) + i), e = __ldg(plane(kp, op, 1) + i), b = __ldg(plane(kp, op, 2) + i),
+                d = __ldg(plane(kp, op, 3) + i);
   return RotCoef{a.x, a.y, b.x, b.y, d.x, d.y, e.x, e.y};
 }
 
@@ -599,6 +606,96 @@ __device__ __forceinline__ void mma_round_mc(const float4* __restrict__ st, cons
 }
 
 // ---------------------------------------------------------------------------
+// tabulated chirps in the fp32 mode
+// ---------------------------------------------------------------------------
+
+// A chirp (OP_CHIRP: K sampled intervals whose moments grow linearly) applies
+// r_k = r0 q^k to the transverse magnetisation before sample k.  The fp64 state
+// leaves the run through its closed form: m -> C_total m (C_total = prod r_k, the
+// plane of the whole run's (K dt, K d0 + K(K-1)/2 dd)) and mz -> A mz + B, applied
+// at the first block.  The samples only feed the fp32 ADC sums, so they run as an
+// fp32 recurrence u <- u r, r <- r q from u = w m: 8 FP32 multiply-adds per
+// sample instead of ~10 fp64 operations and two F2F conversions.  Blocks of
+// kBlk samples are spin-outer; between blocks each spin's (u, r) waits in this
+// warp's window stage (free outside windows).
+template <int S, int NC>
+__device__ __forceinline__ void chirp_f32(const KParams& kp, const DevOp* op, Spins<S>& sp, Strip<float>& strip,
+                                          unsigned char* smem_raw, int cnt, int s0) {
+  constexpr int kSampPerChunk = kChunkSlots / NC;
+  constexpr int kBlk = 2 * kSampPerChunk;
+  const int lane = threadIdx.x & 31;
+  constexpr size_t kStage = NC == 1 ? kStageBytes : McStage<NC>::kBytes;
+  static_assert(S * 32 * 16 <= kStageFloat4 * 16, "chirp stash exceeds the window stage");
+  float4* stash = reinterpret_cast<float4*>(smem_raw + static_cast<size_t>(3 * S) * sp.bd * sizeof(double) +
+                                            static_cast<size_t>(threadIdx.x >> 5) * kStage);
+  const double2 *pr0 = plane(kp, op, 0), *pq = plane(kp, op, 1), *pct = plane(kp, op, 2), *pab = plane(kp, op, 3);
+  const float qsgn = (__ldg(&op->tmode) & 1) ? -1.f : 1.f;
+  for (int k0 = 0; k0 < cnt; k0 += kBlk) {
+    const int cb = min(kBlk, cnt - k0);
+    float ar[2][kChunkSlots], ai[2][kChunkSlots];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int j = 0; j < kChunkSlots; ++j) ar[h][j] = ai[h][j] = 0.f;
+#pragma unroll 1
+    for (int s = 0; s < S; ++s) {
+      if (!sp.act(s)) continue;
+      const int64_t i = sp.idx(s);
+      const double2 qd = __ldg(pq + i);
+      const cf q{static_cast<float>(qd.x), qsgn * static_cast<float>(qd.y)};
+      cf u, r;
+      if (k0 == 0) {
+        const double2 r0 = __ldg(pr0 + i), ct = __ldg(pct + i), ab = __ldg(pab + i);
+        double2 w = make_double2(1.0, 0.0);
+        if (NC == 1 && kp.w != nullptr) w = __ldg(reinterpret_cast<const double2*>(kp.w) + i);
+        const double x = sp.mx(s), y = sp.my(s);
+        u = cf{static_cast<float>(w.x * x - w.y * y), static_cast<float>(w.x * y + w.y * x)};
+        r = cf{static_cast<float>(r0.x), static_cast<float>(r0.y)};
+        sp.mx(s) = ct.x * x - ct.y * y;
+        sp.my(s) = ct.x * y + ct.y * x;
+        sp.mz(s) = fma(sp.mz(s), ab.x, ab.y);
+      } else {
+        const float4 v = stash[s * 32 + lane];
+        u = cf{v.x, v.y};
+        r = cf{v.z, v.w};
+      }
+      cf w[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        w[c] = cf{1.f, 0.f};
+        if (NC > 1 && kp.w32 != nullptr) {
+          const float2 wf = __ldg(kp.w32 + i * NC + c);
+          w[c] = cf{wf.x, wf.y};
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int j = 0; j < kSampPerChunk; ++j) {
+          if (h * kSampPerChunk + j < cb) {
+            u = cmul(u, r);
+            r = cmul(r, q);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+              if (NC == 1) {
+                ar[h][j] += u.r;
+                ai[h][j] += u.i;
+              } else {
+                ar[h][j * NC + c] += w[c].r * u.r - w[c].i * u.i;
+                ai[h][j * NC + c] += w[c].r * u.i + w[c].i * u.r;
+              }
+            }
+          }
+        }
+      }
+      if (k0 + kBlk < cnt) stash[s * 32 + lane] = make_float4(u.r, u.i, r.r, r.i);
+    }
+    strip.push(ar[0], ai[0], min(kSampPerChunk, cb) * NC, (s0 + k0) * NC);
+    if (cb > kSampPerChunk) strip.push(ar[1], ai[1], (cb - kSampPerChunk) * NC, (s0 + k0 + kSampPerChunk) * NC);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // the integrator
 // ---------------------------------------------------------------------------
 
@@ -661,15 +758,15 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
       // behind possibly-aliasing shared/global stores.
       constexpr int G = S < 4 ? S : 4;
       if (rc >= 0) {  // repeated interval: tabulated propagator
-        const double2* tb = reinterpret_cast<const double2*>(kp.rot) + static_cast<int64_t>(rc) * kp.n * 4;
+        const double2 *pc = plane(kp, op, 0), *pab = plane(kp, op, 1);
 #pragma unroll
         for (int g0 = 0; g0 < S; g0 += G) {
           double2 c[G], ab[G];
 #pragma unroll
           for (int g = 0; g < G; ++g) {
             const int64_t i = sp.act(g0 + g) ? sp.idx(g0 + g) : 0;
-            c[g] = __ldg(tb + i * 4 + 1);
-            ab[g] = __ldg(tb + i * 4 + 2);
+            c[g] = __ldg(pc + i);
+            ab[g] = __ldg(pab + i);
           }
 #pragma unroll
           for (int g = 0; g < G; ++g) {
@@ -682,16 +779,17 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
         }
       } else if (pg >= 0) {  // one member of an interval progression: C, then C *= q^adv
         const int adv = __ldg(&op->flags);  // 0 (last member), 1 or 2
-        double2* tb = reinterpret_cast<double2*>(kp.prog) + static_cast<int64_t>(pg) * kp.n * 4;
+        double2* prun = kp.planes + static_cast<int64_t>(__ldg(&op->pl[0])) * kp.n;
+        const double2 *pq = plane(kp, op, adv == 2 ? 2 : 1), *pab = plane(kp, op, 3);  // q or q^2
 #pragma unroll
         for (int g0 = 0; g0 < S; g0 += G) {
           double2 c[G], ab[G], q[G];
 #pragma unroll
           for (int g = 0; g < G; ++g) {
             const int64_t i = sp.act(g0 + g) ? sp.idx(g0 + g) : 0;
-            c[g] = __ldcg(tb + i * 4);  // running factor: L2-coherent (rewritten below)
-            ab[g] = __ldg(tb + i * 4 + 3);
-            q[g] = adv ? __ldg(tb + i * 4 + adv) : make_double2(1.0, 0.0);  // [1] = q, [2] = q^2
+            c[g] = __ldcg(prun + i);  // running factor: L2-coherent (rewritten below)
+            ab[g] = __ldg(pab + i);
+            q[g] = adv ? __ldg(pq + i) : make_double2(1.0, 0.0);
           }
 #pragma unroll
           for (int g = 0; g < G; ++g) {
@@ -701,7 +799,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
             sp.my(s) = c[g].x * y + c[g].y * x;
             sp.mz(s) = fma(sp.mz(s), ab[g].x, ab[g].y);
             if (adv && sp.act(s))
-              __stcg(tb + sp.idx(s) * 4, make_double2(c[g].x * q[g].x - c[g].y * q[g].y,
+              __stcg(prun + sp.idx(s), make_double2(c[g].x * q[g].x - c[g].y * q[g].y,
                                                       c[g].x * q[g].y + c[g].y * q[g].x));
           }
         }
@@ -864,6 +962,12 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
       const double d0x = __ldg(&op->p[1]), d0y = __ldg(&op->p[2]), d0z = __ldg(&op->p[3]);
       const double ddx = __ldg(&op->p[4]), ddy = __ldg(&op->p[5]), ddz = __ldg(&op->p[6]);
       constexpr int kBlk = 2 * kSampPerChunk;
+      if constexpr (sizeof(R) == 4) {
+        if (crc >= 0) {  // tabulated chirp, fp32 samples (see chirp_f32 below)
+          chirp_f32<S, NC>(kp, op, sp, strip, smem_raw, cnt, s0);
+          continue;
+        }
+      }
       for (int k0 = 0; k0 < cnt; k0 += kBlk) {
         const int cb = min(kBlk, cnt - k0);
         R ar[2][kChunkSlots], ai[2][kChunkSlots];
@@ -876,27 +980,29 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
           if (!sp.act(s)) continue;
           const int64_t i = sp.idx(s);
           double rr, ri, qc, qs, e1, rgw;
-          if (crc >= 0) {  // tabulated chirp class: r0, q, q^8, (A, B)
-            const double2* tb = reinterpret_cast<const double2*>(kp.chirp) + (static_cast<int64_t>(crc) * kp.n + i) * 4;
-            const double2 r0 = __ldg(tb), q = __ldg(tb + 1), ab = __ldg(tb + 3);
+          if (crc >= 0) {  // tabulated chirp class (fp64 mode): planes r0, q (conj if tmode), (A, B) of the run
+            const double2 r0 = __ldg(plane(kp, op, 0) + i);
+            double2 q = __ldg(plane(kp, op, 1) + i);
+            if (__ldg(&op->tmode) & 1) q.y = -q.y;
             rr = r0.x;
             ri = r0.y;
             if (k0 > 0) {  // advance to event k0 by q^kBlk per block (chirps are a block or two long)
-              // kBlk = 16 / NC events per block: q^kBlk from the tabulated q^8 (NC <= 2) or from q (NC >= 4)
-              double2 qb = kBlk >= 8 ? __ldg(tb + 2) : q;
+              double2 qb = q;
 #pragma unroll
-              for (int m = kBlk >= 8 ? 8 : 1; m < kBlk; m <<= 1)
-                qb = make_double2(qb.x * qb.x - qb.y * qb.y, 2.0 * qb.x * qb.y);
+              for (int m = 1; m < kBlk; m <<= 1) qb = make_double2(qb.x * qb.x - qb.y * qb.y, 2.0 * qb.x * qb.y);
               for (int a = 0; a < k0; a += kBlk) {
                 const double r0r = rr;
                 rr = r0r * qb.x - ri * qb.y;
                 ri = r0r * qb.y + ri * qb.x;
               }
+            } else {  // mz never enters a sample: the run's longitudinal map at once
+              const double2 ab = __ldg(plane(kp, op, 3) + i);
+              sp.mz(s) = fma(sp.mz(s), ab.x, ab.y);
             }
             qc = q.x;
             qs = q.y;
-            e1 = ab.x;
-            rgw = ab.y;
+            e1 = 1.0;
+            rgw = 0.0;
           } else {
             const SC c = load_sc(kp, i);
             const double2 e = cls >= 0 ? relax_pair(kp, cls, i) : make_double2(1.0, 1.0);
@@ -962,8 +1068,8 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
           double2* pf = reinterpret_cast<double2*>(stb + kStageFloat4 * 16 + 2 * McStage<NC>::kW);
           const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
           float2* out = reinterpret_cast<float2*>(strip.row);
-          const double2* tb = rc >= 0 ? reinterpret_cast<const double2*>(kp.rot) + static_cast<int64_t>(rc) * kp.n * 4
-                                      : nullptr;
+          const bool tb = rc >= 0;  // tabulated: planes Cpre, z, C, (A, B)
+          const double2 *pcp = tb ? plane(kp, op, 0) : nullptr, *pz = tb ? plane(kp, op, 1) : nullptr;
           const int ntile = (cnt + 63) >> 6;
           for (int j = 0; j < ntile; ++j) {
             const bool last = j + 1 == ntile;
@@ -973,9 +1079,9 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
             auto fetch = [&](int r, int buf) {  // (Cpre, z) and the coil weights of this lane's spin r
               if (!sp.act(r)) return;
               const int64_t i = sp.idx(r);
-              if (tb != nullptr) {
-                cp_async16(pf + 2 * lane, tb + i * 4);
-                cp_async16(pf + 2 * lane + 1, tb + i * 4 + 3);
+              if (tb) {
+                cp_async16(pf + 2 * lane, pcp + i);
+                cp_async16(pf + 2 * lane + 1, pz + i);
               }
               const float2* wsrc = kp.w32 + i * NC;
 #pragma unroll
@@ -999,7 +1105,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
                 const int64_t i = sp.idx(r);
                 double pr = cpre.x, pi = cpre.y, zr0 = zz.x, zi0 = zz.y, th = 0.0;
                 SC c{};
-                if (tb == nullptr) {
+                if (!tb) {
                   const int c1 = __ldg(&op->cls);
                   c = load_sc(kp, i);
                   th = theta_of(c, __ldg(&op->p[0]), __ldg(&op->p[1]), __ldg(&op->p[2]), __ldg(&op->p[3]));
@@ -1016,7 +1122,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
                 if (!lead) u = cmul(u, z);
                 const cf z64 = csq(csq(csq(csq(csq(csq(z))))));
                 for (int q = 0; q < j; ++q) u = cmul(u, z64);  // this tile starts at sample 64 j
-                if (tb == nullptr && last) {
+                if (!tb && last) {
                   const int cw = __ldg(&op->flags);
                   const double2 E = cw >= 0 ? relax_pair(kp, cw, i) : make_double2(1.0, 1.0);
                   double cr, ci;
@@ -1038,11 +1144,12 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
               if (k2 < cnt) __stcs(out + static_cast<int64_t>(s0 + k2) * NC + c, make_float2(acc[c][1], acc[c][3]));
             }
           }
-          if (tb != nullptr) {
+          if (tb) {
+            const double2 *pc = plane(kp, op, 2), *pab = plane(kp, op, 3);
 #pragma unroll
             for (int r = 0; r < S; ++r) {
               const int64_t i = sp.act(r) ? sp.idx(r) : 0;
-              const double2 c = __ldg(tb + i * 4 + 1), ab = __ldg(tb + i * 4 + 2);
+              const double2 c = __ldg(pc + i), ab = __ldg(pab + i);
               const double x = sp.mx(r), y = sp.my(r);
               sp.mx(r) = c.x * x - c.y * y;
               sp.my(r) = c.x * y + c.y * x;
@@ -1061,8 +1168,8 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
           double2* pf = reinterpret_cast<double2*>(stb + kStageFloat4 * 16 + 32 * 8);  // [lane][Cpre, z]
           const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
           float2* out = reinterpret_cast<float2*>(strip.row) + s0;
-          const double2* tb = rc >= 0 ? reinterpret_cast<const double2*>(kp.rot) + static_cast<int64_t>(rc) * kp.n * 4
-                                      : nullptr;
+          const bool tb = rc >= 0;  // tabulated: planes Cpre, z, C, (A, B)
+          const int pcp = __ldg(&op->pl[0]), pz = __ldg(&op->pl[1]);  // plane ids (32-bit: fewer live registers)
           constexpr int kMaxTiles = kFull ? 4 : 8;  // 64-sample tiles per pass (4 accumulators each)
           for (int p0 = 0; p0 < cnt; p0 += 64 * kMaxTiles) {  // passes of up to kMaxTiles tiles of 64 samples
             const int ntile = min(kMaxTiles, (cnt - p0 + 63) >> 6);
@@ -1070,9 +1177,9 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
             float acc[kMaxTiles][4];
 #pragma unroll
             for (int j = 0; j < kMaxTiles; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-            if (tb != nullptr && sp.act(0)) {  // (Cpre, z) of round 0 into this lane's prefetch slot
-              cp_async16(pf + 2 * lane, tb + sp.idx(0) * 4);
-              cp_async16(pf + 2 * lane + 1, tb + sp.idx(0) * 4 + 3);
+            if (tb && sp.act(0)) {  // (Cpre, z) of round 0 into this lane's prefetch slot
+              cp_async16(pf + 2 * lane, plane_at(kp, pcp, sp.idx(0)));
+              cp_async16(pf + 2 * lane + 1, plane_at(kp, pz, sp.idx(0)));
             }
             cp_async_commit();
 #pragma unroll 1
@@ -1080,9 +1187,9 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
               cf u{0.f, 0.f}, z{0.f, 0.f};
               cp_async_wait_all();
               const double2 cpre = pf[2 * lane], zz = pf[2 * lane + 1];
-              if (tb != nullptr && r + 1 < S && sp.act(r + 1)) {  // next round's row lands during this round's mma
-                cp_async16(pf + 2 * lane, tb + sp.idx(r + 1) * 4);
-                cp_async16(pf + 2 * lane + 1, tb + sp.idx(r + 1) * 4 + 3);
+              if (tb && r + 1 < S && sp.act(r + 1)) {  // next round's (Cpre, z) lands during this round's mma
+                cp_async16(pf + 2 * lane, plane_at(kp, pcp, sp.idx(r + 1)));
+                cp_async16(pf + 2 * lane + 1, plane_at(kp, pz, sp.idx(r + 1)));
               }
               cp_async_commit();
               if (sp.act(r)) {
@@ -1090,7 +1197,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
                 double pr = cpre.x, pi = cpre.y, zr0 = zz.x, zi0 = zz.y;
                 double th = 0.0;
                 SC c{};
-                if (tb == nullptr) {  // on the fly: a window whose interval is not reused
+                if (!tb) {  // on the fly: a window whose interval is not reused
                   const int c1 = __ldg(&op->cls);
                   c = load_sc(kp, i);
                   th = theta_of(c, __ldg(&op->p[0]), __ldg(&op->p[1]), __ldg(&op->p[2]), __ldg(&op->p[3]));
@@ -1102,7 +1209,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
                   pi = 0.0;
                 }
                 double2 w0 = make_double2(1.0, 0.0);  // tabulated windows carry w in Cpre
-                if (kp.w != nullptr && tb == nullptr) w0 = __ldg(reinterpret_cast<const double2*>(kp.w) + i);
+                if (kp.w != nullptr && !tb) w0 = __ldg(reinterpret_cast<const double2*>(kp.w) + i);
                 const double x = sp.mx(r), y = sp.my(r);
                 const double x0 = pr * x - pi * y, y0 = pr * y + pi * x;
                 u = cf{static_cast<float>(w0.x * x0 - w0.y * y0), static_cast<float>(w0.x * y0 + w0.y * x0)};
@@ -1114,7 +1221,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
                   for (int q = 1; q < 64 * kMaxTiles; q <<= 1) zp = csq(zp);  // z^(64 kMaxTiles)
                   for (int q = 0; q < p0; q += 64 * kMaxTiles) u = cmul(u, zp);
                 }
-                if (tb == nullptr && last) {  // exit propagator of the whole run, on the fly
+                if (!tb && last) {  // exit propagator of the whole run, on the fly
                   const int cw = __ldg(&op->flags);
                   const double2 E = cw >= 0 ? relax_pair(kp, cw, i) : make_double2(1.0, 1.0);
                   double cr, ci;
@@ -1138,13 +1245,14 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
               }
             }
           }
-          if (tb != nullptr) {  // exit: C m, mz -> A mz + B for all spins, loads issued together
+          if (tb) {  // exit: C m, mz -> A mz + B for all spins, loads issued together
+            const double2 *pc = plane(kp, op, 2), *pab = plane(kp, op, 3);
             double2 c[S], ab[S];
 #pragma unroll
             for (int r = 0; r < S; ++r) {
               const int64_t i = sp.act(r) ? sp.idx(r) : 0;
-              c[r] = __ldg(tb + i * 4 + 1);
-              ab[r] = __ldg(tb + i * 4 + 2);
+              c[r] = __ldg(pc + i);
+              ab[r] = __ldg(pab + i);
             }
 #pragma unroll
             for (int r = 0; r < S; ++r) {
@@ -1169,7 +1277,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
         const int64_t i = sp.idx(s);
         RotCoef k;
         if (rc >= 0) {  // tabulated (pre, window, post) propagators
-          k = load_rot(kp, rc, i);
+          k = load_rot(kp, op, i);
         } else {  // on the fly: a window whose interval is not reused
           const int c1 = __ldg(&op->cls), cw = __ldg(&op->flags);
           const double dt = __ldg(&op->p[0]);
@@ -1356,81 +1464,36 @@ __global__ void relax_table_kernel(int64_t n, int n_cls, const double* __restric
   }
 }
 
-// rotation-class propagators, fp64 (program.h RotClass): for class c and spin i
-//   Cpre = e2(pre) e^{-i th_pre}; C = e^{-T/T2} e^{-i (th_pre + m th + th_post)};
-//   A = e^{-T/T1}, B = m0 (1 - A); z = e2(main) e^{-i th}
-// w1: single-coil receive weights (or nullptr): folded into Cpre, so a window forms
-// u = (w Cpre) m straight from the table (no per-window weight load)
-__global__ void rot_table_kernel(int64_t n, int n_cls, const RotClass* __restrict__ rc,
-                                 const SpinConst* __restrict__ sc, const double2* __restrict__ w1,
-                                 double2* __restrict__ out) {
-  const int64_t total = static_cast<int64_t>(n_cls) * n;
+// planes (program.h PlaneDesc), fp64, one thread per (plane, spin):
+//   PL_PHASE: exp(-T/T2) exp(-i (pos . d + dw tw))  (x w1[i] if PL_WEIGHT and single-coil weights are given)
+//   PL_AB:    (exp(-T/T1), m0 (1 - exp(-T/T1)))
+// e.g. a rotation class (pre, m x main, post) gives Cpre = PHASE(pre), z = PHASE(main),
+// C = PHASE(pre + m main + post) and AB(T) with T its whole duration (relax_cache
+// restated, engine.py:292-299, for every interval length the program reuses).
+__global__ void plane_kernel(int64_t n, int n_planes, const PlaneDesc* __restrict__ pd,
+                             const SpinConst* __restrict__ sc, const double2* __restrict__ w1,
+                             double2* __restrict__ out) {
+  const int64_t total = static_cast<int64_t>(n_planes) * n;
   for (int64_t t = gtid(); t < total; t += gstride()) {
     const int64_t c = t / n, i = t - c * n;
-    const RotClass& k = rc[c];
+    const PlaneDesc& k = pd[c];
     const SpinConst s = sc[i];
-    auto theta = [&](const double* iv) { return fma(s.z, iv[3], fma(s.y, iv[2], s.x * iv[1])) + s.dw * iv[0]; };
-    const double th_pre = theta(k.pre), th = theta(k.main), th_post = theta(k.post);
-    const double T = k.pre[0] + k.main[0] * k.mult + k.post[0];
-    double pc, ps, c1, s1, tc, ts;
-    phase_factor(th_pre, pc, ps);
-    phase_factor(th, c1, s1);
-    phase_factor(th_pre + th * k.mult + th_post, tc, ts);
-    const double ep = exp(-k.pre[0] * s.r2), e2 = exp(-k.main[0] * s.r2);
-    const double E2 = exp(-T * s.r2), E1 = exp(-T * s.r1);
-    double2* o = out + t * 4;
-    const double2 w = w1 != nullptr ? w1[i] : make_double2(1.0, 0.0);
-    o[0] = make_double2(w.x * (ep * pc) - w.y * (ep * ps), w.x * (ep * ps) + w.y * (ep * pc));
-    o[1] = make_double2(E2 * tc, E2 * ts);
-    o[2] = make_double2(E1, s.m0 * (1.0 - E1));
-    o[3] = make_double2(e2 * c1, e2 * s1);
-  }
-}
-
-// progression classes (program.h ProgClass): running factor C0 = e2 e^{-i th_0},
-// step q = e^{-i th_step} (same dt, so no off-resonance term), A = e1, B = m0 (1 - e1)
-__global__ void prog_table_kernel(int64_t n, int n_cls, const ProgClass* __restrict__ pc,
-                                  const SpinConst* __restrict__ sc, double2* __restrict__ out) {
-  const int64_t total = static_cast<int64_t>(n_cls) * n;
-  for (int64_t t = gtid(); t < total; t += gstride()) {
-    const int64_t c = t / n, i = t - c * n;
-    const ProgClass& k = pc[c];
-    const SpinConst s = sc[i];
-    const double th0 = fma(s.z, k.d0[2], fma(s.y, k.d0[1], s.x * k.d0[0])) + s.dw * k.dt;
-    const double thq = fma(s.z, k.step[2], fma(s.y, k.step[1], s.x * k.step[0]));
-    double c0, s0, cq, sq;
-    phase_factor(th0, c0, s0);
-    phase_factor(thq, cq, sq);
-    const double e2 = exp(-k.dt * s.r2), e1 = exp(-k.dt * s.r1);
-    double2* o = out + t * 4;
-    o[0] = make_double2(e2 * c0, e2 * s0);
-    o[1] = make_double2(cq, sq);
-    o[2] = make_double2(cq * cq - sq * sq, 2.0 * cq * sq);  // q^2: a member skipped in the series
-    o[3] = make_double2(e1, s.m0 * (1.0 - e1));
-  }
-}
-
-// chirp classes (program.h ChirpClass): r0 = e2 e^{-i th_0}, q = e^{-i th_dd},
-// q^8 = one chunk of kChunkSlots events ahead, (A, B) = (e1, m0 (1 - e1))
-__global__ void chirp_table_kernel(int64_t n, int n_cls, const ChirpClass* __restrict__ cc,
-                                   const SpinConst* __restrict__ sc, double2* __restrict__ out) {
-  const int64_t total = static_cast<int64_t>(n_cls) * n;
-  for (int64_t t = gtid(); t < total; t += gstride()) {
-    const int64_t c = t / n, i = t - c * n;
-    const ChirpClass& k = cc[c];
-    const SpinConst s = sc[i];
-    const double th0 = fma(s.z, k.d0[2], fma(s.y, k.d0[1], s.x * k.d0[0])) + s.dw * k.dt;
-    const double thq = fma(s.z, k.dd[2], fma(s.y, k.dd[1], s.x * k.dd[0]));
-    double c0, s0, cq, sq, c8, s8;
-    phase_factor(th0, c0, s0);
-    phase_factor(thq, cq, sq);
-    phase_factor(thq * static_cast<double>(kChunkSlots), c8, s8);
-    const double e2 = exp(-k.dt * s.r2), e1 = exp(-k.dt * s.r1);
-    double2* o = out + t * 4;
-    o[0] = make_double2(e2 * c0, e2 * s0);
-    o[1] = make_double2(cq, sq);
-    o[2] = make_double2(c8, s8);
-    o[3] = make_double2(e1, s.m0 * (1.0 - e1));
+    if (k.kind == PL_AB) {
+      const double e1 = exp(-k.T * s.r1);
+      out[t] = make_double2(e1, s.m0 * (1.0 - e1));
+      continue;
+    }
+    double pc, ps;
+    phase_factor(fma(s.z, k.d[2], fma(s.y, k.d[1], s.x * k.d[0])) + s.dw * k.tw, pc, ps);
+    const double e2 = k.T != 0.0 ? exp(-k.T * s.r2) : 1.0;
+    pc *= e2;
+    ps *= e2;
+    if ((k.flags & PL_WEIGHT) && w1 != nullptr) {
+      const double2 w = w1[i];
+      out[t] = make_double2(w.x * pc - w.y * ps, w.x * ps + w.y * pc);
+    } else {
+      out[t] = make_double2(pc, ps);
+    }
   }
 }
 
@@ -1577,27 +1640,11 @@ cudaError_t launch_relax_table(int64_t n, int n_cls, const double* T, const Spin
   return cudaGetLastError();
 }
 
-cudaError_t launch_rot_table(int64_t n, int n_cls, const RotClass* rc, const SpinConst* sc, const double* w1,
-                             double* out, cudaStream_t stream) {
-  if (n == 0 || n_cls == 0) return cudaSuccess;
-  rot_table_kernel<<<grid_for(static_cast<int64_t>(n_cls) * n, 256), 256, 0, stream>>>(
-      n, n_cls, rc, sc, reinterpret_cast<const double2*>(w1), reinterpret_cast<double2*>(out));
-  return cudaGetLastError();
-}
-
-cudaError_t launch_prog_table(int64_t n, int n_cls, const ProgClass* pc, const SpinConst* sc, double* out,
-                              cudaStream_t stream) {
-  if (n == 0 || n_cls == 0) return cudaSuccess;
-  prog_table_kernel<<<grid_for(static_cast<int64_t>(n_cls) * n, 256), 256, 0, stream>>>(
-      n, n_cls, pc, sc, reinterpret_cast<double2*>(out));
-  return cudaGetLastError();
-}
-
-cudaError_t launch_chirp_table(int64_t n, int n_cls, const ChirpClass* cc, const SpinConst* sc, double* out,
-                               cudaStream_t stream) {
-  if (n == 0 || n_cls == 0) return cudaSuccess;
-  chirp_table_kernel<<<grid_for(static_cast<int64_t>(n_cls) * n, 256), 256, 0, stream>>>(
-      n, n_cls, cc, sc, reinterpret_cast<double2*>(out));
+cudaError_t launch_planes(int64_t n, int n_planes, const PlaneDesc* pd, const SpinConst* sc, const double* w1,
+                          double* out, cudaStream_t stream) {
+  if (n == 0 || n_planes == 0) return cudaSuccess;
+  plane_kernel<<<grid_for(static_cast<int64_t>(n_planes) * n, 256), 256, 0, stream>>>(
+      n, n_planes, pd, sc, reinterpret_cast<const double2*>(w1), reinterpret_cast<double2*>(out));
   return cudaGetLastError();
 }
 

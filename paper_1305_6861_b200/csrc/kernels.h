@@ -28,9 +28,8 @@ struct KParams {
   int64_t part_stride;           // n_samples * NC * 2
   double* snaps;                 // [n_snap][n][3] or nullptr
   const double* relax;           // [n_relax][n][2]: exp(-T_c/T1_i), exp(-T_c/T2_i)
-  const double* rot;             // [n_rot][n][8]: rotation-class propagators (rot_table_kernel)
-  double* prog;                  // [n_prog][n][8]: progression running factors (updated in place)
-  const double* chirp;           // [n_chirp][n][8]: chirp-class factors (chirp_table_kernel)
+  double2* planes;               // [n_planes][n]: class quantities (plane_kernel); progression running
+                                 // factors are updated in place, every other plane is read-only
   const double* train;           // [n_train][n][12]: train-class affine propagators (train_table_kernel)
   const float2* w32;             // fp32 multi-coil weights, spin-major [n][NC] (tensor-core windows), or nullptr
 };
@@ -79,12 +78,8 @@ cudaError_t launch_prep(int64_t n, const double* pos, const double* dw, const do
                         const double* t2, SpinConst* sc, cudaStream_t stream);
 cudaError_t launch_relax_table(int64_t n, int n_cls, const double* T, const SpinConst* sc, double* out,
                                cudaStream_t stream);
-cudaError_t launch_rot_table(int64_t n, int n_cls, const RotClass* rc, const SpinConst* sc, const double* w1,
-                             double* out, cudaStream_t stream);
-cudaError_t launch_prog_table(int64_t n, int n_cls, const ProgClass* pc, const SpinConst* sc, double* out,
-                              cudaStream_t stream);
-cudaError_t launch_chirp_table(int64_t n, int n_cls, const ChirpClass* cc, const SpinConst* sc, double* out,
-                               cudaStream_t stream);
+cudaError_t launch_planes(int64_t n, int n_planes, const PlaneDesc* pd, const SpinConst* sc, const double* w1,
+                          double* out, cudaStream_t stream);
 cudaError_t launch_train_table(int64_t n, int n_cls, const TrainClass* tc, const double* mats, const SpinConst* sc,
                                double* out, cudaStream_t stream);
 cudaError_t launch_pad_weights(int64_t n, int nc, int ncp, const double* w, double* out,

@@ -55,6 +55,7 @@ void find_progressions(Program& prog);
 void find_chirp_classes(Program& prog);
 void fuse_pulses(Program& prog);
 void find_train_classes(Program& prog);
+void assign_planes(Program& prog);
 
 void compile_program(const TablesView& t, Program& prog) {
   prog = Program();
@@ -485,6 +486,7 @@ void fuse_intervals(Program& prog, const std::function<int32_t(double)>& relax_c
   find_chirp_classes(prog);
   find_train_classes(prog);
   fuse_pulses(prog);
+  assign_planes(prog);
 }
 
 // A hard pulse followed by an interval or a window is applied by that op
@@ -555,6 +557,87 @@ void find_chirp_classes(Program& prog) {
       prog.chirp_classes.push_back(cc);
     }
     op.rot = f->second;
+  }
+}
+
+// Planes (program.h PlaneDesc): every class quantity an op reads becomes a plane
+// id in DevOp.pl; identical planes are stored once.  Pure gradient phases
+// (T = 0, tw = 0) are kept with a canonical sign, so a ramp and its mirror share
+// one q plane (the op conjugates).  Progression running factors are rewritten in
+// place and are never shared.
+void assign_planes(Program& prog) {
+  using Key = std::array<double, 7>;
+  std::map<Key, int32_t> ids;
+  auto plane = [&](int32_t kind, int32_t flags, double T, const double* d, double tw) -> int32_t {
+    PlaneDesc pd{};
+    pd.kind = kind;
+    pd.flags = flags;
+    pd.T = T;
+    for (int a = 0; a < 3; ++a) pd.d[a] = kind == PL_PHASE ? d[a] : 0.0;
+    pd.tw = kind == PL_PHASE ? tw : 0.0;
+    const Key key{static_cast<double>(kind * 16 + flags), pd.T, pd.d[0], pd.d[1], pd.d[2], pd.tw, 0.0};
+    if (!(flags & PL_MUTABLE)) {
+      auto f = ids.find(key);
+      if (f != ids.end()) return f->second;
+    }
+    const int32_t id = static_cast<int32_t>(prog.planes.size());
+    prog.planes.push_back(pd);
+    if (!(flags & PL_MUTABLE)) ids.emplace(key, id);
+    return id;
+  };
+  const double zero[3] = {0.0, 0.0, 0.0};
+  // pure gradient phase with a canonical sign: returns the plane, sets conj when d was negated
+  auto gphase = [&](const double* d, bool& conj) {
+    double c[3] = {d[0], d[1], d[2]};
+    conj = false;
+    for (int a = 0; a < 3; ++a)
+      if (c[a] != 0.0) {
+        conj = c[a] < 0.0;
+        break;
+      }
+    if (conj)
+      for (int a = 0; a < 3; ++a) c[a] = -c[a];
+    return plane(PL_PHASE, 0, 0.0, c, 0.0);
+  };
+  std::vector<std::array<int32_t, 4>> prog_pl(prog.prog_classes.size(), {-1, -1, -1, -1});
+  for (size_t k = 0; k < prog.prog_classes.size(); ++k) {
+    const ProgClass& pc = prog.prog_classes[k];
+    const double two[3] = {2.0 * pc.step[0], 2.0 * pc.step[1], 2.0 * pc.step[2]};
+    prog_pl[k] = {plane(PL_PHASE, PL_MUTABLE, pc.dt, pc.d0, pc.dt), plane(PL_PHASE, 0, 0.0, pc.step, 0.0),
+                  plane(PL_PHASE, 0, 0.0, two, 0.0), plane(PL_AB, 0, pc.dt, zero, 0.0)};
+  }
+  for (DevOp& op : prog.ops) {
+    op.pl[0] = op.pl[1] = op.pl[2] = op.pl[3] = -1;
+    if ((op.kind == OP_EVENT || op.kind == OP_WINDOW) && op.rot >= 0) {
+      const RotClass& rc = prog.rot_classes[op.rot];
+      const double T = rc.pre[0] + rc.main[0] * rc.mult + rc.post[0];
+      double d[3];
+      for (int a = 0; a < 3; ++a) d[a] = rc.pre[1 + a] + rc.main[1 + a] * rc.mult + rc.post[1 + a];
+      const int32_t C = plane(PL_PHASE, 0, T, d, T), AB = plane(PL_AB, 0, T, zero, 0.0);
+      if (op.kind == OP_EVENT) {
+        op.pl[0] = C;
+        op.pl[1] = AB;
+      } else {
+        op.pl[0] = plane(PL_PHASE, PL_WEIGHT, rc.pre[0], rc.pre + 1, rc.pre[0]);
+        op.pl[1] = plane(PL_PHASE, 0, rc.main[0], rc.main + 1, rc.main[0]);
+        op.pl[2] = C;
+        op.pl[3] = AB;
+      }
+    } else if (op.kind == OP_EVENT && op.prg >= 0) {
+      for (int q = 0; q < 4; ++q) op.pl[q] = prog_pl[op.prg][q];
+    } else if (op.kind == OP_CHIRP && op.rot >= 0) {
+      // sample k applies (dt, d0 + k dd): r_k = r0 q^k; the whole run is (K dt, K d0 + K(K-1)/2 dd)
+      const ChirpClass& cc = prog.chirp_classes[op.rot];
+      const double K = static_cast<double>(op.count), tri = 0.5 * K * (K - 1.0);
+      double d[3];
+      for (int a = 0; a < 3; ++a) d[a] = K * cc.d0[a] + tri * cc.dd[a];
+      bool conj = false;
+      op.pl[0] = plane(PL_PHASE, 0, cc.dt, cc.d0, cc.dt);
+      op.pl[1] = gphase(cc.dd, conj);
+      op.pl[2] = plane(PL_PHASE, 0, K * cc.dt, d, K * cc.dt);
+      op.pl[3] = plane(PL_AB, 0, K * cc.dt, zero, 0.0);
+      op.tmode = conj ? 1 : 0;
+    }
   }
 }
 

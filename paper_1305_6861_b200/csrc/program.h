@@ -55,8 +55,11 @@ struct alignas(16) DevOp {
                   // train class (RFTRAIN), -1 = none
   int32_t prg;    // EVENT: progression class (interval of an arithmetic series of moments), -1 = none
   int32_t pre;    // EVENT/WINDOW: hard pulse applied first (matrix index into mats, fused OP_ROT), -1 = none
-  int32_t tmode;  // RFTRAIN: 1 = every sub-pulse rotates about x (real envelope); EVENT/WINDOW: axis of `pre` (1 x, 2 y, 0 general)
-  int32_t pad[4];
+  int32_t tmode;  // RFTRAIN: 1 = every sub-pulse rotates about x (real envelope); EVENT/WINDOW: axis of `pre` (1 x, 2 y, 0 general);
+                  // CHIRP: 1 = the q plane holds conj(q)
+  int32_t pl[4];  // per-spin planes (PlaneDesc) of the op's class, see assign_planes() in program.cpp:
+                  //   EVENT rot: C, AB; EVENT prg: running factor, q, q^2, AB;
+                  //   WINDOW rot: Cpre, z, C, AB; CHIRP: r0, q, C_total, AB_total
 };
 
 // A rotation class: pre, then `mult` times main, then post (intervals (dt,
@@ -109,6 +112,25 @@ struct alignas(16) TrainClass {
 };
 static_assert(sizeof(TrainClass) == 64, "TrainClass must be 64 bytes");
 constexpr int kTrainRow = 12;  // doubles per (train class, spin)
+
+// A plane: one complex (double2) value per spin, tabulated once per call by
+// plane_kernel.  Every class quantity above (a rotation class's Cpre, C, z and
+// (A, B); a progression's running factor, q, q^2, (A, B); a chirp's r0, q,
+// whole-run propagator and (A, B)) is a plane, and identical planes are stored
+// once: e.g. the (A, B) of every interval of the same length, the q of ramps of
+// opposite slope (conjugates), the Cpre of every window without a pre-interval.
+// Each op reads exactly the planes it needs, coalesced (consecutive spins,
+// consecutive 16 B), and the shared planes stay in L2.
+//   PL_PHASE: exp(-T/T2) exp(-i (pos . d + dw tw))  (x w, the single-coil receive weight, if PL_WEIGHT)
+//   PL_AB:    (exp(-T/T1), m0 (1 - exp(-T/T1)))
+enum : int32_t { PL_PHASE = 1, PL_AB = 2 };
+enum : int32_t { PL_WEIGHT = 1, PL_MUTABLE = 2 };
+struct alignas(16) PlaneDesc {
+  int32_t kind, flags;
+  double T, d[3], tw;
+  double pad[2];
+};
+static_assert(sizeof(PlaneDesc) == 64, "PlaneDesc must be 64 bytes");
 
 struct alignas(16) GEv {  // one generic sampled interval
   double dt, dmx, dmy, dmz;

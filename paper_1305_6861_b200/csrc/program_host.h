@@ -31,6 +31,7 @@ struct Program {
   std::vector<ProgClass> prog_classes;
   std::vector<ChirpClass> chirp_classes;
   std::vector<TrainClass> train_classes;
+  std::vector<PlaneDesc> planes;  // per-spin class quantities (assign_planes)
   int32_t n_acq = 0, max_samples = 0, n_snap = 0;
   int64_t n_events = 0;  // reference table size incl. pulses
   int64_t n_samples = 0;
