@@ -112,9 +112,10 @@ int bloch_program_layout(const bloch_ctx* ctx, int64_t* n_ops, int64_t* n_rot_cl
  * small fp64 kernels before the integrator): progression classes (arithmetic
  * series of interval moments), chirp classes (reused trapezoid ramps under the
  * ADC), train classes (reused RF trains, composed into one affine propagator per
- * spin) and the RF-train ops that use them.  Any pointer may be NULL. */
+ * spin) and the RF-train ops that use them; planes (the distinct per-spin class
+ * quantities, 16 B per spin each).  Any pointer may be NULL. */
 int bloch_program_classes(const bloch_ctx* ctx, int64_t* n_prog_classes, int64_t* n_chirp_classes,
-                          int64_t* n_train_classes, int64_t* n_train_class_ops);
+                          int64_t* n_train_classes, int64_t* n_train_class_ops, int64_t* n_planes);
 
 /*
  * Evolve one spin block through the uploaded tables — compute_block.

@@ -74,7 +74,7 @@ SIGNATURES = {
     "bloch_program_layout": (
         c_int, [c_void_p, POINTER(c_int64), POINTER(c_int64), POINTER(c_int64), POINTER(c_int64)]),
     "bloch_program_classes": (
-        c_int, [c_void_p, POINTER(c_int64), POINTER(c_int64), POINTER(c_int64), POINTER(c_int64)]),
+        c_int, [c_void_p] + [POINTER(c_int64)] * 5),
     "bloch_compute_block": (
         c_int,
         [c_void_p, c_int64, _PD, _PD, _PD, _PD, _PD, _PD, _PD, _PD, _PD, c_int32, _PD, _PD,

@@ -392,13 +392,14 @@ int bloch_program_layout(const bloch_ctx* c, int64_t* n_ops, int64_t* n_rot_clas
 }
 
 int bloch_program_classes(const bloch_ctx* c, int64_t* n_prog_classes, int64_t* n_chirp_classes,
-                          int64_t* n_train_classes, int64_t* n_train_class_ops) {
+                          int64_t* n_train_classes, int64_t* n_train_class_ops, int64_t* n_planes) {
   if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
   if (!c->has_prog) return fail(BLOCH_E_STATE, "no tables uploaded");
   if (n_prog_classes) *n_prog_classes = static_cast<int64_t>(c->prog.prog_classes.size());
   if (n_chirp_classes) *n_chirp_classes = static_cast<int64_t>(c->prog.chirp_classes.size());
   if (n_train_classes) *n_train_classes = static_cast<int64_t>(c->prog.train_classes.size());
   if (n_train_class_ops) *n_train_class_ops = c->prog.n_train_class_ops;
+  if (n_planes) *n_planes = static_cast<int64_t>(c->prog.planes.size());
   return BLOCH_OK;
 }
 

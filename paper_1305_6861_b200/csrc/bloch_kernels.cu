@@ -151,6 +151,9 @@ __device__ __forceinline__ const double2* plane(const KParams& kp, const DevOp* 
 __device__ __forceinline__ const double2* plane_at(const KParams& kp, int id, int64_t i) {
   return kp.planes + (static_cast<int64_t>(id) * kp.n + i);
 }
+__device__ __forceinline__ double2 ab_at(const KParams& kp, const DevOp* op, int k, int64_t i) {
+  return __ldg(plane_at(kp, __ldg(&op->pl[k]), i));
+}
 // rotation-class quantities of a window: Cpre, C, (A, B), z
 struct RotCoef {
   double pr, pi, cr, ci, a, b, zr, zi;
@@ -436,6 +439,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifndef BLOCH_MMA_SPLIT
 #define BLOCH_MMA_SPLIT 2
 #endif
+#ifndef BLOCH_PACKED_ADVANCE
+#define BLOCH_PACKED_ADVANCE 1
+#endif
 __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
   hi = __float_as_uint(x) & 0xffffe000u;
 #if BLOCH_MMA_SPLIT == 3
@@ -503,6 +509,7 @@ __device__ __forceinline__ void mma_round_t(const float4* __restrict__ st, const
     split_tf32(e.y, aih, ail);
     const uint32_t naih = aih ^ 0x80000000u, nail = ail ^ 0x80000000u;
     uint32_t brh[NT], brl[NT], bih[NT], bil[NT];
+#if BLOCH_MMA_SPLIT == 3 || !BLOCH_PACKED_ADVANCE
     cf v{e.z, e.w};
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
@@ -510,6 +517,20 @@ __device__ __forceinline__ void mma_round_t(const float4* __restrict__ st, const
       split_tf32(v.i, bih[j], bil[j]);
       if (j + 1 < NT) v = cmul(v, z64);
     }
+#else
+    // packed (FFMA2/FMUL2) tile advance v <- v z^64 and residuals lo = v - hi: half the issue slots
+    float2 v = make_float2(e.z, e.w);
+    const float2 nz = make_float2(-z64.i, z64.r), zz = make_float2(z64.r, z64.i), m1 = make_float2(-1.f, -1.f);
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      brh[j] = __float_as_uint(v.x) & 0xffffe000u;
+      bih[j] = __float_as_uint(v.y) & 0xffffe000u;
+      const float2 lo = __ffma2_rn(make_float2(__uint_as_float(brh[j]), __uint_as_float(bih[j])), m1, v);
+      brl[j] = __float_as_uint(lo.x);
+      bil[j] = __float_as_uint(lo.y);
+      if (j + 1 < NT) v = __ffma2_rn(make_float2(v.y, v.y), nz, __fmul2_rn(make_float2(v.x, v.x), zz));
+    }
+#endif
 #pragma unroll
     for (int j = 0; j < NT; ++j) mma_tf32(acc[j], arh, aih, naih, arh, brh[j], bih[j]);
 #if BLOCH_MMA_SPLIT == 3
@@ -623,13 +644,43 @@ __device__ __forceinline__ void chirp_f32(const KParams& kp, const DevOp* op, Sp
                                           unsigned char* smem_raw, int cnt, int s0) {
   constexpr int kSampPerChunk = kChunkSlots / NC;
   constexpr int kBlk = 2 * kSampPerChunk;
+  constexpr int G = S < 4 ? S : 4;
   const int lane = threadIdx.x & 31;
   constexpr size_t kStage = NC == 1 ? kStageBytes : McStage<NC>::kBytes;
   static_assert(S * 32 * 16 <= kStageFloat4 * 16, "chirp stash exceeds the window stage");
   float4* stash = reinterpret_cast<float4*>(smem_raw + static_cast<size_t>(3 * S) * sp.bd * sizeof(double) +
                                             static_cast<size_t>(threadIdx.x >> 5) * kStage);
-  const double2 *pr0 = plane(kp, op, 0), *pq = plane(kp, op, 1), *pct = plane(kp, op, 2), *pab = plane(kp, op, 3);
+  const double2 *pr0 = plane(kp, op, 0), *pq = plane(kp, op, 1), *pct = plane(kp, op, 2);
   const float qsgn = (__ldg(&op->tmode) & 1) ? -1.f : 1.f;
+  // entry: u = w m into the stash, then the state leaves through the closed form (loads of a group of
+  // spins issued together, as in the interval handler)
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    double2 w = make_double2(1.0, 0.0);
+    if (NC == 1 && kp.w != nullptr && sp.act(s)) w = __ldg(reinterpret_cast<const double2*>(kp.w) + sp.idx(s));
+    const double x = sp.mx(s), y = sp.my(s);
+    stash[s * 32 + lane] =
+        make_float4(static_cast<float>(w.x * x - w.y * y), static_cast<float>(w.x * y + w.y * x), 0.f, 0.f);
+  }
+#pragma unroll
+  for (int g0 = 0; g0 < S; g0 += G) {
+    double2 ct[G], ab[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int64_t i = sp.act(g0 + g) ? sp.idx(g0 + g) : 0;
+      ct[g] = __ldg(pct + i);
+      ab[g] = ab_at(kp, op, 3, i);
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int s = g0 + g;
+      const double x = sp.mx(s), y = sp.my(s);
+      sp.mx(s) = ct[g].x * x - ct[g].y * y;
+      sp.my(s) = ct[g].x * y + ct[g].y * x;
+      sp.mz(s) = fma(sp.mz(s), ab[g].x, ab[g].y);
+    }
+  }
+  // samples: spin-outer per block; the next spin's (r0, q) loads are in flight while this spin runs
   for (int k0 = 0; k0 < cnt; k0 += kBlk) {
     const int cb = min(kBlk, cnt - k0);
     float ar[2][kChunkSlots], ai[2][kChunkSlots];
@@ -637,28 +688,22 @@ __device__ __forceinline__ void chirp_f32(const KParams& kp, const DevOp* op, Sp
     for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int j = 0; j < kChunkSlots; ++j) ar[h][j] = ai[h][j] = 0.f;
+    double2 nq = __ldg(pq + (sp.act(0) ? sp.idx(0) : 0)), nr = k0 == 0 ? __ldg(pr0 + (sp.act(0) ? sp.idx(0) : 0))
+                                                                       : make_double2(0.0, 0.0);
 #pragma unroll 1
     for (int s = 0; s < S; ++s) {
+      const double2 qd = nq, r0 = nr;
+      if (s + 1 < S) {
+        const int64_t in = sp.act(s + 1) ? sp.idx(s + 1) : 0;
+        nq = __ldg(pq + in);
+        if (k0 == 0) nr = __ldg(pr0 + in);
+      }
       if (!sp.act(s)) continue;
       const int64_t i = sp.idx(s);
-      const double2 qd = __ldg(pq + i);
       const cf q{static_cast<float>(qd.x), qsgn * static_cast<float>(qd.y)};
-      cf u, r;
-      if (k0 == 0) {
-        const double2 r0 = __ldg(pr0 + i), ct = __ldg(pct + i), ab = __ldg(pab + i);
-        double2 w = make_double2(1.0, 0.0);
-        if (NC == 1 && kp.w != nullptr) w = __ldg(reinterpret_cast<const double2*>(kp.w) + i);
-        const double x = sp.mx(s), y = sp.my(s);
-        u = cf{static_cast<float>(w.x * x - w.y * y), static_cast<float>(w.x * y + w.y * x)};
-        r = cf{static_cast<float>(r0.x), static_cast<float>(r0.y)};
-        sp.mx(s) = ct.x * x - ct.y * y;
-        sp.my(s) = ct.x * y + ct.y * x;
-        sp.mz(s) = fma(sp.mz(s), ab.x, ab.y);
-      } else {
-        const float4 v = stash[s * 32 + lane];
-        u = cf{v.x, v.y};
-        r = cf{v.z, v.w};
-      }
+      const float4 v = stash[s * 32 + lane];
+      cf u{v.x, v.y}, r{v.z, v.w};
+      if (k0 == 0) r = cf{static_cast<float>(r0.x), static_cast<float>(r0.y)};
       cf w[NC];
 #pragma unroll
       for (int c = 0; c < NC; ++c) {

@@ -352,9 +352,10 @@ class BlochEngine:
         lay = [ctypes.c_int64() for _ in range(4)]
         _capi.check(self._lib.bloch_program_layout(self._h, *[ctypes.byref(v) for v in lay]), "bloch_program_layout")
         out.update(zip(("ops", "rot_classes", "relax_classes", "onthefly_intervals"), (v.value for v in lay)))
-        cls = [ctypes.c_int64() for _ in range(4)]
+        cls = [ctypes.c_int64() for _ in range(5)]
         _capi.check(self._lib.bloch_program_classes(self._h, *[ctypes.byref(v) for v in cls]), "bloch_program_classes")
-        out.update(zip(("prog_classes", "chirp_classes", "train_classes", "train_class_ops"), (v.value for v in cls)))
+        out.update(zip(("prog_classes", "chirp_classes", "train_classes", "train_class_ops", "planes"),
+                       (v.value for v in cls)))
         return out
 
     def last_timing(self) -> Dict[str, float]:
