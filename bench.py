@@ -378,8 +378,9 @@ def main():
         pass
     # the contract's measured denominators (MEASURED_PEAKS.json), beside the SURVEY §8d model:
     # HBM traffic of the integrator (ncu capture) and the tensor pipe's actual work in the ADC
-    # windows (mma.sync tf32, 3 split passes x 4 real MAC per spin-sample-coil), whose measured
-    # peak is 512 MAC/clk/SM (profiles/r1_mma_microbench.txt).
+    # windows: per spin-sample-coil one tf32 m16n8k8 pass (4 real MAC at the measured 512 MAC/clk/SM)
+    # and one bf16 m16n8k16 pass for both cross terms (8 real MAC at 1024 MAC/clk/SM), i.e. 8
+    # tf32-rate MAC equivalents (profiles/r1_mma_microbench.txt).
     hbm_peak = bf16_peak = None
     try:
         with open(peaks_path) as fh:
@@ -387,7 +388,7 @@ def main():
         hbm_peak, bf16_peak = float(mp["hbm_gbs"]), float(mp["bf16_tflops"])
     except Exception:
         pass
-    w_mma = n_local * pstats["window_samples"] * C * 12 if args.precision == 32 else 0
+    w_mma = n_local * pstats["window_samples"] * C * 8 if args.precision == 32 else 0
     p_mma = n_sm * 512 * f_max * 1e6
     measured = {
         "hbm": {"achieved_gbs": traffic / t_kernel / 1e9 if traffic else None, "peak_gbs": hbm_peak,
@@ -395,8 +396,9 @@ def main():
                 "source": "peak of measured (MEASURED_PEAKS.json hbm_gbs)"},
         "tensor_mma_tf32": {"achieved_tflops": 2 * w_mma / t_kernel / 1e12, "peak_tflops": 2 * p_mma / 1e12,
                             "frac": w_mma / p_mma / t_kernel,
-                            "source": "peak of measured (mma.sync m16n8k8 tf32 512 MAC/clk/SM, "
-                                      "profiles/r1_mma_microbench.txt); bf16 GEMM peak of measured "
+                            "source": "tf32-rate MAC equivalents (tf32 hi*hi + bf16 k16 cross terms) over the "
+                                      "measured mma.sync m16n8k8 tf32 peak, 512 MAC/clk/SM "
+                                      "(profiles/r1_mma_microbench.txt); bf16 GEMM peak of measured "
                                       f"{bf16_peak} TFLOP/s is tcgen05 bf16 and does not apply"},
     }
     roofline = {
@@ -419,7 +421,7 @@ def main():
         "metric": metric, "value": value, "unit": metric, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_total_s * 1e3 / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None,
-        "dtype": ("f64 spin state/phase/fold; f32 ADC sums (3-pass split tf32 on the tensor cores)"
+        "dtype": ("f64 spin state/phase/fold; f32 ADC sums (tf32 hi*hi + bf16 cross terms on the tensor cores)"
                   if args.precision == 32 else "f64"),
         "data": "synthetic (seeded, BASELINE.json config recipe)",
         "config": {"workload": w.name, "config_index": w.index, "spins_total": w.n_spins, "spins_per_rank": n_local,
