@@ -48,6 +48,9 @@ import numpy as np  # noqa: E402
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="N > 1: weak = every rank integrates a full config-sized spin set (world interleaved "
+                         "copies of the lattice, parallel.weak_copy); strong = the config's spins sharded")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=1)
@@ -190,7 +193,7 @@ def main():
         line = {
             "metric": metric, "value": cb["value"], "unit": cb["unit"], "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["seconds_per_step"] * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, BASELINE.json config recipe)",
             "config": {"workload": w.name, "config_index": w.index, "spins_total": w.n_spins, "events_per_spin": E,
                        "coils": w.n_coils},
@@ -204,7 +207,7 @@ def main():
     import torch.distributed as dist
 
     from paper_1305_6861_b200.engine import _unit_weight, get_engine
-    from paper_1305_6861_b200.parallel import reduce_kspace, shard_block
+    from paper_1305_6861_b200.parallel import lattice_spacing, reduce_kspace, shard_block, weak_copy
 
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
@@ -221,9 +224,14 @@ def main():
     counts = event_counts(tables_plain)
     E = counts["events"]
     tables = precompute_sequence_tables(seq, snapshot_times=(seq.end_time,))  # final M is part of the output
-    shard = shard_block(w.block, world, rank)
+    weak = args.scaling == "weak"
+    if weak:
+        shard = weak_copy(w.block, world, rank, lattice_spacing(w.block.pos)) if world > 1 else w.block
+    else:
+        shard = shard_block(w.block, world, rank)
     n_local, C = shard.n, w.n_coils
-    log(f"[rank {rank}] config {w.index} {w.name}: {w.n_spins} spins ({n_local} local) x {E} events, "
+    n_total = world * n_local if weak else w.n_spins
+    log(f"[rank {rank}] config {w.index} {w.name}: {n_total} spins ({n_local} local, {args.scaling}) x {E} events, "
         f"setup {time.perf_counter() - t_setup:.1f}s", args.quiet)
 
     eng = get_engine(local_rank, args.precision)
@@ -287,7 +295,7 @@ def main():
     if world > 1:
         dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
     t_total_s, t_kernel_s = total_ms[0].item() / 1e3, total_ms[1].item() / 1e3
-    value = w.n_spins * E * args.steps / t_total_s
+    value = n_total * E * args.steps / t_total_s
 
     # ---- end to end through the public host API (pinned host buffers) ------------------
     e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
@@ -349,7 +357,7 @@ def main():
     e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
-    e2e_value = w.n_spins * E * e2e_steps / e2e_s.item()
+    e2e_value = n_total * E * e2e_steps / e2e_s.item()
     h2d = sum(a.nbytes for a in h.values()) + (0 if unit_w else wt.nbytes)
     d2h = out_e.nbytes + out_s.nbytes
 
@@ -420,11 +428,15 @@ def main():
     line = {
         "metric": metric, "value": value, "unit": metric, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_total_s * 1e3 / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None,
+        "scaling": args.scaling, "vs_baseline": None,
         "dtype": ("f64 spin state/phase/fold; f32 ADC sums (tf32 hi*hi + bf16 cross terms on the tensor cores)"
                   if args.precision == 32 else "f64"),
         "data": "synthetic (seeded, BASELINE.json config recipe)",
-        "config": {"workload": w.name, "config_index": w.index, "spins_total": w.n_spins, "spins_per_rank": n_local,
+        "config": {"workload": w.name, "config_index": w.index, "spins_total": n_total, "spins_per_rank": n_local,
+                   "sharding": ("weak: every rank a full config-sized spin set (world interleaved copies of the "
+                                "lattice, shifted by rank/world of its x spacing; parallel.weak_copy), one NCCL "
+                                "reduce of the k-space" if weak else "strong: np.linspace spin shards of the config")
+                               if world > 1 else "single GPU",
                    "events_per_spin": E, "coils": C, "event_classes": counts, "program": pstats,
                    "l2": "flushed between timed steps (256 MiB write)", "parallelism": f"spin-shards x{world}"},
         "roofline": roofline,

@@ -39,6 +39,32 @@ def shard_block(block: SpinBlock, world: int, rank: int) -> SpinBlock:
     )
 
 
+def lattice_spacing(pos: np.ndarray, axis: int = 0) -> float:
+    """Smallest positive spacing of the isochromat lattice along ``axis`` (0 if a single site)."""
+    u = np.unique(np.asarray(pos)[:, axis]) if len(pos) else np.zeros(0)
+    d = np.diff(u)
+    d = d[d > 0]
+    return float(d.min()) if d.size else 0.0
+
+
+def weak_copy(block: SpinBlock, world: int, rank: int, spacing: float) -> SpinBlock:
+    """Rank's spin set for weak scaling: the whole block, shifted by rank/world of the lattice spacing in x.
+
+    The global object is ``world`` interleaved copies of the block's isochromat lattice (world x the
+    isochromats per voxel along x); each isochromat of copy r keeps its site's tissue, off-resonance
+    and receive weight.  Rank 0's copy is the block itself, so one rank is exactly the single-GPU
+    workload, and each rank's work is fixed as the world grows.  The k-space is the sum over copies
+    (``reduce_kspace``).
+    """
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError(f"bad rank {rank} of {world}")
+    pos = np.array(block.pos, dtype=np.float64, copy=True)
+    if rank:
+        pos[:, 0] += spacing * rank / world
+    return SpinBlock(index=rank, pos=pos, mx=block.mx, my=block.my, mz=block.mz, t1=block.t1, t2=block.t2,
+                     m0=block.m0, domega=block.domega, weight=block.weight)
+
+
 def reduce_kspace(partial, dst: int = 0):
     """Sum a float64 partial k-space tensor over all ranks into ``dst`` (in place).
 

@@ -65,3 +65,53 @@ def test_two_rank_reduce_matches_single_process(tmp_path):
                                    b.t1, b.t2, b.m0, b.domega, b.weight)
     assert O.rel_l2(ref_e, got["echoes"]) <= 1e-13
     assert np.array_equal(ref_s[0], got["final"])
+
+
+def _weak_worker(rank, world, port, out_path):
+    import torch
+    import torch.distributed as dist
+
+    from oracle import bloch_oracle as O
+    from paper_1305_6861_b200 import configs
+    from paper_1305_6861_b200.parallel import lattice_spacing, reduce_kspace, weak_copy
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    w = configs.make(0).subset(8)
+    seq = w.sequence
+    tables = O.precompute_tables(seq)
+    mine = weak_copy(w.block, world, rank, lattice_spacing(configs.make(0).block.pos))
+    echoes, _ = O.compute_block(tables, mine.pos, mine.mx, mine.my, mine.mz, mine.t1, mine.t2, mine.m0,
+                                mine.domega, mine.weight)
+    t = torch.from_numpy(np.ascontiguousarray(echoes).view(np.float64).copy())
+    reduce_kspace(t, dst=0)
+    if rank == 0:
+        np.save(out_path, t.numpy().view(np.complex128).reshape(echoes.shape))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_weak_scaling_copies_sum_to_the_interleaved_object(tmp_path):
+    """bench.py --scaling weak: rank r integrates the whole lattice shifted by r/world of its x spacing;
+    the reduced k-space equals one process integrating all copies as one block."""
+    import torch.multiprocessing as mp
+
+    from oracle import bloch_oracle as O
+    from paper_1305_6861_b200 import configs
+    from paper_1305_6861_b200.parallel import lattice_spacing, weak_copy
+
+    out = str(tmp_path / "weak.npy")
+    mp.start_processes(_weak_worker, args=(2, _free_port(), out), nprocs=2, join=True, start_method="spawn")
+    got = np.load(out)
+    w = configs.make(0).subset(8)
+    h = lattice_spacing(configs.make(0).block.pos)
+    assert h > 0
+    c0, c1 = weak_copy(w.block, 2, 0, h), weak_copy(w.block, 2, 1, h)
+    assert np.array_equal(c0.pos, w.block.pos)  # rank 0 is the single-GPU workload
+    assert np.allclose(c1.pos[:, 0] - w.block.pos[:, 0], h / 2) and np.array_equal(c1.pos[:, 1:], w.block.pos[:, 1:])
+    cat = lambda a, b: np.concatenate([a, b], axis=-1)
+    both = {k: cat(getattr(c0, k), getattr(c1, k)) for k in ("mx", "my", "mz", "t1", "t2", "m0", "domega", "weight")}
+    ref, _ = O.compute_block(O.precompute_tables(w.sequence), np.vstack([c0.pos, c1.pos]), both["mx"], both["my"],
+                             both["mz"], both["t1"], both["t2"], both["m0"], both["domega"], both["weight"])
+    assert O.rel_l2(ref, got) <= 1e-13
