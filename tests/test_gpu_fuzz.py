@@ -258,3 +258,68 @@ def test_compiler_accepts_random_sequences_v2():
             assert eng.program_stats()["events"] == O.event_count(t), seed
     finally:
         eng.close()
+
+
+def random_sequence_v3(seed):
+    """Third generator: structures that the table compiler turns into shared per-spin tables — the same
+    shaped pulse under the same gradient several times (train class: one composed affine propagator per
+    spin) and alternating trapezoid readouts whose ramps mirror each other (chirp classes sharing a
+    conjugated q plane), between hard pulses and plain windows."""
+    rng = np.random.default_rng(20_000 + seed)
+    m = int(rng.integers(4, 40))
+    env = (np.hanning(m + 2)[1:-1] * float(rng.uniform(5e-7, 4e-6))).astype(complex)
+    if seed % 2:  # a complex envelope (phase-modulated): general sub-pulse axes
+        env = env * np.exp(1j * np.linspace(0.0, float(rng.uniform(0.5, 3.0)), m))
+    gz = float(rng.uniform(-4e-3, 4e-3))
+    g = float(rng.uniform(5e-4, 3e-3))
+    dur = float(rng.uniform(3e-4, 2e-3))
+    n_read = int(rng.integers(40, 160))
+    els, row = [], 0
+    for rep in range(int(rng.integers(2, 5))):
+        els.extend(expand_shaped_pulse(env, 1e-5, GradientWaveform.constant(gz=gz)))
+        els.append(ElementarySequence(duration=float(rng.uniform(2e-4, 1e-3))))
+        for line in range(2):
+            sign = 1.0 if line % 2 == 0 else -1.0
+            els.append(ElementarySequence(gradient=GradientWaveform.trapezoid(gx=sign * g, ramp_s=0.2 * dur,
+                                                                             flat_s=0.6 * dur),
+                                          duration=dur, acquisition=AcquisitionSpec(True, n_read), kspace_row=row,
+                                          kspace_reversed=bool(line)))
+            row += 1
+            els.append(ElementarySequence(gradient=GradientWaveform.constant(gy=3e-4), duration=4e-5))
+        els.append(ElementarySequence(pulse=HardPulse(float(rng.uniform(0.3, 2.0)), float(rng.uniform(0, 6.28))),
+                                      duration=float(rng.uniform(1e-4, 5e-4))))
+    return Sequence(els, name=f"fuzz3_{seed}")
+
+
+def _host_stats(seq):
+    from paper_1305_6861_b200.engine import BlochEngine
+
+    eng = BlochEngine(device=-1)
+    try:
+        eng.set_tables(precompute_sequence_tables(seq))
+        return eng.program_stats()
+    finally:
+        eng.close()
+
+
+def test_compiler_shares_trains_and_mirrored_ramps():
+    for seed in range(8):
+        st = _host_stats(random_sequence_v3(seed))
+        assert st["train_classes"] == 1 and st["train_class_ops"] >= 2, (seed, st)
+        assert st["chirp_classes"] >= 2 and st["chirp_samples"] > 0, (seed, st)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(16))
+def test_shared_tables_match_oracle(seed):
+    seq = random_sequence_v3(seed)
+    b = random_spins(seed)
+    snaps_t = (seq.end_time * 0.5, seq.end_time)
+    t = precompute_sequence_tables(seq, snapshot_times=snaps_t)
+    ot = O.precompute_tables(seq, snapshot_times=snaps_t)
+    ref_e, ref_s = O.compute_block(ot, b.pos, b.mx, b.my, b.mz, b.t1, b.t2, b.m0, b.domega, b.weight)
+    for precision, tol_k, tol_m in ((64, 1e-10, 1e-11), (32, 1e-4, 1e-9)):
+        e, s = compute_block(t, b, precision=precision)
+        assert O.rel_l2(ref_e, e) <= tol_k, (seed, precision, O.rel_l2(ref_e, e))
+        for a, r in zip(s, ref_s):
+            assert O.rel_l2(r, a) <= tol_m, (seed, precision, O.rel_l2(r, a))
