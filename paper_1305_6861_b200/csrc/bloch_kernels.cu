@@ -17,8 +17,8 @@
 //
 // Uniform ADC windows (OP_WINDOW): per spin the sample factor
 // z = e2 * exp(-i*theta) and the closed-form propagators of the whole
-// (pre, samples, post) run come from the rotation-class table (built once per
-// call by rot_table_kernel, fp64); the receive-weighted transverse
+// (pre, samples, post) run come from the per-spin planes of its rotation
+// class (plane_kernel, fp64, once per call); the receive-weighted transverse
 // magnetisation u = w * (Cpre m) is advanced by one complex multiply per sample
 // (engine.py:289-305 for every sample of the window: same theta, same e2 from
 // the relax cache).  The state leaving the window is C m, mz -> A mz + B in
