@@ -82,7 +82,7 @@ struct bloch_ctx {
   DevBuf d_ops, d_gev, d_mats, d_sample_g, d_relax_t, d_planes, d_train_cls;
   DevBuf in_pos, in_mx, in_my, in_mz, in_t1, in_t2, in_m0, in_dw, in_w;
   DevBuf sc, wpad, w32;
-  DevBuf partial, echo, snaps, relax, planetab, traintab;
+  DevBuf partial, echo, snaps, relax, planetab, planetab32, traintab;
   DevBuf raster_scratch;
   std::vector<unsigned char> raster_staging;
   float kernel_ms = 0.f, device_ms = 0.f;
@@ -285,7 +285,7 @@ int bloch_destroy(bloch_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   c->drop_graph();
-  for (DevBuf* b : {&c->d_ops, &c->d_gev, &c->d_mats, &c->d_sample_g, &c->d_relax_t, &c->relax, &c->d_planes, &c->planetab, &c->in_pos, &c->in_mx, &c->in_my, &c->in_mz,
+  for (DevBuf* b : {&c->d_ops, &c->d_gev, &c->d_mats, &c->d_sample_g, &c->d_relax_t, &c->relax, &c->d_planes, &c->planetab, &c->planetab32, &c->in_pos, &c->in_mx, &c->in_my, &c->in_mz,
                     &c->in_t1, &c->in_t2, &c->in_m0, &c->in_dw, &c->in_w, &c->sc, &c->wpad, &c->w32, &c->partial,
                     &c->echo, &c->snaps, &c->d_train_cls, &c->traintab,
                     &c->raster_scratch})
@@ -499,8 +499,10 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       const int n_planes = static_cast<int>(P.planes.size());
       if (n_planes > 0) {
         c->planetab.ensure(2 * nd * n_planes);
+        float2* p32 = nullptr;  // fp32 mode: the PL_SAMPLE planes as float2
+        if (c->precision == BLOCH_PREC_F32) p32 = static_cast<float2*>(c->planetab32.ensure(nd * n_planes));
         ck(bloch::launch_planes(n, n_planes, c->d_planes.as<bloch::PlaneDesc>(), d_sc, n_coils == 1 ? d_w : nullptr,
-                                c->planetab.as<double>(), st),
+                                c->planetab.as<double>(), p32, st),
            "plane kernel");
         c->launches++;
       }
@@ -581,6 +583,7 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       kp.snaps = d_snap;
       kp.relax = c->relax.as<double>();
       kp.planes = c->planetab.as<double2>();
+      kp.planes32 = c->precision == BLOCH_PREC_F32 ? c->planetab32.as<float2>() : nullptr;
       kp.train = c->traintab.as<double>();
       if (c->gate_wait) ck(cudaStreamWaitEvent(st, c->gate_wait, 0), "gate wait");
       ck(cudaEventRecordWithFlags(c->ev[1], st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault), "event");

@@ -151,6 +151,10 @@ __device__ __forceinline__ const double2* plane(const KParams& kp, const DevOp* 
 __device__ __forceinline__ const double2* plane_at(const KParams& kp, int id, int64_t i) {
   return kp.planes + (static_cast<int64_t>(id) * kp.n + i);
 }
+// fp32 mode: a PL_SAMPLE plane (window Cpre / z, chirp r0 / q) as float2
+__device__ __forceinline__ const float2* plane32_at(const KParams& kp, int id, int64_t i) {
+  return kp.planes32 + (static_cast<int64_t>(id) * kp.n + i);
+}
 __device__ __forceinline__ double2 ab_at(const KParams& kp, const DevOp* op, int k, int64_t i) {
   return __ldg(plane_at(kp, __ldg(&op->pl[k]), i));
 }
@@ -158,9 +162,19 @@ __device__ __forceinline__ double2 ab_at(const KParams& kp, const DevOp* op, int
 struct RotCoef {
   double pr, pi, cr, ci, a, b, zr, zi;
 };
+template <typename R>
 __device__ __forceinline__ RotCoef load_rot(const KParams& kp, const DevOp* op, int64_t i) {
-  const double2 a = __ldg(plane(kp, op, 0) + i), e = __ldg(plane(kp, op, 1) + i), b = __ldg(plane(kp, op, 2) + i),
-                d = __ldg(plane(kp, op, 3) + i);
+  const double2 b = __ldg(plane(kp, op, 2) + i), d = __ldg(plane(kp, op, 3) + i);
+  double2 a, e;
+  if constexpr (sizeof(R) == 4) {  // Cpre and z only form fp32 samples: float2 planes
+    const float2 af = __ldg(kp.planes32 + (static_cast<int64_t>(__ldg(&op->pl[0])) * kp.n + i));
+    const float2 ef = __ldg(kp.planes32 + (static_cast<int64_t>(__ldg(&op->pl[1])) * kp.n + i));
+    a = make_double2(af.x, af.y);
+    e = make_double2(ef.x, ef.y);
+  } else {
+    a = __ldg(plane(kp, op, 0) + i);
+    e = __ldg(plane(kp, op, 1) + i);
+  }
   return RotCoef{a.x, a.y, b.x, b.y, d.x, d.y, e.x, e.y};
 }
 
@@ -425,6 +439,10 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
@@ -650,7 +668,8 @@ __device__ __forceinline__ void chirp_f32(const KParams& kp, const DevOp* op, Sp
   static_assert(S * 32 * 16 <= kStageFloat4 * 16, "chirp stash exceeds the window stage");
   float4* stash = reinterpret_cast<float4*>(smem_raw + static_cast<size_t>(3 * S) * sp.bd * sizeof(double) +
                                             static_cast<size_t>(threadIdx.x >> 5) * kStage);
-  const double2 *pr0 = plane(kp, op, 0), *pq = plane(kp, op, 1), *pct = plane(kp, op, 2);
+  const float2 *pr0 = plane32_at(kp, __ldg(&op->pl[0]), 0), *pq = plane32_at(kp, __ldg(&op->pl[1]), 0);
+  const double2* pct = plane(kp, op, 2);
   const float qsgn = (__ldg(&op->tmode) & 1) ? -1.f : 1.f;
   // entry: u = w m into the stash, then the state leaves through the closed form (loads of a group of
   // spins issued together, as in the interval handler)
@@ -688,11 +707,11 @@ __device__ __forceinline__ void chirp_f32(const KParams& kp, const DevOp* op, Sp
     for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int j = 0; j < kChunkSlots; ++j) ar[h][j] = ai[h][j] = 0.f;
-    double2 nq = __ldg(pq + (sp.act(0) ? sp.idx(0) : 0)), nr = k0 == 0 ? __ldg(pr0 + (sp.act(0) ? sp.idx(0) : 0))
-                                                                       : make_double2(0.0, 0.0);
+    float2 nq = __ldg(pq + (sp.act(0) ? sp.idx(0) : 0)), nr = k0 == 0 ? __ldg(pr0 + (sp.act(0) ? sp.idx(0) : 0))
+                                                                      : make_float2(0.f, 0.f);
 #pragma unroll 1
     for (int s = 0; s < S; ++s) {
-      const double2 qd = nq, r0 = nr;
+      const float2 qd = nq, r0 = nr;
       if (s + 1 < S) {
         const int64_t in = sp.act(s + 1) ? sp.idx(s + 1) : 0;
         nq = __ldg(pq + in);
@@ -700,10 +719,10 @@ __device__ __forceinline__ void chirp_f32(const KParams& kp, const DevOp* op, Sp
       }
       if (!sp.act(s)) continue;
       const int64_t i = sp.idx(s);
-      const cf q{static_cast<float>(qd.x), qsgn * static_cast<float>(qd.y)};
+      const cf q{qd.x, qsgn * qd.y};
       const float4 v = stash[s * 32 + lane];
       cf u{v.x, v.y}, r{v.z, v.w};
-      if (k0 == 0) r = cf{static_cast<float>(r0.x), static_cast<float>(r0.y)};
+      if (k0 == 0) r = cf{r0.x, r0.y};
       cf w[NC];
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
@@ -1110,11 +1129,11 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
                       static_cast<size_t>(threadIdx.x >> 5) * McStage<NC>::kBytes;
           float4* st = reinterpret_cast<float4*>(stb);
           float2* wbuf = reinterpret_cast<float2*>(stb + kStageFloat4 * 16);  // 2 x [32][NC]
-          double2* pf = reinterpret_cast<double2*>(stb + kStageFloat4 * 16 + 2 * McStage<NC>::kW);
+          float2* pf = reinterpret_cast<float2*>(stb + kStageFloat4 * 16 + 2 * McStage<NC>::kW);  // [lane][Cpre, z]
           const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
           float2* out = reinterpret_cast<float2*>(strip.row);
-          const bool tb = rc >= 0;  // tabulated: planes Cpre, z, C, (A, B)
-          const double2 *pcp = tb ? plane(kp, op, 0) : nullptr, *pz = tb ? plane(kp, op, 1) : nullptr;
+          const bool tb = rc >= 0;  // tabulated: planes Cpre, z (float2), C, (A, B)
+          const int pcp = __ldg(&op->pl[0]), pz = __ldg(&op->pl[1]);
           const int ntile = (cnt + 63) >> 6;
           for (int j = 0; j < ntile; ++j) {
             const bool last = j + 1 == ntile;
@@ -1125,8 +1144,8 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
               if (!sp.act(r)) return;
               const int64_t i = sp.idx(r);
               if (tb) {
-                cp_async16(pf + 2 * lane, pcp + i);
-                cp_async16(pf + 2 * lane + 1, pz + i);
+                cp_async8(pf + 2 * lane, plane32_at(kp, pcp, i));
+                cp_async8(pf + 2 * lane + 1, plane32_at(kp, pz, i));
               }
               const float2* wsrc = kp.w32 + i * NC;
 #pragma unroll
@@ -1138,7 +1157,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
 #pragma unroll 1
             for (int r = 0; r < S; ++r) {
               cp_async_wait_all();
-              const double2 cpre = pf[2 * lane], zz = pf[2 * lane + 1];
+              const float2 cpre = pf[2 * lane], zz = pf[2 * lane + 1];
               if (!sp.act(r)) {  // inactive spin: zero weights (the buffer may hold another spin's)
 #pragma unroll
                 for (int c = 0; c < NC; ++c) wbuf[(r & 1) * 32 * NC + lane * NC + c] = make_float2(0.f, 0.f);
@@ -1210,7 +1229,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
                       static_cast<size_t>(threadIdx.x >> 5) * kStageBytes;
           float4* st = reinterpret_cast<float4*>(stb);
           float2* z64s = reinterpret_cast<float2*>(stb + kStageFloat4 * 16);
-          double2* pf = reinterpret_cast<double2*>(stb + kStageFloat4 * 16 + 32 * 8);  // [lane][Cpre, z]
+          float2* pf = reinterpret_cast<float2*>(stb + kStageFloat4 * 16 + 32 * 8);  // [lane][Cpre, z]
           const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
           float2* out = reinterpret_cast<float2*>(strip.row) + s0;
           const bool tb = rc >= 0;  // tabulated: planes Cpre, z, C, (A, B)
@@ -1223,18 +1242,18 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
 #pragma unroll
             for (int j = 0; j < kMaxTiles; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
             if (tb && sp.act(0)) {  // (Cpre, z) of round 0 into this lane's prefetch slot
-              cp_async16(pf + 2 * lane, plane_at(kp, pcp, sp.idx(0)));
-              cp_async16(pf + 2 * lane + 1, plane_at(kp, pz, sp.idx(0)));
+              cp_async8(pf + 2 * lane, plane32_at(kp, pcp, sp.idx(0)));
+              cp_async8(pf + 2 * lane + 1, plane32_at(kp, pz, sp.idx(0)));
             }
             cp_async_commit();
 #pragma unroll 1
             for (int r = 0; r < S; ++r) {
               cf u{0.f, 0.f}, z{0.f, 0.f};
               cp_async_wait_all();
-              const double2 cpre = pf[2 * lane], zz = pf[2 * lane + 1];
+              const float2 cpre = pf[2 * lane], zz = pf[2 * lane + 1];
               if (tb && r + 1 < S && sp.act(r + 1)) {  // next round's (Cpre, z) lands during this round's mma
-                cp_async16(pf + 2 * lane, plane_at(kp, pcp, sp.idx(r + 1)));
-                cp_async16(pf + 2 * lane + 1, plane_at(kp, pz, sp.idx(r + 1)));
+                cp_async8(pf + 2 * lane, plane32_at(kp, pcp, sp.idx(r + 1)));
+                cp_async8(pf + 2 * lane + 1, plane32_at(kp, pz, sp.idx(r + 1)));
               }
               cp_async_commit();
               if (sp.act(r)) {
@@ -1322,7 +1341,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
         const int64_t i = sp.idx(s);
         RotCoef k;
         if (rc >= 0) {  // tabulated (pre, window, post) propagators
-          k = load_rot(kp, op, i);
+          k = load_rot<R>(kp, op, i);
         } else {  // on the fly: a window whose interval is not reused
           const int c1 = __ldg(&op->cls), cw = __ldg(&op->flags);
           const double dt = __ldg(&op->p[0]);
@@ -1517,7 +1536,7 @@ __global__ void relax_table_kernel(int64_t n, int n_cls, const double* __restric
 // restated, engine.py:292-299, for every interval length the program reuses).
 __global__ void plane_kernel(int64_t n, int n_planes, const PlaneDesc* __restrict__ pd,
                              const SpinConst* __restrict__ sc, const double2* __restrict__ w1,
-                             double2* __restrict__ out) {
+                             double2* __restrict__ out, float2* __restrict__ out32) {
   const int64_t total = static_cast<int64_t>(n_planes) * n;
   for (int64_t t = gtid(); t < total; t += gstride()) {
     const int64_t c = t / n, i = t - c * n;
@@ -1535,10 +1554,14 @@ __global__ void plane_kernel(int64_t n, int n_planes, const PlaneDesc* __restric
     ps *= e2;
     if ((k.flags & PL_WEIGHT) && w1 != nullptr) {
       const double2 w = w1[i];
-      out[t] = make_double2(w.x * pc - w.y * ps, w.x * ps + w.y * pc);
-    } else {
-      out[t] = make_double2(pc, ps);
+      const double r = w.x * pc - w.y * ps;
+      ps = w.x * ps + w.y * pc;
+      pc = r;
     }
+    if ((k.flags & PL_SAMPLE) && out32 != nullptr)
+      out32[t] = make_float2(static_cast<float>(pc), static_cast<float>(ps));
+    else
+      out[t] = make_double2(pc, ps);
   }
 }
 
@@ -1686,10 +1709,10 @@ cudaError_t launch_relax_table(int64_t n, int n_cls, const double* T, const Spin
 }
 
 cudaError_t launch_planes(int64_t n, int n_planes, const PlaneDesc* pd, const SpinConst* sc, const double* w1,
-                          double* out, cudaStream_t stream) {
+                          double* out, float2* out32, cudaStream_t stream) {
   if (n == 0 || n_planes == 0) return cudaSuccess;
   plane_kernel<<<grid_for(static_cast<int64_t>(n_planes) * n, 256), 256, 0, stream>>>(
-      n, n_planes, pd, sc, reinterpret_cast<const double2*>(w1), reinterpret_cast<double2*>(out));
+      n, n_planes, pd, sc, reinterpret_cast<const double2*>(w1), reinterpret_cast<double2*>(out), out32);
   return cudaGetLastError();
 }
 

@@ -30,6 +30,7 @@ struct KParams {
   const double* relax;           // [n_relax][n][2]: exp(-T_c/T1_i), exp(-T_c/T2_i)
   double2* planes;               // [n_planes][n]: class quantities (plane_kernel); progression running
                                  // factors are updated in place, every other plane is read-only
+  const float2* planes32;        // fp32 mode: [n_planes][n] float2 copies of the PL_SAMPLE planes (same ids)
   const double* train;           // [n_train][n][12]: train-class affine propagators (train_table_kernel)
   const float2* w32;             // fp32 multi-coil weights, spin-major [n][NC] (tensor-core windows), or nullptr
 };
@@ -79,7 +80,7 @@ cudaError_t launch_prep(int64_t n, const double* pos, const double* dw, const do
 cudaError_t launch_relax_table(int64_t n, int n_cls, const double* T, const SpinConst* sc, double* out,
                                cudaStream_t stream);
 cudaError_t launch_planes(int64_t n, int n_planes, const PlaneDesc* pd, const SpinConst* sc, const double* w1,
-                          double* out, cudaStream_t stream);
+                          double* out, float2* out32, cudaStream_t stream);
 cudaError_t launch_train_table(int64_t n, int n_cls, const TrainClass* tc, const double* mats, const SpinConst* sc,
                                double* out, cudaStream_t stream);
 cudaError_t launch_pad_weights(int64_t n, int nc, int ncp, const double* w, double* out,

@@ -597,7 +597,7 @@ void assign_planes(Program& prog) {
       }
     if (conj)
       for (int a = 0; a < 3; ++a) c[a] = -c[a];
-    return plane(PL_PHASE, 0, 0.0, c, 0.0);
+    return plane(PL_PHASE, PL_SAMPLE, 0.0, c, 0.0);
   };
   std::vector<std::array<int32_t, 4>> prog_pl(prog.prog_classes.size(), {-1, -1, -1, -1});
   for (size_t k = 0; k < prog.prog_classes.size(); ++k) {
@@ -618,8 +618,8 @@ void assign_planes(Program& prog) {
         op.pl[0] = C;
         op.pl[1] = AB;
       } else {
-        op.pl[0] = plane(PL_PHASE, PL_WEIGHT, rc.pre[0], rc.pre + 1, rc.pre[0]);
-        op.pl[1] = plane(PL_PHASE, 0, rc.main[0], rc.main + 1, rc.main[0]);
+        op.pl[0] = plane(PL_PHASE, PL_WEIGHT | PL_SAMPLE, rc.pre[0], rc.pre + 1, rc.pre[0]);
+        op.pl[1] = plane(PL_PHASE, PL_SAMPLE, rc.main[0], rc.main + 1, rc.main[0]);
         op.pl[2] = C;
         op.pl[3] = AB;
       }
@@ -632,7 +632,7 @@ void assign_planes(Program& prog) {
       double d[3];
       for (int a = 0; a < 3; ++a) d[a] = K * cc.d0[a] + tri * cc.dd[a];
       bool conj = false;
-      op.pl[0] = plane(PL_PHASE, 0, cc.dt, cc.d0, cc.dt);
+      op.pl[0] = plane(PL_PHASE, PL_SAMPLE, cc.dt, cc.d0, cc.dt);
       op.pl[1] = gphase(cc.dd, conj);
       op.pl[2] = plane(PL_PHASE, 0, K * cc.dt, d, K * cc.dt);
       op.pl[3] = plane(PL_AB, 0, K * cc.dt, zero, 0.0);

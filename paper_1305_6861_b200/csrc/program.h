@@ -124,7 +124,9 @@ constexpr int kTrainRow = 12;  // doubles per (train class, spin)
 //   PL_PHASE: exp(-T/T2) exp(-i (pos . d + dw tw))  (x w, the single-coil receive weight, if PL_WEIGHT)
 //   PL_AB:    (exp(-T/T1), m0 (1 - exp(-T/T1)))
 enum : int32_t { PL_PHASE = 1, PL_AB = 2 };
-enum : int32_t { PL_WEIGHT = 1, PL_MUTABLE = 2 };
+// PL_SAMPLE: the plane only feeds fp32 ADC samples (a window's Cpre and z, a chirp's r0 and q); in
+// the fp32 mode it is stored as float2 (the kernel converts it to fp32 anyway): half the bytes.
+enum : int32_t { PL_WEIGHT = 1, PL_MUTABLE = 2, PL_SAMPLE = 4 };
 struct alignas(16) PlaneDesc {
   int32_t kind, flags;
   double T, d[3], tw;
