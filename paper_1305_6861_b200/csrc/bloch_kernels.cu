@@ -1269,14 +1269,15 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
                   phase_factor(th, zr0, zi0);
                   zr0 *= e.y;
                   zi0 *= e.y;
-                  pr = 1.0;
-                  pi = 0.0;
+                  // no pre-interval on the fly: the entry factor is the receive weight alone
+                  // (tabulated windows carry w in their Cpre plane)
+                  const double2 w0 = kp.w != nullptr ? __ldg(reinterpret_cast<const double2*>(kp.w) + i)
+                                                     : make_double2(1.0, 0.0);
+                  pr = w0.x;
+                  pi = w0.y;
                 }
-                double2 w0 = make_double2(1.0, 0.0);  // tabulated windows carry w in Cpre
-                if (kp.w != nullptr && !tb) w0 = __ldg(reinterpret_cast<const double2*>(kp.w) + i);
                 const double x = sp.mx(r), y = sp.my(r);
-                const double x0 = pr * x - pi * y, y0 = pr * y + pi * x;
-                u = cf{static_cast<float>(w0.x * x0 - w0.y * y0), static_cast<float>(w0.x * y0 + w0.y * x0)};
+                u = cf{static_cast<float>(pr * x - pi * y), static_cast<float>(pr * y + pi * x)};
                 z = cf{static_cast<float>(zr0), static_cast<float>(zi0)};
                 if (!lead) u = cmul(u, z);  // first sample after one interval
                 if (p0 > 0) {               // later pass: u z^p0
