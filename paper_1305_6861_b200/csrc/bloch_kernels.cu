@@ -120,8 +120,13 @@ struct Spins {
   int64_t base;  // spin index of slot 0 of this thread
   int bd;
   int64_t n;
+  int nact;      // active slots: idx(s) < n exactly for s < nact (idx grows with s)
   __device__ __forceinline__ int64_t idx(int s) const { return base + static_cast<int64_t>(s) * bd; }
-  __device__ __forceinline__ bool act(int s) const { return idx(s) < n; }
+  __device__ __forceinline__ bool act(int s) const { return s < nact; }
+  __device__ __forceinline__ void init_active() {
+    const int64_t left = n - base;
+    nact = left <= 0 ? 0 : static_cast<int>(left >= static_cast<int64_t>(S) * bd ? S : (left + bd - 1) / bd);
+  }
   __device__ __forceinline__ double& mx(int s) { return sm[(0 * S + s) * bd + threadIdx.x]; }
   __device__ __forceinline__ double& my(int s) { return sm[(1 * S + s) * bd + threadIdx.x]; }
   __device__ __forceinline__ double& mz(int s) { return sm[(2 * S + s) * bd + threadIdx.x]; }
@@ -779,6 +784,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
   sp.base = static_cast<int64_t>(blockIdx.x) * kp.spins_per_cta + threadIdx.x;
   sp.bd = bd;
   sp.n = kp.n;
+  sp.init_active();
   Strip<R> strip;  // one partial row per warp of the grid
   strip.lane = threadIdx.x & 31;
   strip.row = reinterpret_cast<R*>(kp.partial) +
