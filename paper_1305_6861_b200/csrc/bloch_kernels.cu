@@ -496,7 +496,7 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1
 // (the swizzle makes both the staging stores and the k-block loads
 // conflict-free), then z^64 per spin.
 constexpr int kStageFloat4 = 8 * 32;
-constexpr int kStageBytes = kStageFloat4 * 16 + 32 * 8 + 32 * 32;  // + cp.async slot (Cpre, z) per lane
+constexpr int kStageBytes = kStageFloat4 * 16 + 32 * 8 + 32 * 32;  // + z^64 per lane + cp.async slot (Cpre, z: 16 B used of 32)
 __device__ __forceinline__ int stage_idx(int g, int q) { return g * 32 + (q ^ ((g & 1) << 2)); }
 
 // One lane's spin into the stage: its 8 powers z^g and 8 values u z^(8g).

@@ -143,7 +143,6 @@ struct alignas(16) GEv {  // one generic sampled interval
 static_assert(sizeof(GEv) == 48, "GEv must be 48 bytes");
 
 constexpr int kChunkSlots = 8;   // ADC slots reduced per warp transpose (samples x coils)
-constexpr int kStripSlots = 256; // slots buffered per warp in shared memory before a CTA flush
 constexpr int kMinWindow = 4;    // shortest uniform run compiled as OP_WINDOW
 constexpr int kMinChirp = 3;     // shortest linear-increment run compiled as OP_CHIRP
 constexpr int kMinTrain = 4;     // shortest pulse+interval run compiled as OP_RFTRAIN
