@@ -41,7 +41,7 @@ from .errors import (
     WorkerPanic,
 )
 from .recon import ImageVolume, KSpaceMatrix, assemble_kspace, cpmg_fit, reconstruct
-from .phantom import Phantom, PhantomBox, SpinSample, rasterize, rasterize_arrays
+from .phantom import Phantom, PhantomBox, SpinSample, rasterize, rasterize_arrays, shepp_logan, shepp_logan_m0
 from .sequence import (
     AcquisitionSpec,
     ElementarySequence,

@@ -11,7 +11,8 @@ reference's list-of-``SpinSample`` return type.
 
 Box properties may be constants or callables ``f(x, y, z)``; callables are
 first tried on whole coordinate arrays and fall back to per-site evaluation.
-Out of scope: the object-file grammar and the Shepp-Logan table.
+The ten-ellipse head phantom (:func:`shepp_logan`, phantom.py:145-205) is
+here, vectorised.  Out of scope: the object-file grammar.
 """
 
 from __future__ import annotations
@@ -147,3 +148,63 @@ def rasterize(phantom: Phantom, spacing, cap: int = DEFAULT_SPIN_CAP) -> List[Sp
         )
         for p, m0, t1, t2, dw in zip(a["pos"], a["m0"], a["t1"], a["t2"], a["delta_omega"])
     ]
+
+
+# ---------------------------------------------------------------------------
+# ten-ellipse head phantom (phantom.py:145-205)
+# ---------------------------------------------------------------------------
+
+# The classic Shepp-Logan geometry in units of the half-width (centre x0, y0;
+# semi-axes a, b; rotation in degrees) with the reference's per-region
+# equilibrium magnetisation; later rows override earlier ones inside their
+# footprint (phantom.py:167-182).
+HEAD_ELLIPSES = np.array([
+    # x0,     y0,      a,      b,      phi,   m0
+    [0.0,     0.0,     0.69,   0.92,   0.0,   1.00],
+    [0.0,    -0.0184,  0.6624, 0.874,  0.0,   0.51],
+    [0.22,    0.0,     0.11,   0.31,  -18.0,  0.40],
+    [-0.22,   0.0,     0.16,   0.41,   18.0,  0.40],
+    [0.0,     0.35,    0.21,   0.25,   0.0,   0.60],
+    [0.0,     0.1,     0.046,  0.046,  0.0,   0.80],
+    [0.0,    -0.1,     0.046,  0.046,  0.0,   0.80],
+    [-0.08,  -0.605,   0.046,  0.023,  0.0,   0.70],
+    [0.0,    -0.605,   0.023,  0.023,  0.0,   0.70],
+    [0.06,   -0.605,   0.023,  0.046,  0.0,   0.70],
+])
+SHEPP_LOGAN_T1 = 1.0
+SHEPP_LOGAN_T2 = 0.2
+# cos/sin of each rotation from the math library, as the reference's scalar test evaluates them
+_HEAD_TRIG = [(math.cos(math.radians(p)), math.sin(math.radians(p))) for p in HEAD_ELLIPSES[:, 4]]
+
+
+def shepp_logan_m0(x, y, scale: float = 1.0):
+    """Equilibrium magnetisation of the head phantom at (x, y), 0 outside (phantom.py:185-191).
+
+    Accepts scalars or arrays; the membership test is the reference's expression
+    (phantom.py:158-164) evaluated elementwise in the same order, so the labels
+    agree bit for bit."""
+    xa = np.asarray(x, dtype=float) / scale
+    ya = np.asarray(y, dtype=float) / scale
+    value = np.zeros(np.broadcast(xa, ya).shape)
+    for (x0, y0, a, b, _phi, m0), (c, s) in zip(HEAD_ELLIPSES, _HEAD_TRIG):
+        dx, dy = xa - x0, ya - y0
+        u = (dx * c + dy * s) / a
+        v = (-dx * s + dy * c) / b
+        value = np.where(u * u + v * v <= 1.0, m0, value)
+    return float(value) if value.ndim == 0 else value
+
+
+def shepp_logan(scale: float, thickness: float = 1e-3) -> Phantom:
+    """Ten-ellipse head phantom scaled so the unit half-width maps to ``scale`` metres: one thin box
+    with an ellipse-membership M0 (phantom.py:194-205)."""
+    if scale <= 0.0:
+        raise InvalidParameter(f"scale must be positive, got {scale}")
+    box = PhantomBox(
+        origin=(-scale, -scale, -thickness / 2.0),
+        size=(2.0 * scale, 2.0 * scale, thickness),
+        m0=lambda x, y, z: shepp_logan_m0(x, y, scale),
+        t1=SHEPP_LOGAN_T1,
+        t2=SHEPP_LOGAN_T2,
+        delta_omega=0.0,
+    )
+    return Phantom([box])

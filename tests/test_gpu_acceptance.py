@@ -6,7 +6,9 @@
   dM/dt = gamma M x B - relaxation (the reference's ODE oracle, tests/oracles.py:42-67,
   restated here), rel error <= 1e-6;
 * criterion 4 (tests/test_acceptance.py:234-255): Hahn echo peak = M0 exp(-TE/T2) within 1e-4
-  through run(Experiment).
+  through run(Experiment);
+* criteria 6, 7, 9 and 2: the head-phantom image, the TSE ghost, CPMG T2 mapping and the k-t
+  engine agreement (see the tests below).
 """
 
 import math
@@ -219,3 +221,29 @@ def test_spin_engine_vs_kt_engine(precision, tol):
         kt = g[f"seq{i}_kt"]
         worst = max(worst, np.linalg.norm(spin - kt) / np.linalg.norm(spin))
     assert worst <= tol, f"worst rel L2 {worst:.2e}"
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+def test_head_phantom_image(precision):
+    """Criterion 6 (tests/test_acceptance.py:341-374): 64^2 spin echo of the ten-ellipse head phantom,
+    one spin per voxel slightly off the pixel raster, through run -> assembly -> GPU reconstruction:
+    Pearson r >= 0.95 against the phantom's M0 map, the edge overshoot (band-limitation ringing)
+    >= 5%, and ~2,120 spins."""
+    from paper_1305_6861_b200 import shepp_logan, shepp_logan_m0
+    from paper_1305_6861_b200.recon import assemble_kspace, reconstruct
+
+    fov, n, scale = 0.5, 64, 0.255
+    seq = build_spin_echo(fov=fov, n=n, te=0.05, tr=3.0, readout_grad=0.239e-3)
+    res = run(Experiment(sequence=seq, phantom=shepp_logan(scale), spacing=(fov / n * 0.999, fov / n * 0.999, 1.0),
+                         precision=precision))
+    k = assemble_kspace(res.echo_matrix(), seq.trajectory_table(), n_rows=n, fov=fov)[0]
+    img = reconstruct(k, device="cuda")
+    mag = img.magnitude
+    xs, ys = img.axis_coords(1), img.axis_coords(0)
+    ref = shepp_logan_m0(xs[None, :], ys[:, None], scale)
+    pearson = np.corrcoef(mag.ravel(), ref.ravel())[0, 1]
+    row = mag[n // 2]
+    overshoot = row[10:14].max() / np.median(row[13:19]) - 1.0
+    assert pearson >= 0.95, pearson
+    assert overshoot >= 0.05, overshoot
+    assert abs(res.spin_count - 2120) <= 0.10 * 2120, res.spin_count
