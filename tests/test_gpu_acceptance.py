@@ -247,3 +247,26 @@ def test_head_phantom_image(precision):
     assert pearson >= 0.95, pearson
     assert overshoot >= 0.05, overshoot
     assert abs(res.spin_count - 2120) <= 0.10 * 2120, res.spin_count
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+def test_parallel_determinism_and_compare_tool(precision):
+    """Criterion 10 (tests/test_acceptance.py:505-530): the result does not depend on workers, blocks
+    or the deterministic flag (the device fold is always in a fixed order: bit-identical, -inf dB),
+    and the comparison tool rates identity with zero exceedances and a 1e-6 scaling at -120 dB."""
+    from paper_1305_6861_b200 import compare_results, delta_e_stoer
+
+    grad = readout_gradient(0.25, 16, 0.008)
+    seq = build_spin_echo(fov=0.25, n=16, te=0.03, tr=1.0, readout_grad=grad)
+    ph = Phantom([_thin_box(-0.05, -0.04, 0.1, 0.08, m0=1.0, t1=1.0, t2=0.2)])
+    common = dict(sequence=seq, phantom=ph, spacing=(0.006, 0.006, 0.002), blocks=32, precision=precision)
+    ref = run(Experiment(workers=1, deterministic=True, **common))
+    det8 = run(Experiment(workers=8, deterministic=True, **common))
+    nondet = run(Experiment(workers=8, deterministic=False, **common))
+    assert np.array_equal(ref.echo_matrix(), det8.echo_matrix())
+    assert np.array_equal(ref.echo_matrix(), nondet.echo_matrix())
+    assert delta_e_stoer(ref.echo_matrix(), det8.echo_matrix()) <= -200.0
+    rng = np.random.default_rng(3)
+    probe = rng.normal(size=512) + 1j * rng.normal(size=512)
+    assert compare_results(probe, probe.copy()).exceedances == 0
+    assert abs(delta_e_stoer(probe, probe * (1.0 + 1e-6)) + 120.0) <= 0.5
