@@ -295,6 +295,9 @@ def _f64(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
+MAX_COILS = 8  # receive coils per device call (bloch_compute_block); more run as groups (BlochEngine.compute)
+
+
 class BlochEngine:
     """One libbloch_b200 context: a CUDA device, a state precision, the uploaded tables."""
 
@@ -403,7 +406,25 @@ class BlochEngine:
         """compute_block on host numpy arrays; returns (echoes, snapshots).
 
         ``out_echoes`` (complex128 (C, n_acq, max_ns)) and ``out_snaps`` (float64
-        (n_snap, n, 3)) may be preallocated (e.g. pinned) buffers."""
+        (n_snap, n, 3)) may be preallocated (e.g. pinned) buffers.  More than
+        ``MAX_COILS`` receive coils run as consecutive groups of coils (the spin
+        state is recomputed per group; the snapshots come from the first)."""
+        w = np.asarray(weight)
+        if w.ndim == 2 and w.shape[0] > MAX_COILS:
+            f = self.set_tables(tables)
+            eshape = (w.shape[0], f["n_acq"], f["max_ns"])
+            if out_echoes is None:
+                out_echoes = np.zeros(eshape, dtype=np.complex128)
+            elif out_echoes.shape != eshape or out_echoes.dtype != np.complex128:
+                raise InvalidParameter(f"out_echoes must be complex128 {eshape}")
+            snaps = None
+            for g0 in range(0, w.shape[0], MAX_COILS):
+                e, s = self._submit(tables, pos, mx, my, mz, t1, t2, m0, domega, w[g0:g0 + MAX_COILS], block_index,
+                                    None, out_snaps if g0 == 0 else None, sync=True).wait()
+                out_echoes[g0:g0 + MAX_COILS] = e
+                if g0 == 0:
+                    snaps = s
+            return out_echoes, snaps
         return self._submit(tables, pos, mx, my, mz, t1, t2, m0, domega, weight, block_index, out_echoes,
                             out_snaps, sync=True).wait()
 

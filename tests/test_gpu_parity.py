@@ -228,3 +228,28 @@ def test_pipeline_matches_synchronous_compute():
         e, s = p.wait()
         assert np.array_equal(e, ref_e) and np.array_equal(s[0], ref_s[0])
     pipe.close()
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+def test_more_coils_than_one_call_takes(precision):
+    """12 receive coils (> MAX_COILS = 8 per device call): BlochEngine.compute runs coil groups; every
+    coil's k-space matches the oracle (one weighted sum per coil, engine.py:303-305 per weight)."""
+    from oracle import bloch_oracle as O
+
+    rec = load_golden("mixed")
+    b = _block(rec)
+    rng = np.random.default_rng(12)
+    w = rng.uniform(0.3, 1.0, (12, b.n)) * np.exp(1j * rng.uniform(0, 2 * math.pi, (12, b.n)))
+    seq = _sequence_of("mixed")
+    snaps_t = tuple(rec["snapshot_times"].tolist())
+    t = precompute_sequence_tables(seq, snapshot_times=snaps_t)
+    e, s = compute_block(t, SpinBlock(index=0, pos=b.pos, mx=b.mx, my=b.my, mz=b.mz, t1=b.t1, t2=b.t2, m0=b.m0,
+                                      domega=b.domega, weight=w), precision=precision)
+    ot = O.precompute_tables(seq, snapshot_times=snaps_t)
+    ref_e, ref_s = O.compute_block(ot, b.pos, b.mx, b.my, b.mz, b.t1, b.t2, b.m0, b.domega, w)
+    assert e.shape == ref_e.shape == (12,) + ref_e.shape[1:]
+    for c in range(12):
+        assert rel_l2(ref_e[c], e[c]) <= KSPACE_TOL[precision], c
+    for a, r in zip(s, ref_s):
+        if r is not None:
+            assert rel_l2(r, a) <= STATE_TOL[precision]
