@@ -474,6 +474,11 @@ __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) 
 #endif
 }
 
+#ifndef BLOCH_KB_UNROLL
+#define BLOCH_KB_UNROLL 2
+#endif
+constexpr int kKbUnroll = BLOCH_KB_UNROLL;  // k-block loop unroll of the single-coil window rounds
+
 // {x, y} -> bf16x2 (x in the low half) by truncation: the high halves of the fp32 words
 __device__ __forceinline__ uint32_t pack_bf16(uint32_t x, uint32_t y) { return __byte_perm(x, y, 0x7632); }
 
@@ -521,7 +526,7 @@ template <int NT, int MT>
 __device__ __forceinline__ void mma_round_t(const float4* __restrict__ st, const float2* __restrict__ z64s, int lane,
                                             float (&acc)[MT][4]) {
   const int g = lane >> 2, t = lane & 3;
-#pragma unroll 2
+#pragma unroll kKbUnroll
   for (int kb = 0; kb < 8; ++kb) {
     const int q = 4 * kb + t;
     const float4 e = st[stage_idx(g, q)];
