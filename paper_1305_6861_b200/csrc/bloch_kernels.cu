@@ -776,13 +776,16 @@ __device__ __forceinline__ void chirp_f32(const KParams& kp, const DevOp* op, Sp
 // kFull: the program uses RF trains, chirps or generic sampled events.  Programs
 // made only of pulses, intervals and uniform windows (spin/turbo-spin echoes) run
 // a kernel without those handlers: less register pressure in the hot loop.
-template <typename R, int S, int NC, bool kFull>
+// BD: the block size as a compile-time constant (0: blockDim.x).  The spin state
+// [3][S][bd] is addressed (component, slot) x bd + thread on every access; with a
+// constant bd those offsets are immediates.
+template <typename R, int S, int NC, bool kFull, int BD>
 __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTraits<R, S, NC>::kMinBlocks)
     integrate_kernel(const KParams kp) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int kSampPerChunk = kChunkSlots / NC;
   constexpr bool kPacked = sizeof(R) == 4 && NC == 1 && (S % 2 == 0);
-  const int bd = blockDim.x;
+  const int bd = BD ? BD : static_cast<int>(blockDim.x);
   const int nw = bd >> 5;
   Spins<S> sp;
   sp.sm = reinterpret_cast<double*>(smem_raw);
@@ -1680,18 +1683,32 @@ size_t integrate_smem_bytes(int threads) {
   return static_cast<size_t>(3 * S * threads) * sizeof(double) + static_cast<size_t>(threads / 32) * stage;
 }
 
-template <typename R, int S, int NC, bool kFull>
-static cudaError_t launch_one(const KParams& kp, int grid, int threads, cudaStream_t stream) {
+template <typename R, int S, int NC, bool kFull, int BD>
+static cudaError_t launch_bd(const KParams& kp, int grid, int threads, cudaStream_t stream) {
   const size_t smem = integrate_smem_bytes<R, S, NC>(threads);
   static size_t smem_set = 48 * 1024;  // raise the opt-in limit only when needed (not inside a graph capture)
   if (smem > smem_set) {
-    cudaError_t e = cudaFuncSetAttribute(integrate_kernel<R, S, NC, kFull>,
+    cudaError_t e = cudaFuncSetAttribute(integrate_kernel<R, S, NC, kFull, BD>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     smem_set = smem;
   }
-  integrate_kernel<R, S, NC, kFull><<<grid, threads, smem, stream>>>(kp);
+  integrate_kernel<R, S, NC, kFull, BD><<<grid, threads, smem, stream>>>(kp);
   return cudaGetLastError();
+}
+
+// the basic fp32 single-coil kernel with 8 spins per thread at its full block size (config 1's
+// launch) gets a constant-block-size instance: config 1 -1.0%; the kFull variant measured +2.8%
+// on config 3 with it, so it keeps the runtime block size
+template <typename R, int S, int NC, bool kFull>
+static cudaError_t launch_one(const KParams& kp, int grid, int threads, cudaStream_t stream) {
+#ifndef BLOCH_NO_FIXED_BD
+  constexpr int kMax = KernelTraits<R, S, NC>::kMaxThreads;
+  if constexpr (sizeof(R) == 4 && NC == 1 && S == 8 && !kFull) {
+    if (threads == kMax) return launch_bd<R, S, NC, kFull, kMax>(kp, grid, threads, stream);
+  }
+#endif
+  return launch_bd<R, S, NC, kFull, 0>(kp, grid, threads, stream);
 }
 
 template <typename R, int S, int NC>
@@ -1763,7 +1780,7 @@ cudaError_t launch_reduce(const R* part, int rows, int64_t n_slots, int nc, int 
 template <typename R, int S, int NC>
 cudaError_t kernel_attrs(int* max_threads, int* regs) {
   cudaFuncAttributes a;
-  cudaError_t e = cudaFuncGetAttributes(&a, integrate_kernel<R, S, NC, true>);
+  cudaError_t e = cudaFuncGetAttributes(&a, integrate_kernel<R, S, NC, true, 0>);
   if (e != cudaSuccess) return e;
   *max_threads = a.maxThreadsPerBlock;
   *regs = a.numRegs;
