@@ -138,8 +138,10 @@ Variant pick_variant(int prec, int64_t n, int ncp, int n_sm, int max_window) {
     auto fits = [&](int s) { return n >= int64_t(n_sm) * 16 * 32 * s; };
     if (ncp == 1) {
       if (force_s == 2 || force_s == 4 || force_s == 8) return {32, force_s, 1};
-      // 512-sample windows run fastest with 4 spins per thread (config 2: 35.0 vs 38.1 ms)
-      if (fits(8) && max_window < 384) return {32, 8, 1};
+      // long windows no longer favour 4 spins per thread since the 2-unit window products
+      // (config 2, 512-sample windows: S=8 26.6 ms vs S=4 27.3; it was 35.0 vs 38.1 with 3 tf32 passes)
+      (void)max_window;
+      if (fits(8)) return {32, 8, 1};
       return {32, fits(4) ? 4 : 2, 1};
     }
     if (ncp == 8) {
