@@ -227,6 +227,12 @@ int bloch_last_timing(const bloch_ctx* ctx, float* kernel_ms, float* device_ms,
 int bloch_last_launch(const bloch_ctx* ctx, int32_t* prec, int32_t* spins_per_thread, int32_t* coils,
                       int32_t* grid, int32_t* threads);
 
+/* Program segments of the last call.  The integrator keeps one partial-sum row per warp and
+ * recorded sample; when that would exceed BLOCH_PARTIAL_BUDGET_MB (default 24 GiB) the op stream
+ * runs as several launches over contiguous op ranges, the fp64 state handed over through global
+ * memory and each range's samples folded before the next: the results are bit-identical. */
+int bloch_last_segments(const bloch_ctx* ctx, int32_t* segments);
+
 #ifdef __cplusplus
 }
 #endif

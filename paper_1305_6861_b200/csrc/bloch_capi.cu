@@ -88,6 +88,8 @@ struct bloch_ctx {
   float kernel_ms = 0.f, device_ms = 0.f;
   int launches = 0;
   int last_launch[5] = {0, 0, 0, 0, 0};  // prec, spins per thread, coils, grid, threads of the last integrator
+  int32_t last_segments = 0;               // program segments of the last call (bounded partial rows)
+  DevBuf state;                            // segment hand-over state, two (mx, my, mz) sets
   // CUDA graph of the device work of a device-resident call (prep, tables, integrator, fold),
   // captured on the second identical call and replayed while the arguments stay the same
   uint64_t prog_gen = 0;
@@ -122,6 +124,53 @@ struct Variant {
   int prec, S, NC;
   bool full = true;  // program uses RF trains / chirps / generic sampled events
 };
+
+// a contiguous op range and the contiguous compact samples it records
+struct Segment {
+  int32_t op_begin, op_end;
+  int64_t sample_begin, n_samples;
+};
+
+int64_t op_samples(const bloch::DevOp& op) {
+  switch (op.kind) {
+    case bloch::OP_WINDOW:
+    case bloch::OP_CHIRP:
+    case bloch::OP_GSAMP:
+      return op.count;
+    default:
+      return 0;
+  }
+}
+
+// Cut the program so that each segment's partial rows (bytes_per_sample per recorded sample) stay
+// within the budget: BLOCH_PARTIAL_BUDGET_MB, default 24 GiB.  Samples are contiguous in op order
+// (compact ids follow the walk), so a segment is an op range plus a sample range.  An op is never
+// split; one op larger than the budget gets a segment of its own.
+std::vector<Segment> plan_segments(const bloch::Program& P, int64_t bytes_per_sample) {
+  static const int64_t budget = [] {
+    const char* e = getenv("BLOCH_PARTIAL_BUDGET_MB");
+    const double mb = e ? atof(e) : 24.0 * 1024.0;
+    return std::max<int64_t>(1, static_cast<int64_t>(mb * 1048576.0));
+  }();
+  const int64_t cap = std::max<int64_t>(1, budget / std::max<int64_t>(1, bytes_per_sample));
+  std::vector<Segment> segs;
+  Segment cur{0, 0, 0, 0};
+  int64_t next_sample = 0;
+  for (int32_t o = 0; o < static_cast<int32_t>(P.ops.size()); ++o) {
+    const int64_t k = op_samples(P.ops[o]);
+    if (k > 0 && cur.n_samples > 0 && cur.n_samples + k > cap) {
+      cur.op_end = o;
+      segs.push_back(cur);
+      cur = Segment{o, o, next_sample, 0};
+    }
+    if (k > 0 && cur.n_samples == 0) cur.sample_begin = P.ops[o].s0;
+    cur.n_samples += k;
+    next_sample = cur.sample_begin + cur.n_samples;
+  }
+  cur.op_end = static_cast<int32_t>(P.ops.size());
+  segs.push_back(cur);
+  return segs;
+}
 
 // pick (S, NC) for a block of n spins with ncp (power-of-two) coils; max_window: the longest
 // uniform ADC window of the program (samples)
@@ -289,7 +338,7 @@ int bloch_destroy(bloch_ctx* c) {
   c->drop_graph();
   for (DevBuf* b : {&c->d_ops, &c->d_gev, &c->d_mats, &c->d_sample_g, &c->d_relax_t, &c->relax, &c->d_planes, &c->planetab, &c->planetab32, &c->in_pos, &c->in_mx, &c->in_my, &c->in_mz,
                     &c->in_t1, &c->in_t2, &c->in_m0, &c->in_dw, &c->in_w, &c->sc, &c->wpad, &c->w32, &c->partial,
-                    &c->echo, &c->snaps, &c->d_train_cls, &c->traintab,
+                    &c->echo, &c->snaps, &c->d_train_cls, &c->traintab, &c->state,
                     &c->raster_scratch})
     b->release();
   for (auto& ev : c->ev)
@@ -563,10 +612,20 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       c->last_launch[2] = v.NC;
       c->last_launch[3] = static_cast<int>(grid);
       c->last_launch[4] = static_cast<int>(threads);
-      const int64_t n_slots = P.n_samples * ncp;
       const size_t rsz = v.prec == 32 ? sizeof(float) : sizeof(double);
       const int64_t rows = grid * (threads / 32);  // one partial row per warp
-      c->partial.ensure(static_cast<size_t>(std::max<int64_t>(1, rows * n_slots * 2)) * rsz);
+      // Program segments: the partial rows hold one slot per (warp, sample, coil), so a long
+      // acquisition on a large block can exceed the device.  The op stream is cut into segments
+      // whose samples fit the budget; each runs as its own launch (state handed over in fp64
+      // through global memory, bit-identical to one launch) followed by the fold of its samples.
+      const std::vector<Segment> segs = plan_segments(P, rows * ncp * 2 * static_cast<int64_t>(rsz));
+      int64_t max_seg_slots = 1;
+      for (const Segment& g : segs) max_seg_slots = std::max<int64_t>(max_seg_slots, g.n_samples * ncp);
+      c->partial.ensure(static_cast<size_t>(rows * max_seg_slots * 2) * rsz);
+      c->last_segments = static_cast<int32_t>(segs.size());
+      if (segs.size() > 1) {
+        c->state.ensure(static_cast<size_t>(6) * nd);  // two ping-pong (mx, my, mz) sets
+      }
       bloch::KParams kp{};
       kp.ops = c->d_ops.as<bloch::DevOp>();
       kp.n_ops = static_cast<int32_t>(P.ops.size());
@@ -581,7 +640,6 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       kp.w = d_w;
       kp.w32 = (d_w && ncp >= 2 && c->precision == BLOCH_PREC_F32) ? c->w32.as<float2>() : nullptr;
       kp.partial = c->partial.p;
-      kp.part_stride = n_slots * 2;
       kp.snaps = d_snap;
       kp.relax = c->relax.as<double>();
       kp.planes = c->planetab.as<double2>();
@@ -589,20 +647,40 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       kp.train = c->traintab.as<double>();
       if (c->gate_wait) ck(cudaStreamWaitEvent(st, c->gate_wait, 0), "gate wait");
       ck(cudaEventRecordWithFlags(c->ev[1], st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault), "event");
-      ck(dispatch(v, kp, static_cast<int>(grid), static_cast<int>(threads), st), "integrate kernel");
-      if (c->gate_signal) ck(cudaEventRecord(c->gate_signal, st), "gate signal");
-      ck(cudaEventRecordWithFlags(c->ev[2], st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault), "event");
-      c->launches++;
-      if (n_slots > 0) {
-        if (v.prec == 32)
-          ck(bloch::launch_reduce<float>(c->partial.as<float>(), static_cast<int>(rows), n_slots,
-                                         n_coils, ncp, c->d_sample_g.as<int64_t>(), G, d_echo, st),
-             "reduce kernel");
-        else
-          ck(bloch::launch_reduce<double>(c->partial.as<double>(), static_cast<int>(rows), n_slots,
-                                          n_coils, ncp, c->d_sample_g.as<int64_t>(), G, d_echo, st),
-             "reduce kernel");
+      double* state = c->state.as<double>();
+      for (size_t k = 0; k < segs.size(); ++k) {
+        const Segment& g = segs[k];
+        const int64_t seg_slots = g.n_samples * ncp;
+        kp.op_begin = g.op_begin;
+        kp.n_ops = g.op_end;
+        kp.sample_base = static_cast<int32_t>(g.sample_begin);
+        kp.part_stride = seg_slots * 2;
+        kp.mx0 = k == 0 ? d_mx : state + ((k - 1) & 1) * 3 * n;
+        kp.my0 = k == 0 ? d_my : state + ((k - 1) & 1) * 3 * n + n;
+        kp.mz0 = k == 0 ? d_mz : state + ((k - 1) & 1) * 3 * n + 2 * n;
+        const bool hand_over = k + 1 < segs.size();
+        kp.mx1 = hand_over ? state + (k & 1) * 3 * n : nullptr;
+        kp.my1 = hand_over ? state + (k & 1) * 3 * n + n : nullptr;
+        kp.mz1 = hand_over ? state + (k & 1) * 3 * n + 2 * n : nullptr;
+        ck(dispatch(v, kp, static_cast<int>(grid), static_cast<int>(threads), st), "integrate kernel");
         c->launches++;
+        if (!hand_over) {  // after the last integrator launch (the fold of its samples follows)
+          if (c->gate_signal) ck(cudaEventRecord(c->gate_signal, st), "gate signal");
+          ck(cudaEventRecordWithFlags(c->ev[2], st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault),
+             "event");
+        }
+        if (seg_slots > 0) {
+          const int64_t* sg = c->d_sample_g.as<int64_t>() + g.sample_begin;
+          if (v.prec == 32)
+            ck(bloch::launch_reduce<float>(c->partial.as<float>(), static_cast<int>(rows), seg_slots, n_coils, ncp,
+                                           sg, G, d_echo, st),
+               "reduce kernel");
+          else
+            ck(bloch::launch_reduce<double>(c->partial.as<double>(), static_cast<int>(rows), seg_slots, n_coils,
+                                            ncp, sg, G, d_echo, st),
+               "reduce kernel");
+          c->launches++;
+        }
       }
     } else {
       ck(cudaEventRecordWithFlags(c->ev[1], st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault), "event");
@@ -758,6 +836,12 @@ int bloch_last_launch(const bloch_ctx* c, int32_t* prec, int32_t* spins_per_thre
   int32_t* out[5] = {prec, spins_per_thread, coils, grid, threads};
   for (int i = 0; i < 5; ++i)
     if (out[i]) *out[i] = c->last_launch[i];
+  return BLOCH_OK;
+}
+
+int bloch_last_segments(const bloch_ctx* c, int32_t* segments) {
+  if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
+  if (segments) *segments = c->last_segments;
   return BLOCH_OK;
 }
 

@@ -807,7 +807,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
     sp.mz(s) = a ? kp.mz0[i] : 0.0;
   }
 
-  for (int o = 0; o < kp.n_ops; ++o) {
+  for (int o = kp.op_begin; o < kp.n_ops; ++o) {
     const DevOp* op = kp.ops + o;
     const int kind = __ldg(&op->kind);
 
@@ -1009,7 +1009,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
     }
 
     if (kind == OP_GSAMP) {  // generic sampled intervals
-      const int cnt = __ldg(&op->count), g0 = __ldg(&op->aux), s0 = __ldg(&op->s0);
+      const int cnt = __ldg(&op->count), g0 = __ldg(&op->aux), s0 = __ldg(&op->s0) - kp.sample_base;
       for (int k0 = 0; k0 < cnt; k0 += kSampPerChunk) {
         const int ck = min(kSampPerChunk, cnt - k0);
         R ar[kChunkSlots], ai[kChunkSlots];
@@ -1035,7 +1035,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
     if (kind == OP_CHIRP) {  // linear-increment sampled run: geometric rotation factors, fp64
       // Spin-outer over blocks of two chunks: each spin's chirp-class row (or its
       // SpinConst) is read once per block, not once per 8-sample chunk.
-      const int cnt = __ldg(&op->count), s0 = __ldg(&op->s0), cls = __ldg(&op->cls), crc = __ldg(&op->rot);
+      const int cnt = __ldg(&op->count), s0 = __ldg(&op->s0) - kp.sample_base, cls = __ldg(&op->cls), crc = __ldg(&op->rot);
       const double dt = __ldg(&op->p[0]);
       const double d0x = __ldg(&op->p[1]), d0y = __ldg(&op->p[2]), d0z = __ldg(&op->p[3]);
       const double ddx = __ldg(&op->p[4]), ddy = __ldg(&op->p[5]), ddz = __ldg(&op->p[6]);
@@ -1132,7 +1132,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
 
     // OP_WINDOW
     {
-      const int cnt = __ldg(&op->count), lead = __ldg(&op->aux), s0 = __ldg(&op->s0), rc = __ldg(&op->rot),
+      const int cnt = __ldg(&op->count), lead = __ldg(&op->aux), s0 = __ldg(&op->s0) - kp.sample_base, rc = __ldg(&op->rot),
                 pre = __ldg(&op->pre);
       if constexpr (!kFull) {
         if (pre >= 0) apply_pre<S>(kp, sp, pre, __ldg(&op->tmode));
@@ -1504,6 +1504,16 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
           strip.push(ar, ai, ck * NC, (s0 + k0) * NC);
         }
       }
+    }
+  }
+  if (kp.mx1 != nullptr) {  // a segmented program: the state travels to the next segment's launch
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      if (!sp.act(s)) continue;
+      const int64_t i = sp.idx(s);
+      kp.mx1[i] = sp.mx(s);
+      kp.my1[i] = sp.my(s);
+      kp.mz1[i] = sp.mz(s);
     }
   }
 }

@@ -22,7 +22,10 @@ struct KParams {
   const double* mats;            // OP_RFTRAIN matrices, 9 per pair
   int64_t n;                     // spins
   const SpinConst* sc;           // [n]
-  const double *mx0, *my0, *mz0; // initial state (SpinBlock.mx/my/mz)
+  const double *mx0, *my0, *mz0; // initial state (SpinBlock.mx/my/mz, or the previous segment's state)
+  double *mx1, *my1, *mz1;       // state at the end of this launch's op range, or nullptr
+  int32_t op_begin;              // this launch runs ops [op_begin, n_ops): a program segment
+  int32_t sample_base;           // compact index of the segment's first sample (partial rows start there)
   const double* w;               // [NC][n][2] complex weights, or nullptr = 1+0j
   void* partial;                 // [warps of the grid][part_stride] of R
   int64_t part_stride;           // n_samples * NC * 2

@@ -373,6 +373,13 @@ class BlochEngine:
         _capi.check(self._lib.bloch_last_launch(self._h, *[ctypes.byref(x) for x in v]), "bloch_last_launch")
         return dict(zip(("precision", "spins_per_thread", "coils", "grid", "threads"), (x.value for x in v)))
 
+    def last_segments(self) -> int:
+        """Program segments of the last call (bloch_last_segments): 1 unless the partial rows of one
+        launch would exceed BLOCH_PARTIAL_BUDGET_MB."""
+        v = ctypes.c_int32()
+        _capi.check(self._lib.bloch_last_segments(self._h, ctypes.byref(v)), "bloch_last_segments")
+        return v.value
+
     def set_stream(self, stream_ptr: int) -> None:
         """Run on an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream); 0 = own stream."""
         _capi.check(self._lib.bloch_set_stream(self._h, ctypes.c_void_p(int(stream_ptr) or None)), "bloch_set_stream")
