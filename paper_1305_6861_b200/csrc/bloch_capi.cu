@@ -186,12 +186,15 @@ Variant pick_variant(int prec, int64_t n, int ncp, int n_sm, int max_window) {
     // S=2 3.63; the full config 1 (697k) S=8 10.25 vs S=4 10.90
     auto fits = [&](int s) { return n >= int64_t(n_sm) * 16 * 32 * s; };
     if (ncp == 1) {
-      if (force_s == 2 || force_s == 4 || force_s == 8) return {32, force_s, 1};
+      if (force_s == 1 || force_s == 2 || force_s == 4 || force_s == 8) return {32, force_s, 1};
       // long windows no longer favour 4 spins per thread since the 2-unit window products
       // (config 2, 512-sample windows: S=8 26.6 ms vs S=4 27.3; it was 35.0 vs 38.1 with 3 tf32 passes)
       (void)max_window;
       if (fits(8)) return {32, 8, 1};
-      return {32, fits(4) ? 4 : 2, 1};
+      // below one wave of 4-spin threads, one spin per thread (more warps, more waves) wins every
+      // measured shard: config 1 / 4 2.72 vs 2.91 ms (S=2), / 8 1.35 vs 1.42, / 16 0.94 vs 1.16;
+      // config 2 / 8 4.37 vs 5.00; config 0 (2,444 spins) 0.17 vs 0.22
+      return {32, fits(4) ? 4 : 1, 1};
     }
     if (ncp == 8) {
       // eight coils carry 4x the accumulators per spin, so fewer warps already saturate: measured

@@ -784,7 +784,8 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
     integrate_kernel(const KParams kp) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int kSampPerChunk = kChunkSlots / NC;
-  constexpr bool kPacked = sizeof(R) == 4 && NC == 1 && (S % 2 == 0);
+  constexpr bool kPacked = sizeof(R) == 4 && NC == 1 && (S % 2 == 0);  // FFMA2 recurrence over spin pairs
+  constexpr bool kMma1 = sizeof(R) == 4 && NC == 1;                     // single-coil tensor-core windows
   const int bd = BD ? BD : static_cast<int>(blockDim.x);
   const int nw = bd >> 5;
   Spins<S> sp;
@@ -1237,7 +1238,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
           continue;
         }
       }
-      if constexpr (kPacked) {
+      if constexpr (kMma1) {
         if (cnt >= kMmaMinWindow) {  // tensor-core window (see the notes above stage_spin)
           char* stb = reinterpret_cast<char*>(smem_raw) + static_cast<size_t>(3 * S) * bd * sizeof(double) +
                       static_cast<size_t>(threadIdx.x >> 5) * kStageBytes;
@@ -1685,10 +1686,9 @@ __global__ void reduce_partials_kernel(const R* __restrict__ part, int rows, int
 
 template <typename R, int S, int NC>
 size_t integrate_smem_bytes(int threads) {
-  constexpr bool kPacked = sizeof(R) == 4 && NC == 1 && (S % 2 == 0);
   // fp64 spin state [3][S][threads] + (fp32 single-coil) the tensor-core window stage, 16 B per spin
   size_t stage = 0;
-  if constexpr (kPacked) stage = kStageBytes;
+  if constexpr (sizeof(R) == 4 && NC == 1) stage = kStageBytes;
   if constexpr (sizeof(R) == 4 && NC >= 2) stage = McStage<NC>::kBytes;
   return static_cast<size_t>(3 * S * threads) * sizeof(double) + static_cast<size_t>(threads / 32) * stage;
 }

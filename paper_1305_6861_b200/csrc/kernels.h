@@ -56,6 +56,7 @@ struct KernelTraits<float, 8, 1> {  // the fp32 single-coil workhorse: 2 CTAs x 
   X(float, 8, 1)                  \
   X(float, 4, 1)                  \
   X(float, 2, 1)                  \
+  X(float, 1, 1)                  \
   X(float, 4, 2)                  \
   X(float, 4, 4)                  \
   X(float, 4, 8)                  \
@@ -69,6 +70,12 @@ struct KernelTraits<float, 8, 1> {  // the fp32 single-coil workhorse: 2 CTAs x 
 template <>
 struct KernelTraits<float, 4, 1> {  // long windows (>= 384 samples): 2 CTAs x 12 warps, 4 spins per thread
   static constexpr int kMaxThreads = 384;
+  static constexpr int kMinBlocks = 2;
+};
+
+template <>
+struct KernelTraits<float, 1, 1> {  // small blocks (spin shards): one spin per thread, 2 CTAs x 10 warps
+  static constexpr int kMaxThreads = 320;
   static constexpr int kMinBlocks = 2;
 };
 
