@@ -199,7 +199,10 @@ Variant pick_variant(int prec, int64_t n, int ncp, int n_sm, int max_window) {
     if (ncp == 8) {
       // eight coils carry 4x the accumulators per spin, so fewer warps already saturate: measured
       // config 4 (274k) S=4 63.7 vs S=2 71.3 ms; config 4 / 2 S=4 42.2 vs S=2 37.0; / 8 33.1 vs 20.6
-      if (force_s == 2 || force_s == 4) return {32, force_s, 8};
+      if (force_s == 1 || force_s == 2 || force_s == 4) return {32, force_s, 8};
+      // and very small eight-coil shards one spin per thread: config 4 / 8 (34k) 7.42 vs 8.26 ms (S=2),
+      // but / 4 (69k) 12.66 vs 12.13
+      if (n < int64_t(n_sm) * 10 * 32) return {32, 1, 8};
       return {32, n >= int64_t(n_sm) * 8 * 32 * 4 ? 4 : 2, 8};
     }
     return {32, 4, ncp};

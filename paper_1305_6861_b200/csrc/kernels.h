@@ -61,6 +61,7 @@ struct KernelTraits<float, 8, 1> {  // the fp32 single-coil workhorse: 2 CTAs x 
   X(float, 4, 4)                  \
   X(float, 4, 8)                  \
   X(float, 2, 8)                  \
+  X(float, 1, 8)                  \
   X(double, 4, 1)                 \
   X(double, 1, 1)                 \
   X(double, 2, 2)                 \
@@ -75,6 +76,12 @@ struct KernelTraits<float, 4, 1> {  // long windows (>= 384 samples): 2 CTAs x 1
 
 template <>
 struct KernelTraits<float, 1, 1> {  // small blocks (spin shards): one spin per thread, 2 CTAs x 10 warps
+  static constexpr int kMaxThreads = 320;
+  static constexpr int kMinBlocks = 2;
+};
+
+template <>
+struct KernelTraits<float, 1, 8> {  // small eight-coil blocks: one spin per thread
   static constexpr int kMaxThreads = 320;
   static constexpr int kMinBlocks = 2;
 };
