@@ -1,38 +1,51 @@
 #!/usr/bin/env python
 """bench.py — isochromat-event updates/s of the sm_100a Bloch engine (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
-    torchrun --nproc-per-node N bench.py --gpus N ...   (one process per GPU, NCCL)
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--scaling strong|weak]
+                    [--impl ours|reference] [--full-lattice]
+
+One process per GPU.  ``--gpus N > 1`` without a torchrun environment re-launches
+itself under ``python -m torch.distributed.run --nproc-per-node N`` (127.0.0.1);
+under torchrun (WORLD_SIZE set) it must equal the world size.
 
 A step is one pass of the hot path over the workload: every spin of config C
-(default 1 — "2D spin echo at scale", the configuration BASELINE.json's metric
-is quoted on) through the whole event stream, plus the fp64 fold of the
-partial k-space (and, for N > 1, the one NCCL reduce to rank 0).
+(default 2, "2D turbo spin echo" — the largest configuration by work, 1.98e11
+isochromat-event updates) through the whole event stream, the reduction of the
+ADC sums to the k-space and, for N > 1, the one NCCL reduce to rank 0.  The
+default is STRONG scaling: the config's own spins are sharded over the ranks
+with the reference's np.linspace bounds (partition_blocks, engine.py:229-251).
 
-* ``value``: N_spins * E / T with inputs resident in HBM, T = device time of
-  the K timed steps (CUDA events on the launching stream, L2 flushed between
-  steps by writing 256 MiB, max over ranks).  E is the reference table size
-  (pulses + events).
-* ``e2e``: the same metric through the public host API
-  (``BlochEngine.compute`` -> C-ABI ``bloch_compute_block`` with pinned host
-  buffers): every step copies the spin arrays host->device and the k-space and
-  final magnetisation device->host.  This is the headline against the
-  reference arm.
-* ``roofline``: FP32/MUFU model of SURVEY §8d (the path is not a dense
-  contraction): achieved = model ops / integrator-kernel time, peak = SMs x
-  128 FP32 lanes x f_max; ``frac`` = roofline time / measured kernel time.
-* ``cpu_baseline``: the oracle port of the reference's ``compute_block`` on
-  every host core (rank 0, N = 1), a bounded spin sample through the full
-  event stream.
-* ``--impl reference``: that CPU path alone, as the reference arm.
+* ``value``: N_spins * E / T with inputs resident in HBM, T = device time of the
+  K timed steps (CUDA events on the launching stream, L2 flushed between steps
+  by writing 256 MiB, max over ranks).  E is the reference table size (pulses +
+  events).
+* ``e2e``: the same metric through the public host API (BlochEngine / Pipeline
+  -> C-ABI bloch_compute_block, pinned host buffers): every step copies the
+  spin arrays host->device and the k-space and final magnetisation
+  device->host.  This is the headline against the reference arm.
+* ``roofline``: the integrator against the tensor pipe it runs on (mma.sync:
+  per spin-sample-coil one tf32 m16n8k8 pass + one bf16 m16n8k16 pass = 8
+  tf32-rate MAC, peak 512 MAC/clk/SM measured, profiles/r1_mma_microbench.txt),
+  plus the issue-slot floor from the committed ncu counters of this build
+  (profiles/ncu_counters.json) and the SURVEY §8d FP32/MUFU model as
+  ``model_frac`` (a model of the reference's per-event arithmetic, which the
+  closed-form windows do not execute, so it exceeds 1).
+* ``per_config``: value / kernel ms / fracs of configs 0-4 (device-resident,
+  same world and sharding) — the other configurations on the same box.
+* ``strong_scaling_projection`` (N = 1): device time of the 1/2, 1/4, 1/8
+  shards on this GPU, i.e. the per-rank work of a strong-scaled run.
+* ``cpu_baseline`` / ``--impl reference``: the reference's compute_block on
+  every host core — the unmodified reference from baseline/_ref through its own
+  _run_pool when it is installed (single-coil configs), else the oracle port —
+  on a bounded spin sample through the full event stream.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -44,23 +57,33 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
+METRIC = "isochromat-event updates/s"
+L2_NOTE = "flushed between timed steps (256 MiB write)"
+MMA_MAC_PER_CLK_SM = 512  # mma.sync m16n8k8 tf32, measured (profiles/r1_mma_microbench.txt)
 
-def parse_args():
+
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
-                    help="N > 1: weak = every rank integrates a full config-sized spin set (world interleaved "
-                         "copies of the lattice, parallel.weak_copy); strong = the config's spins sharded")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="N > 1: strong = the config's spins sharded over the ranks (default); weak = every rank "
+                         "integrates a full config-sized spin set (world interleaved copies of the lattice)")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--precision", type=int, default=32, choices=[32, 64])
+    ap.add_argument("--full-lattice", action="store_true",
+                    help="background tissue on every lattice site: all 1,048,576 sites of configs 1-4 emit a spin")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-per-config", action="store_true")
+    ap.add_argument("--no-projection", action="store_true")
     ap.add_argument("--cpu-spins-per-core", type=int, default=2048)
+    ap.add_argument("--dry", action="store_true",
+                    help="plumbing check without a GPU: gloo ranks, shards, one reduce, max-over-ranks timing")
     ap.add_argument("--quiet", action="store_true")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def log(msg, quiet=False):
@@ -133,14 +156,48 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# the CPU reference path (oracle port of compute_block, all host cores)
+# workload description shared by both arms (identical `config` objects)
 # ---------------------------------------------------------------------------
 
 
-def cpu_sample(workload, tables, E, spins_per_core, steps=1, warmup=0, quiet=False):
-    """Time the oracle port of the reference's compute_block on a spin sample (bounded CPU work)."""
-    from oracle import cpu_pool
+def make_workload(args):
+    from paper_1305_6861_b200 import configs
 
+    return configs.make(args.config, full_lattice=args.full_lattice)
+
+
+def config_dict(w, world, E, counts, scaling, full_lattice):
+    return {"workload": w.name, "config_index": w.index, "spins_total": w.n_spins, "events_per_spin": E,
+            "coils": w.n_coils, "event_classes": counts, "full_lattice": bool(full_lattice),
+            "sharding": ("single GPU" if world == 1 else
+                         "strong: np.linspace spin shards of the config (partition_blocks, engine.py:229-251), one "
+                         "NCCL reduce of the fp64 k-space" if scaling == "strong" else
+                         "weak: every rank a full config-sized spin set (world interleaved lattice copies, "
+                         "parallel.weak_copy), one NCCL reduce of the fp64 k-space"),
+            "l2": L2_NOTE, "parallelism": f"spin-shards x{world}"}
+
+
+# ---------------------------------------------------------------------------
+# the CPU reference path (all host cores)
+# ---------------------------------------------------------------------------
+
+
+def _reference_engine():
+    """The unmodified reference (baseline/_ref, installed by tools/install_reference.sh), or None."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "mrsim")):
+        return None
+    if path not in sys.path:
+        sys.path.append(path)
+    try:
+        import mrsim.engine as ref_engine  # noqa: F401
+    except Exception:
+        return None
+    return ref_engine
+
+
+def cpu_sample(workload, E, spins_per_core, steps=1, warmup=0, quiet=False):
+    """Time the reference's compute_block on a bounded spin sample with every host core."""
     cores = os.cpu_count() or 1
     n_sample = min(workload.n_spins, cores * spins_per_core)
     stride = max(1, workload.n_spins // n_sample)
@@ -149,176 +206,384 @@ def cpu_sample(workload, tables, E, spins_per_core, steps=1, warmup=0, quiet=Fal
     arrays = dict(pos=sub.pos[idx], mx=sub.mx[idx], my=sub.my[idx], mz=sub.mz[idx], t1=sub.t1[idx], t2=sub.t2[idx],
                   m0=sub.m0[idx], domega=sub.domega[idx], weight=np.asarray(sub.weight)[..., idx])
     n = int(arrays["mx"].size)
+    ref = _reference_engine() if workload.n_coils == 1 else None
+    for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ.setdefault(k, "1")
+    if ref is not None:
+        # the reference itself: its precompute, SpinBlock, partition_blocks and process pool (engine.py:540-595)
+        from types import SimpleNamespace
+
+        tables = ref.precompute_sequence_tables(workload.sequence)
+        block = ref.SpinBlock(index=0, pos=np.ascontiguousarray(arrays["pos"]), mx=arrays["mx"].copy(),
+                              my=arrays["my"].copy(), mz=arrays["mz"].copy(), t1=arrays["t1"].copy(),
+                              t2=arrays["t2"].copy(), m0=arrays["m0"].copy(), domega=arrays["domega"].copy(),
+                              weight=np.asarray(arrays["weight"], dtype=np.complex128).reshape(-1).copy())
+        exp = SimpleNamespace(workers=cores, deterministic=True)
+
+        def one():
+            try:
+                from threadpoolctl import threadpool_limits
+
+                lim = threadpool_limits(1)
+            except Exception:
+                lim = None
+            t0 = time.perf_counter()
+            blocks = ref.partition_blocks(block, 4 * cores)
+            ref._run_pool(exp, tables, blocks, {})
+            wall = time.perf_counter() - t0
+            if lim is not None:
+                lim.restore_original_limits()
+            return wall
+
+        kind, what = "reference", (f"mrsim.engine._run_pool (baseline/_ref, unmodified) with {cores} workers, "
+                                   f"4 blocks/worker, deterministic, 1 BLAS thread each")
+    else:
+        from oracle import cpu_pool
+        from oracle.bloch_oracle import precompute_tables
+
+        tables = precompute_tables(workload.sequence)
+
+        def one():
+            return cpu_pool.run_pool(tables, arrays, workers=cores)[2]
+
+        kind, what = "port", (f"oracle/bloch_oracle.compute_block on a {cores}-process pool (engine._run_pool "
+                              f"restated, 4 blocks/worker, 1 BLAS thread each)")
     walls = []
     for i in range(warmup + steps):
-        _, _, wall = cpu_pool.run_pool(tables, arrays, workers=cores)
-        log(f"[cpu] step {i}: {n} spins x {E} events in {wall:.2f}s", quiet)
+        wall = one()
+        log(f"[cpu] step {i}: {n} spins x {E} events in {wall:.2f}s ({kind})", quiet)
         if i >= warmup:
             walls.append(wall)
     mean = sum(walls) / len(walls)
-    return {
-        "value": n * E / mean,
-        "unit": "isochromat-event updates/s",
-        "cores": cores,
-        "kind": "port",
-        "sample": f"{n} spins (every {stride}th in rasterisation order) x {E} events of config "
-                  f"{workload.index}, oracle/bloch_oracle.compute_block on a {cores}-process pool "
-                  f"(engine._run_pool restated, 4 blocks/worker, 1 BLAS thread each), mean of {len(walls)}",
-        "seconds_per_step": mean,
+    return {"value": n * E / mean, "unit": METRIC, "cores": cores, "kind": kind,
+            "sample": f"{n} spins (every {stride}th in rasterisation order) x {E} events of config {workload.index}, "
+                      f"{what}, mean of {len(walls)}",
+            "seconds_per_step": mean}
+
+
+def reference_arm(args):
+    from paper_1305_6861_b200.engine import event_counts, precompute_sequence_tables
+
+    w = make_workload(args)
+    counts = event_counts(precompute_sequence_tables(w.sequence))
+    E = counts["events"]
+    cb = cpu_sample(w, E, args.cpu_spins_per_core, steps=args.steps, warmup=args.warmup, quiet=args.quiet)
+    line = {
+        "metric": METRIC, "value": cb["value"], "unit": METRIC, "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["seconds_per_step"] * 1e3,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE.json config recipe)",
+        "config": config_dict(w, args.gpus, E, counts, args.scaling, args.full_lattice),
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": cb["value"], "unit": METRIC, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    print(json.dumps(line), flush=True)
+    return 0
 
 
 # ---------------------------------------------------------------------------
+# one process per GPU: spawn / plumbing check
+# ---------------------------------------------------------------------------
 
 
-def main():
-    args = parse_args()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+def _free_port():
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn(args_argv, n):
+    """Re-launch this script with n ranks under torch.distributed.run; rank 0 prints the line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__), *args_argv]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
+
+
+def dry_run(args, world, rank):
+    """The multi-rank plumbing without a GPU: shards, one gloo reduce, max-over-ranks time, the JSON line."""
+    import torch
+    import torch.distributed as dist
 
     from paper_1305_6861_b200 import configs
     from paper_1305_6861_b200.engine import event_counts, precompute_sequence_tables
+    from paper_1305_6861_b200.parallel import reduce_kspace, shard_block
 
-    metric = "isochromat-event updates/s"
+    if world > 1:
+        dist.init_process_group("gloo")
+    w = configs.make(args.config, full_lattice=args.full_lattice)
+    counts = event_counts(precompute_sequence_tables(w.sequence))
+    E = counts["events"]
+    shard = shard_block(w.block, world, rank) if args.scaling == "strong" else w.block
+    k = torch.zeros(4, dtype=torch.float64)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        k.fill_(float(shard.n))
+        reduce_kspace(k, dst=0)
+    t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    n_total = w.n_spins if args.scaling == "strong" else world * w.n_spins
+    if rank == 0:
+        assert args.scaling != "strong" or int(k[0].item()) == w.n_spins, "shards do not cover the config"
+        print(json.dumps({"metric": METRIC, "value": n_total * E * args.steps / max(t.item(), 1e-9), "unit": METRIC,
+                          "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "dry": True,
+                          "scaling": args.scaling, "spins_reduced": int(k[0].item()),
+                          "config": config_dict(w, world, E, counts, args.scaling, args.full_lattice)}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
 
+
+# ---------------------------------------------------------------------------
+# GPU measurement
+# ---------------------------------------------------------------------------
+
+
+def _peaks():
+    f_max, hbm = 1965.0, None
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            mp = json.load(fh)
+        f_max = float(mp.get("sm_max_mhz", f_max))
+        hbm = float(mp.get("hbm_gbs")) if mp.get("hbm_gbs") else None
+    except Exception:
+        pass
+    return f_max, hbm
+
+
+def _lib_sha():
+    import hashlib
+
+    from paper_1305_6861_b200 import _capi
+
+    path = os.environ.get("BLOCH_LIB") or _capi.LIB_PATH
+    try:
+        with open(path, "rb") as fh:
+            return hashlib.sha256(fh.read()).hexdigest()[:16]
+    except OSError:
+        return None
+
+
+def _ncu_counters(config_index, lib_sha):
+    """Per-launch ncu counters of the integrator for this build (profiles/ncu_counters.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_counters.json")) as fh:
+            d = json.load(fh)
+    except Exception:
+        return None
+    rec = d.get(f"config{config_index}")
+    if not rec or (lib_sha and rec.get("lib_sha16") not in (None, lib_sha)):
+        return None
+    return rec
+
+
+def roofline(counts, pstats, n_local, C, t_kernel_s, n_sm, f_max_mhz, config_index, lib_sha, precision, hbm_peak):
+    """The integrator's floors: tensor pipe (measured mma.sync rate), issue slots (ncu), and the §8d model."""
+    f = f_max_mhz * 1e6
+    w_mma = n_local * pstats["window_samples"] * C * 8 if precision == 32 else 0
+    p_mma = n_sm * MMA_MAC_PER_CLK_SM * f
+    t_tensor = w_mma / p_mma
+    w_fp32 = n_local * (9 * counts["rot"] + 12 * counts["prec_relax"] + 9 * counts["prec"] + 4 * C * counts["adc"])
+    w_mufu = n_local * 2 * (counts["prec_relax"] + counts["prec"])
+    t_model = max(w_fp32 / (n_sm * 128 * f), w_mufu / (n_sm * 16 * f))
+    rec = _ncu_counters(config_index, lib_sha)
+    t_issue = rec["inst_executed"] / (n_sm * 4 * f) if rec and rec.get("inst_executed") else None
+    traffic = (rec.get("dram_read") or 0) + (rec.get("dram_write") or 0) if rec else None
+    out = {
+        "bound": "tensor",
+        "achieved": 2 * w_mma / t_kernel_s / 1e12,
+        "peak": 2 * p_mma / 1e12,
+        "unit": "TFLOP/s",
+        "frac": t_tensor / t_kernel_s,
+        "traffic": traffic,
+        "peak_source": f"mma.sync tf32 m16n8k8, {MMA_MAC_PER_CLK_SM} MAC/clk/SM measured (profiles/"
+                       f"r1_mma_microbench.txt) x {n_sm} SM x {f_max_mhz:.0f} MHz; work = 8 tf32-rate MAC per "
+                       "spin-sample-coil (tf32 hi*hi + one bf16 k16 pass for both cross terms)",
+        "issue_frac": t_issue / t_kernel_s if t_issue else None,
+        "issue_source": (f"ncu smsp__inst_executed.sum {rec['inst_executed']:.4g} per launch / (4 x {n_sm} x f), "
+                         f"profiles/ncu_counters.json ({rec.get('source', '')})") if t_issue else
+                        "no ncu counters for this build/config",
+        "floor_frac": max(t_tensor, t_issue or 0.0) / t_kernel_s,
+        "model_frac": t_model / t_kernel_s,
+        "model": "SURVEY §8d: T* = max(W_fp32 / (SM 128 f), W_mufu / (SM 16 f)), W_fp32 = N(9 rot + 12 prec_relax + "
+                 "9 prec + 4C adc), W_mufu = 2N(prec_relax + prec) — the reference's per-event arithmetic; the "
+                 "engine's closed-form windows do less, so model_frac > 1",
+        "kernel_ms": t_kernel_s * 1e3,
+        "tensor_floor_ms": t_tensor * 1e3,
+        "issue_floor_ms": t_issue * 1e3 if t_issue else None,
+        "model_ms": t_model * 1e3,
+        "hbm": ({"achieved_gbs": traffic / t_kernel_s / 1e9, "peak_gbs": hbm_peak,
+                 "frac": traffic / t_kernel_s / 1e9 / hbm_peak} if traffic and hbm_peak else None),
+    }
+    return out
+
+
+class Runner:
+    """One engine + stream on this rank; device-resident steps of a (sharded) workload."""
+
+    def __init__(self, local_rank, precision, world, rank, scaling):
+        import torch
+
+        from paper_1305_6861_b200.engine import get_engine
+
+        self.torch = torch
+        self.dev = torch.device("cuda", local_rank)
+        self.stream = torch.cuda.Stream(self.dev)
+        torch.cuda.set_stream(self.stream)
+        self.eng = get_engine(local_rank, precision)
+        self.eng.set_stream(self.stream.cuda_stream)
+        self.world, self.rank, self.scaling = world, rank, scaling
+        self.flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=self.dev)  # 256 MiB > 126 MB L2
+
+    def shard(self, w):
+        from paper_1305_6861_b200.parallel import lattice_spacing, shard_block, weak_copy
+
+        if self.world == 1:
+            return w.block, w.n_spins
+        if self.scaling == "weak":
+            return weak_copy(w.block, self.world, self.rank, lattice_spacing(w.block.pos)), self.world * w.n_spins
+        return shard_block(w.block, self.world, self.rank), w.n_spins
+
+    def prepare(self, w, shard):
+        from paper_1305_6861_b200.engine import _unit_weight, precompute_sequence_tables
+
+        torch = self.torch
+        C, n = w.n_coils, shard.n
+        seq = w.sequence
+        tables = precompute_sequence_tables(seq, snapshot_times=(seq.end_time,))  # final M is part of the output
+
+        def dev64(a):
+            return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(self.dev)
+
+        wt = np.ascontiguousarray(np.asarray(shard.weight, dtype=np.complex128).reshape(C, n)).view(np.float64)
+        d = {"pos": dev64(shard.pos), "mx": dev64(shard.mx), "my": dev64(shard.my), "mz": dev64(shard.mz),
+             "t1": dev64(shard.t1), "t2": dev64(shard.t2), "m0": dev64(shard.m0), "domega": dev64(shard.domega),
+             "weight": dev64(wt)}
+        ptrs = {k: v.data_ptr() for k, v in d.items()}
+        unit_w = C == 1 and _unit_weight(wt.view(np.complex128))
+        if unit_w:  # the uniform 1+0j receive weight travels as NULL, as BlochEngine.compute sends it
+            ptrs["weight"] = 0
+        f = self.eng.set_tables(tables)
+        echo = torch.zeros(C * f["n_acq"] * f["max_ns"] * 2, dtype=torch.float64, device=self.dev)
+        snap = torch.empty(max(1, n) * 3, dtype=torch.float64, device=self.dev)
+        return dict(tables=tables, d=d, ptrs=ptrs, echo=echo, snap=snap, n=n, C=C, wt=wt, unit_w=unit_w, f=f)
+
+    def timed(self, p, steps, warmup, clocks=None):
+        """K device-resident steps (compute + reduce), L2 flushed before each; per-step device time."""
+        import torch.distributed as dist
+
+        from paper_1305_6861_b200.parallel import reduce_kspace
+
+        torch = self.torch
+
+        def step():
+            self.eng.compute_device(p["tables"], p["ptrs"], p["n"], p["C"], p["echo"].data_ptr(),
+                                    p["snap"].data_ptr())
+            if self.world > 1:
+                reduce_kspace(p["echo"], dst=0)
+
+        for _ in range(warmup):
+            self.flush.fill_(1.0)
+            step()
+        torch.cuda.synchronize()
+        if self.world > 1:
+            dist.barrier()
+        if clocks is not None:
+            clocks.start()
+            time.sleep(0.3)
+        torch.cuda.synchronize()
+        if self.world > 1:
+            dist.barrier()
+        if clocks is not None:
+            clocks.mark()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        kernel_ms, launches = [], 0
+        for k in range(steps):
+            self.flush.fill_(float(k))  # untimed: evict the L2 between steps
+            ev[k][0].record(self.stream)
+            step()
+            ev[k][1].record(self.stream)
+            t = self.eng.last_timing()  # waits for this step's work
+            kernel_ms.append(t["kernel_ms"])
+            launches += t["launches"]
+        torch.cuda.synchronize()
+        if self.world > 1:
+            dist.barrier()
+        if clocks is not None:
+            clocks.mark()
+            clocks.stop()
+        step_ms = [a.elapsed_time(b) for a, b in ev]
+        tot = torch.tensor([sum(step_ms), sum(kernel_ms)], dtype=torch.float64, device=self.dev)
+        if self.world > 1:
+            dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+        return tot[0].item() / 1e3, tot[1].item() / 1e3, launches
+
+
+def main(argv=None):
+    argv = list(sys.argv[1:] if argv is None else argv)
+    args = parse_args(argv)
+    env_world = os.environ.get("WORLD_SIZE")
     if args.impl == "reference":
-        if rank != 0:
+        if int(os.environ.get("RANK", "0")) != 0:
             return 0
-        w = configs.make(args.config)
-        tables = precompute_sequence_tables(w.sequence)
-        E = event_counts(tables)["events"]
-        cb = cpu_sample(w, tables, E, args.cpu_spins_per_core, steps=args.steps,
-                        warmup=args.warmup, quiet=args.quiet)
-        line = {
-            "metric": metric, "value": cb["value"], "unit": cb["unit"], "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["seconds_per_step"] * 1e3,
-            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded, BASELINE.json config recipe)",
-            "config": {"workload": w.name, "config_index": w.index, "spins_total": w.n_spins, "events_per_spin": E,
-                       "coils": w.n_coils},
-            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
-            "e2e": {"value": cb["value"], "unit": cb["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        }
-        print(json.dumps(line), flush=True)
-        return 0
+        return reference_arm(args)
+    if env_world is None and args.gpus > 1:
+        return spawn(argv, args.gpus)
+    world = int(env_world or "1")
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
+    if args.dry:
+        return dry_run(args, world, rank)
 
     import torch
     import torch.distributed as dist
 
-    from paper_1305_6861_b200.engine import _unit_weight, get_engine
-    from paper_1305_6861_b200.parallel import lattice_spacing, reduce_kspace, shard_block, weak_copy
+    from paper_1305_6861_b200 import configs
+    from paper_1305_6861_b200.engine import event_counts, precompute_sequence_tables
 
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    # one explicit stream shared by torch (flush, events, NCCL ordering) and the library
-    stream = torch.cuda.Stream(dev)
-    torch.cuda.set_stream(stream)
+    run = Runner(local_rank, args.precision, world, rank, args.scaling)
+    dev = run.dev
+    f_max, hbm_peak = _peaks()
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    lib_sha = _lib_sha()
 
     t_setup = time.perf_counter()
-    w = configs.make(args.config)
-    seq = w.sequence
-    tables_plain = precompute_sequence_tables(seq)
-    counts = event_counts(tables_plain)
+    w = make_workload(args)
+    counts = event_counts(precompute_sequence_tables(w.sequence))
     E = counts["events"]
-    tables = precompute_sequence_tables(seq, snapshot_times=(seq.end_time,))  # final M is part of the output
-    weak = args.scaling == "weak"
-    if weak:
-        shard = weak_copy(w.block, world, rank, lattice_spacing(w.block.pos)) if world > 1 else w.block
-    else:
-        shard = shard_block(w.block, world, rank)
-    n_local, C = shard.n, w.n_coils
-    n_total = world * n_local if weak else w.n_spins
+    shard, n_total = run.shard(w)
+    p = run.prepare(w, shard)
+    pstats = run.eng.program_stats()
+    n_local, C = p["n"], p["C"]
     log(f"[rank {rank}] config {w.index} {w.name}: {n_total} spins ({n_local} local, {args.scaling}) x {E} events, "
         f"setup {time.perf_counter() - t_setup:.1f}s", args.quiet)
 
-    eng = get_engine(local_rank, args.precision)
-    eng.set_stream(stream.cuda_stream)
-    eng.set_tables(tables)
-    pstats = eng.program_stats()
-
-    def dev64(a):
-        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
-
-    wt = np.ascontiguousarray(np.asarray(shard.weight, dtype=np.complex128).reshape(C, n_local)).view(np.float64)
-    d = {"pos": dev64(shard.pos), "mx": dev64(shard.mx), "my": dev64(shard.my), "mz": dev64(shard.mz),
-         "t1": dev64(shard.t1), "t2": dev64(shard.t2), "m0": dev64(shard.m0), "domega": dev64(shard.domega),
-         "weight": dev64(wt)}
-    ptrs = {k: v.data_ptr() for k, v in d.items()}
-    unit_w = C == 1 and _unit_weight(wt.view(np.complex128))
-    if unit_w:  # the uniform 1+0j receive weight travels as NULL, as BlochEngine.compute sends it
-        ptrs["weight"] = 0
-    n_acq = tables.n_acq
-    max_ns = max(e.n_samples for e in tables.entries)
-    echo = torch.zeros(C * n_acq * max_ns * 2, dtype=torch.float64, device=dev)
-    snap = torch.empty(max(1, n_local) * 3, dtype=torch.float64, device=dev)
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
-
-    def step():
-        eng.compute_device(tables, ptrs, n_local, C, echo.data_ptr(), snap.data_ptr())
-        if world > 1:
-            reduce_kspace(echo, dst=0)
-
-    for _ in range(args.warmup):
-        flush.fill_(1.0)
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
     clocks = ClockSampler(local_rank)
-    clocks.start()
-    time.sleep(0.3)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clocks.mark()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    kernel_ms, launches = [], 0
-    for k in range(args.steps):
-        flush.fill_(float(k))  # untimed: evict the L2 between steps
-        ev[k][0].record(stream)
-        step()
-        ev[k][1].record(stream)
-        t = eng.last_timing()  # waits for this step's work
-        kernel_ms.append(t["kernel_ms"])
-        launches += t["launches"]
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clocks.mark()
-    clocks.stop()
-    launch_shape = eng.last_launch()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    total_ms = torch.tensor([sum(step_ms), sum(kernel_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
-    t_total_s, t_kernel_s = total_ms[0].item() / 1e3, total_ms[1].item() / 1e3
+    t_total_s, t_kernel_s, launches = run.timed(p, args.steps, args.warmup, clocks)
     value = n_total * E * args.steps / t_total_s
+    launch_shape = run.eng.last_launch()
+    t_kernel = t_kernel_s / args.steps
 
     # ---- end to end through the public host API (pinned host buffers) ------------------
+    from paper_1305_6861_b200.parallel import reduce_kspace
+
     e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).pin_memory().numpy()
-    h = {"pos": pin(shard.pos), "mx": pin(shard.mx), "my": pin(shard.my), "mz": pin(shard.mz), "t1": pin(shard.t1),
-         "t2": pin(shard.t2), "m0": pin(shard.m0), "domega": pin(shard.domega)}
-    hw = torch.from_numpy(wt.copy()).pin_memory().numpy().view(np.complex128).reshape(C, n_local)
+    h = {k: pin(getattr(shard, k)) for k in ("pos", "mx", "my", "mz", "t1", "t2", "m0", "domega")}
+    hw = torch.from_numpy(p["wt"].copy()).pin_memory().numpy().view(np.complex128).reshape(C, n_local)
     if C == 1:
         hw = hw[0]
-    out_e = torch.zeros(C * n_acq * max_ns * 2, dtype=torch.float64).pin_memory().numpy().view(np.complex128)
-    out_e = out_e.reshape(C, n_acq, max_ns)
-    out_s = torch.zeros(1 * n_local * 3, dtype=torch.float64).pin_memory().numpy().reshape(1, n_local, 3)
+    f = p["f"]
+    n_acq, max_ns = f["n_acq"], f["max_ns"]
+    tables = p["tables"]
     red = torch.zeros(C * n_acq * max_ns * 2, dtype=torch.float64, device=dev)
-
-    def e2e_step():
-        e, s = eng.compute(tables, h["pos"], h["mx"], h["my"], h["mz"], h["t1"], h["t2"], h["m0"], h["domega"], hw,
-                           out_echoes=out_e, out_snaps=out_s)
-        if world > 1:
-            red.copy_(torch.from_numpy(out_e.view(np.float64).reshape(-1)), non_blocking=False)
-            reduce_kspace(red, dst=0)
-            torch.cuda.synchronize()
-        return e, s
-
     if world == 1:
         # one GPU: the engine's double-buffered Pipeline (two contexts, own streams and device buffers),
         # so step k+1's uploads and step k's downloads overlap the kernels; every step still moves its
@@ -344,8 +609,20 @@ def main():
         t0 = time.perf_counter()
         e2e_run(e2e_steps)
         torch.cuda.synchronize()
+        out_e, out_s = slots[0]
         e2e_path = "Pipeline (2 engine contexts) -> bloch_compute_block, pinned host buffers, uploads/downloads overlapped"
     else:
+        out_e = torch.zeros(C * n_acq * max_ns * 2, dtype=torch.float64).pin_memory().numpy().view(np.complex128)
+        out_e = out_e.reshape(C, n_acq, max_ns)
+        out_s = torch.zeros(n_local * 3, dtype=torch.float64).pin_memory().numpy().reshape(1, n_local, 3)
+
+        def e2e_step():
+            run.eng.compute(tables, h["pos"], h["mx"], h["my"], h["mz"], h["t1"], h["t2"], h["m0"], h["domega"], hw,
+                            out_echoes=out_e, out_snaps=out_s)
+            red.copy_(torch.from_numpy(out_e.view(np.float64).reshape(-1)), non_blocking=False)
+            reduce_kspace(red, dst=0)
+            torch.cuda.synchronize()
+
         e2e_step()
         torch.cuda.synchronize()
         dist.barrier()
@@ -358,97 +635,75 @@ def main():
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     e2e_value = n_total * E * e2e_steps / e2e_s.item()
-    h2d = sum(a.nbytes for a in h.values()) + (0 if unit_w else wt.nbytes)
+    h2d = sum(a.nbytes for a in h.values()) + (0 if p["unit_w"] else p["wt"].nbytes)
     d2h = out_e.nbytes + out_s.nbytes
 
-    # ---- roofline (FP32 / MUFU model) --------------------------------------
-    props = torch.cuda.get_device_properties(dev)
-    n_sm = props.multi_processor_count
-    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    f_max = 1965.0
-    try:
-        with open(peaks_path) as fh:
-            f_max = float(json.load(fh).get("sm_max_mhz", f_max))
-    except Exception:
-        pass
-    w_fp32 = n_local * (9 * counts["rot"] + 12 * counts["prec_relax"] + 9 * counts["prec"] + 4 * C * counts["adc"])
-    w_mufu = n_local * 2 * (counts["prec_relax"] + counts["prec"])
-    p_fp32 = n_sm * 128 * f_max * 1e6
-    p_mufu = n_sm * 16 * f_max * 1e6
-    t_star = max(w_fp32 / p_fp32, w_mufu / p_mufu)
-    t_kernel = t_kernel_s / args.steps
-    model_ops = max(w_fp32, 8 * w_mufu)
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            traffic = json.load(fh).get(f"config{args.config}")
-    except Exception:
-        pass
-    # the contract's measured denominators (MEASURED_PEAKS.json), beside the SURVEY §8d model:
-    # HBM traffic of the integrator (ncu capture) and the tensor pipe's actual work in the ADC
-    # windows: per spin-sample-coil one tf32 m16n8k8 pass (4 real MAC at the measured 512 MAC/clk/SM)
-    # and one bf16 m16n8k16 pass for both cross terms (8 real MAC at 1024 MAC/clk/SM), i.e. 8
-    # tf32-rate MAC equivalents (profiles/r1_mma_microbench.txt).
-    hbm_peak = bf16_peak = None
-    try:
-        with open(peaks_path) as fh:
-            mp = json.load(fh)
-        hbm_peak, bf16_peak = float(mp["hbm_gbs"]), float(mp["bf16_tflops"])
-    except Exception:
-        pass
-    w_mma = n_local * pstats["window_samples"] * C * 8 if args.precision == 32 else 0
-    p_mma = n_sm * 512 * f_max * 1e6
-    measured = {
-        "hbm": {"achieved_gbs": traffic / t_kernel / 1e9 if traffic else None, "peak_gbs": hbm_peak,
-                "frac": traffic / t_kernel / 1e9 / hbm_peak if traffic and hbm_peak else None,
-                "source": "peak of measured (MEASURED_PEAKS.json hbm_gbs)"},
-        "tensor_mma_tf32": {"achieved_tflops": 2 * w_mma / t_kernel / 1e12, "peak_tflops": 2 * p_mma / 1e12,
-                            "frac": w_mma / p_mma / t_kernel,
-                            "source": "tf32-rate MAC equivalents (tf32 hi*hi + bf16 k16 cross terms) over the "
-                                      "measured mma.sync m16n8k8 tf32 peak, 512 MAC/clk/SM "
-                                      "(profiles/r1_mma_microbench.txt); bf16 GEMM peak of measured "
-                                      f"{bf16_peak} TFLOP/s is tcgen05 bf16 and does not apply"},
-    }
-    roofline = {
-        "bound": "fp32+mufu",
-        "achieved": model_ops / t_kernel / 1e12,
-        "peak": p_fp32 / 1e12,
-        "unit": "TFLOP/s",
-        "frac": t_star / t_kernel,
-        "traffic": traffic,
-        "model": "ops = max(W_fp32, 8*W_mufu); W_fp32 = N(9 rot + 12 prec_relax + 9 prec + 4C adc), "
-                 "W_mufu = 2N(prec_relax + prec); FP32 op = 1 lane-instruction (FFMA/FMUL/FADD); "
-                 f"peak = {n_sm} SM x 128 lanes x {f_max:.0f} MHz (nominal; FFMA measured 125.3/128, profiles/)",
-        "kernel_ms": t_kernel * 1e3,
-        "roofline_ms": t_star * 1e3,
-        "updates_per_s_at_roofline": n_local * E / t_star,
-        "measured_peaks": measured,
-    }
-
+    roof = roofline(counts, pstats, n_local, C, t_kernel, n_sm, f_max, w.index, lib_sha, args.precision, hbm_peak)
     line = {
-        "metric": metric, "value": value, "unit": metric, "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_total_s * 1e3 / args.steps, "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None,
-        "dtype": ("f64 spin state/phase/fold; f32 ADC sums (tf32 hi*hi + bf16 cross terms on the tensor cores)"
-                  if args.precision == 32 else "f64"),
+        "dtype": ("f64 spin state/phase; f32 ADC sums (tf32 hi*hi + bf16 cross terms on the tensor cores), "
+                  "f64 fold" if args.precision == 32 else "f64"),
         "data": "synthetic (seeded, BASELINE.json config recipe)",
-        "config": {"workload": w.name, "config_index": w.index, "spins_total": n_total, "spins_per_rank": n_local,
-                   "sharding": ("weak: every rank a full config-sized spin set (world interleaved copies of the "
-                                "lattice, shifted by rank/world of its x spacing; parallel.weak_copy), one NCCL "
-                                "reduce of the k-space" if weak else "strong: np.linspace spin shards of the config")
-                               if world > 1 else "single GPU",
-                   "events_per_spin": E, "coils": C, "event_classes": counts, "program": pstats,
-                   "l2": "flushed between timed steps (256 MiB write)", "parallelism": f"spin-shards x{world}"},
-        "roofline": roofline,
+        "config": config_dict(w, world, E, counts, args.scaling, args.full_lattice),
+        "spins_per_rank": n_local,
+        "program": pstats,
+        "roofline": roof,
         "integrator_launch": launch_shape,
-        "e2e": {"value": e2e_value, "unit": metric, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+        "e2e": {"value": e2e_value, "unit": METRIC, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "steps": e2e_steps, "path": e2e_path},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "kernel_ms_per_step": t_kernel * 1e3,
+        "lib_sha16": lib_sha,
     }
+    del p
+    if world == 1:
+        pipe.close()
+
+    # ---- the other configurations, same world and sharding --------------------------------
+    if not args.no_per_config:
+        per = {}
+        for c in range(configs.N_CONFIGS):
+            wc = w if c == args.config else configs.make(c, full_lattice=args.full_lattice)
+            cc = event_counts(precompute_sequence_tables(wc.sequence))
+            sh, nt = run.shard(wc)
+            pc = run.prepare(wc, sh)
+            ps = run.eng.program_stats()
+            st = max(3, min(args.steps, 10))
+            tt, tk, _ = run.timed(pc, st, 2)
+            rc = roofline(cc, ps, pc["n"], pc["C"], tk / st, n_sm, f_max, c, lib_sha, args.precision, hbm_peak)
+            per[f"config{c}"] = {"workload": wc.name, "spins_total": nt, "events_per_spin": cc["events"],
+                                 "value": nt * cc["events"] * st / tt, "ms_per_step": tt * 1e3 / st,
+                                 "kernel_ms": tk * 1e3 / st, "frac": rc["frac"], "issue_frac": rc["issue_frac"],
+                                 "model_frac": rc["model_frac"],
+                                 "spins_per_thread": run.eng.last_launch()["spins_per_thread"]}
+            del pc
+        line["per_config"] = per
+
+    # ---- strong scaling: the per-rank work of N = 2, 4, 8 on this GPU -----------------------
+    if world == 1 and not args.no_projection:
+        from paper_1305_6861_b200.parallel import shard_block
+
+        proj = {}
+        t1 = t_total_s / args.steps
+        for nr in (2, 4, 8):
+            sh = shard_block(w.block, nr, 0)  # the largest shard (np.linspace bounds)
+            pc = run.prepare(w, sh)
+            st = max(3, min(args.steps, 10))
+            tt, tk, _ = run.timed(pc, st, 2)
+            proj[str(nr)] = {"shard_spins": sh.n, "ms_per_step": tt * 1e3 / st, "kernel_ms": tk * 1e3 / st,
+                             "efficiency_est": t1 / (nr * tt / st), "spins_per_thread":
+                             run.eng.last_launch()["spins_per_thread"]}
+            del pc
+        line["strong_scaling_projection"] = {
+            "note": "one B200: device time of rank 0's np.linspace shard (the largest) per step vs this line's "
+                    "ms_per_step; excludes the NCCL reduce of the fp64 k-space (config 2: 4 MiB)",
+            **proj}
+
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = cpu_sample(w, tables_plain, E, args.cpu_spins_per_core, quiet=args.quiet)
+        cb = cpu_sample(w, E, args.cpu_spins_per_core, quiet=args.quiet)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
     if rank == 0:
         print(json.dumps(line), flush=True)

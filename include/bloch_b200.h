@@ -49,8 +49,8 @@ extern "C" {
 #define BLOCH_E_NOMEM -4   /* device allocation failed                            */
 
 /* precision of the per-spin state inside the kernel */
-#define BLOCH_PREC_F32 32 /* fp32 state, fp64 phase / signal accumulation (default) */
-#define BLOCH_PREC_F64 64 /* fp64 everywhere (for the reference's 1e-12 unit tests) */
+#define BLOCH_PREC_F32 32 /* fp64 spin state and phases; fp32 ADC sample sums (tensor cores) (default) */
+#define BLOCH_PREC_F64 64 /* fp64 everywhere, sample sums included (the reference's 1e-12 unit tests) */
 
 /* bloch_compute_block flags */
 #define BLOCH_IN_DEVICE 1u  /* spin arrays are device pointers (else host)          */
@@ -74,6 +74,25 @@ int bloch_device_count(int* out);
 /* Create a context on `device` (or BLOCH_HOST_ONLY) with state precision BLOCH_PREC_F32 / _F64. */
 int bloch_create(int device, int precision, bloch_ctx** out);
 int bloch_destroy(bloch_ctx* ctx);
+
+/*
+ * A device set (the reference's domain decomposition over spins, engine.py:229-251 and
+ * 540-595, across the GPUs of one box, from one host thread).  The context holds one sub-context per
+ * device, in rank order.  bloch_set_tables compiles the program once per device; bloch_compute_block
+ * (host spin arrays only) cuts the block into contiguous shards with np.linspace bounds — rank r takes
+ * [floor(r n/k), floor((r+1) n/k)) exactly as partition_blocks — evolves them concurrently, each on its
+ * own device and stream, copies each shard's final magnetisation rows into place (rank order is the
+ * reference's block order, engine.py:497-504) and performs the one exchange: every partial k-space is
+ * pulled to the first device (peer copies over NVLink/NVSwitch) and summed there in rank order in fp64
+ * (the reference's ordered fold, engine.py:493-496, 594-595).  Outputs are host buffers, or device
+ * buffers on the first device.  Listing a device twice is allowed (two shards on one GPU).
+ */
+int bloch_create_multi(const int32_t* devices, int32_t n_devices, int precision, bloch_ctx** out);
+/* Devices of a context (1 for a single-device context); `devices` may be NULL or hold n entries. */
+int bloch_device_count_of(const bloch_ctx* ctx, int32_t* n_devices, int32_t* devices);
+/* Per-device integrator and whole-call device time (ms) of the last synchronous call, rank order:
+ * `capacity` entries at most (the reference's per-worker busy time, engine.py:516-525). */
+int bloch_last_device_times(const bloch_ctx* ctx, int32_t capacity, float* kernel_ms, float* device_ms);
 /* Stream used for all work of this context (a cudaStream_t; NULL = context-owned). */
 int bloch_set_stream(bloch_ctx* ctx, void* stream);
 
@@ -232,6 +251,7 @@ int bloch_last_launch(const bloch_ctx* ctx, int32_t* prec, int32_t* spins_per_th
  * runs as several launches over contiguous op ranges, the fp64 state handed over through global
  * memory and each range's samples folded before the next: the results are bit-identical. */
 int bloch_last_segments(const bloch_ctx* ctx, int32_t* segments);
+
 
 #ifdef __cplusplus
 }

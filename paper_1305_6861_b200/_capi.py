@@ -60,6 +60,9 @@ SIGNATURES = {
     "bloch_device_count": (c_int, [POINTER(c_int)]),
     "bloch_create": (c_int, [c_int, c_int, POINTER(c_void_p)]),
     "bloch_destroy": (c_int, [c_void_p]),
+    "bloch_create_multi": (c_int, [POINTER(c_int32), c_int32, c_int, POINTER(c_void_p)]),
+    "bloch_device_count_of": (c_int, [c_void_p, POINTER(c_int32), POINTER(c_int32)]),
+    "bloch_last_device_times": (c_int, [c_void_p, c_int32, POINTER(c_float), POINTER(c_float)]),
     "bloch_set_stream": (c_int, [c_void_p, c_void_p]),
     "bloch_set_tables": (
         c_int,

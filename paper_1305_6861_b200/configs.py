@@ -126,7 +126,7 @@ class _Ellipses:
             lab = np.where(r <= 1.0, k, lab)  # later entries override earlier ones
         return lab
 
-    def phantom(self, origin, size) -> Phantom:
+    def phantom(self, origin, size, bg_m0: float = 0.0) -> Phantom:
         def prop(table, background):
             def f(x, y, z):
                 lab = self.label(x, y, z)
@@ -134,7 +134,7 @@ class _Ellipses:
 
             return f
 
-        return Phantom([PhantomBox(origin=origin, size=size, m0=prop(self.pd, 0.0), t1=prop(self.t1, 1.0),
+        return Phantom([PhantomBox(origin=origin, size=size, m0=prop(self.pd, bg_m0), t1=prop(self.t1, 1.0),
                                    t2=prop(self.t2, 0.1))])
 
 
@@ -146,9 +146,14 @@ def _block(spins, domega, weight) -> SpinBlock:
     )
 
 
-def _plane(pixels: int, iso: int, ell: _Ellipses) -> Dict[str, np.ndarray]:
+# --full-lattice: PD of the background tissue (T1 1 s, T2 0.1 s) †, so every lattice site emits a spin
+FULL_LATTICE_BG_PD = 0.1
+
+
+def _plane(pixels: int, iso: int, ell: _Ellipses, full_lattice: bool = False) -> Dict[str, np.ndarray]:
     spacing = FOV / (pixels * iso)
-    ph = ell.phantom(origin=(-FOV / 2, -FOV / 2, -spacing / 2), size=(FOV, FOV, spacing))
+    ph = ell.phantom(origin=(-FOV / 2, -FOV / 2, -spacing / 2), size=(FOV, FOV, spacing),
+                     bg_m0=FULL_LATTICE_BG_PD if full_lattice else 0.0)
     return rasterize_arrays(ph, (spacing, spacing, spacing), cap=4_000_000)
 
 
@@ -187,20 +192,20 @@ def _ring_coils(coil_rng, n_coils: int):
     return coils
 
 
-def config0() -> Workload:
+def config0(full_lattice: bool = False) -> Workload:
     geo, tissue, _dw, _rf, _coil = _streams(0)
     ell = _Ellipses(geo, tissue)
-    spins = _plane(64, 1, ell)
+    spins = _plane(64, 1, ell, full_lattice)
     seq = config_sequence(0)
     blk = _block(spins, np.zeros(spins["m0"].size), np.full(spins["m0"].size, 1.0 + 0.0j))
     return Workload(0, "cfg0_se64", seq, blk, {"fov": FOV, "grid": [64, 64], "iso": 1, "te": 0.02, "tr": 0.5,
                                                  "dwell": 10e-6})
 
 
-def config1() -> Workload:
+def config1(full_lattice: bool = False) -> Workload:
     geo, tissue, dwr, _rf, _coil = _streams(1)
     ell = _Ellipses(geo, tissue)
-    spins = _plane(256, 4, ell)
+    spins = _plane(256, 4, ell, full_lattice)
     seq = config_sequence(1)
     dw = dwr.normal(0.0, 2.0 * math.pi * 20.0, spins["m0"].size)
     blk = _block(spins, dw, np.full(spins["m0"].size, 1.0 + 0.0j))
@@ -208,10 +213,10 @@ def config1() -> Workload:
                                                        "tr": 0.8, "dwell": 10e-6, "dw_sigma_hz": 20.0})
 
 
-def config2() -> Workload:
+def config2(full_lattice: bool = False) -> Workload:
     geo, tissue, dwr, rf, _coil = _streams(2)
     ell = _Ellipses(geo, tissue)
-    spins = _plane(512, 2, ell)
+    spins = _plane(512, 2, ell, full_lattice)
     n, tf = 512, 16
     seq = config_sequence(2, rf)
     # smooth cubic 2-D polynomial B0 map, peak +-2pi*100 rad/s over the lattice
@@ -257,10 +262,10 @@ def epi_trapezoid_sequence(n_lines=128, dwell=4e-6, ramp=40e-6, flat=500e-6, bli
                                                       "ramp": ramp, "flat": flat, "blip": blip})
 
 
-def config3() -> Workload:
+def config3(full_lattice: bool = False) -> Workload:
     geo, tissue, dwr, _rf, _coil = _streams(3)
     ell = _Ellipses(geo, tissue, t2_range=(0.02, 0.12))
-    spins = _plane(128, 8, ell)
+    spins = _plane(128, 8, ell, full_lattice)
     seq = config_sequence(3)
     c = dwr.uniform(-0.4, 0.4, (5, 2)) * FOV
     sig = dwr.uniform(0.05, 0.15, 5) * FOV
@@ -328,12 +333,13 @@ def multipulse_3d_sequence(n_lines=128, n_read=256, dwell=10e-6, flips=(math.pi 
                                                      "windows": list(windows)})
 
 
-def config4(n_coils: int = 8) -> Workload:
+def config4(n_coils: int = 8, full_lattice: bool = False) -> Workload:
     geo, tissue, _dw, _rf, coil = _streams(4)
     ext = (FOV, FOV, FOV / 2)
     ell = _Ellipses(geo, tissue, dim=3, extent=ext)
     spacing = FOV / 128
-    ph = ell.phantom(origin=(-FOV / 2, -FOV / 2, -FOV / 4), size=(FOV, FOV, FOV / 2))
+    ph = ell.phantom(origin=(-FOV / 2, -FOV / 2, -FOV / 4), size=(FOV, FOV, FOV / 2),
+                     bg_m0=FULL_LATTICE_BG_PD if full_lattice else 0.0)
     spins = rasterize_arrays(ph, (spacing, spacing, spacing), cap=4_000_000)
     seq = config_sequence(4)
     coils = _ring_coils(coil, n_coils)
@@ -347,8 +353,14 @@ def config4(n_coils: int = 8) -> Workload:
 BUILDERS = {0: config0, 1: config1, 2: config2, 3: config3, 4: config4}
 
 
-def make(index: int) -> Workload:
-    return BUILDERS[int(index)]()
+def make(index: int, full_lattice: bool = False) -> Workload:
+    """Config `index`; ``full_lattice`` gives the background sites PD 0.1 (so configs 1-4 hold all
+    1,048,576 lattice sites as spins, the count BASELINE.json states) and marks the name with ``_full``."""
+    w = BUILDERS[int(index)](full_lattice=full_lattice)
+    if full_lattice:
+        w.name += "_full"
+        w.meta["full_lattice_bg_pd"] = FULL_LATTICE_BG_PD
+    return w
 
 
 # ---------------------------------------------------------------------------

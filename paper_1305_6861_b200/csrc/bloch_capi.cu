@@ -4,7 +4,10 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <cmath>
+
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
@@ -39,11 +42,16 @@ inline void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// bumped whenever any device buffer is (re)allocated: a captured CUDA graph holds raw pointers into
+// the context's scratch buffers, so a graph recorded before a reallocation must never be replayed
+std::atomic<uint64_t> g_alloc_gen{0};
+
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
   void* ensure(size_t bytes) {
     if (bytes <= cap) return p;
+    g_alloc_gen.fetch_add(1);
     if (p) cudaFree(p);
     p = nullptr;
     cap = 0;
@@ -83,6 +91,7 @@ struct bloch_ctx {
   DevBuf in_pos, in_mx, in_my, in_mz, in_t1, in_t2, in_m0, in_dw, in_w;
   DevBuf sc, wpad, w32;
   DevBuf partial, echo, snaps, relax, planetab, planetab32, traintab;
+
   DevBuf raster_scratch;
   std::vector<unsigned char> raster_staging;
   float kernel_ms = 0.f, device_ms = 0.f;
@@ -99,9 +108,11 @@ struct bloch_ctx {
     int32_t n_coils = 0;
     uint32_t flags = 0;
     uint64_t gen = 0;
+    uint64_t alloc = 0;  // g_alloc_gen: no buffer reallocated since
     cudaStream_t st = nullptr;
     bool operator==(const GraphKey& o) const {
-      if (n != o.n || n_coils != o.n_coils || flags != o.flags || gen != o.gen || st != o.st) return false;
+      if (n != o.n || n_coils != o.n_coils || flags != o.flags || gen != o.gen || alloc != o.alloc || st != o.st)
+        return false;
       for (int i = 0; i < 12; ++i)
         if (p[i] != o.p[i]) return false;
       return true;
@@ -110,6 +121,13 @@ struct bloch_ctx {
   cudaGraphExec_t graph_exec = nullptr;
   int graph_launches = 0;
   cudaEvent_t gate_wait = nullptr, gate_signal = nullptr;  // bloch_set_kernel_gate
+  // device-set context (bloch_create_multi): one sub-context per device, in rank order; this context's
+  // own device / stream (the first device's) runs the cross-device reduction
+  std::vector<bloch_ctx*> subs;
+  std::vector<DevBuf> sub_echo, sub_snap;  // each sub-context's partial echoes / snapshots, on its device
+  std::vector<cudaEvent_t> sub_done;       // recorded on each sub-context's stream after its work
+  DevBuf gather;                           // [n_sub][len] partial echoes on the first device
+  std::vector<float> sub_kernel_ms, sub_device_ms;
   void drop_graph() {
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
     graph_exec = nullptr;
@@ -339,12 +357,22 @@ int bloch_destroy(bloch_ctx* c) {
     delete c;
     return BLOCH_OK;
   }
+  for (size_t i = 0; i < c->subs.size(); ++i) {
+    cudaSetDevice(c->subs[i]->device);
+    if (i < c->sub_echo.size()) c->sub_echo[i].release();
+    if (i < c->sub_snap.size()) c->sub_snap[i].release();
+    if (i < c->sub_done.size() && c->sub_done[i]) cudaEventDestroy(c->sub_done[i]);
+    bloch_destroy(c->subs[i]);
+  }
+  c->subs.clear();
+  cudaSetDevice(c->device);
+  c->gather.release();
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   c->drop_graph();
   for (DevBuf* b : {&c->d_ops, &c->d_gev, &c->d_mats, &c->d_sample_g, &c->d_relax_t, &c->relax, &c->d_planes, &c->planetab, &c->planetab32, &c->in_pos, &c->in_mx, &c->in_my, &c->in_mz,
                     &c->in_t1, &c->in_t2, &c->in_m0, &c->in_dw, &c->in_w, &c->sc, &c->wpad, &c->w32, &c->partial,
-                    &c->echo, &c->snaps, &c->d_train_cls, &c->traintab, &c->state,
+                    &c->echo, &c->snaps, &c->d_train_cls, &c->traintab, &c->state, 
                     &c->raster_scratch})
     b->release();
   for (auto& ev : c->ev)
@@ -356,6 +384,7 @@ int bloch_destroy(bloch_ctx* c) {
 
 int bloch_set_stream(bloch_ctx* c, void* stream) {
   if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
+  if (!c->subs.empty()) return fail(BLOCH_E_STATE, "a device-set context owns one stream per device");
   if (c->device == BLOCH_HOST_ONLY) return fail(BLOCH_E_STATE, "host-only context has no stream");
   cudaSetDevice(c->device);
   c->drop_graph();
@@ -385,6 +414,14 @@ int bloch_set_tables(bloch_ctx* c, int32_t n_es, const int64_t* es_ev_offset,
   const int64_t E = n_es > 0 ? es_ev_offset[n_es] : 0;
   if (E > 0 && (!ev_dt || !ev_dmom || !ev_sample || !ev_snap))
     return fail(BLOCH_E_INVALID, "NULL event array");
+  for (bloch_ctx* sub : c->subs) {  // a device-set context: every device gets the program
+    const int st = bloch_set_tables(sub, n_es, es_ev_offset, es_has_pulse, es_pulse_mat, es_acq, ev_dt, ev_dmom,
+                                    ev_sample, ev_snap, n_acq, max_samples, n_snap);
+    if (st != BLOCH_OK) {
+      c->has_prog = false;
+      return st;
+    }
+  }
   bloch::TablesView tv{n_es, es_ev_offset, es_has_pulse, es_pulse_mat, es_acq, ev_dt,
                        ev_dmom, ev_sample, ev_snap, n_acq, max_samples, n_snap};
   try {
@@ -460,12 +497,194 @@ int bloch_program_classes(const bloch_ctx* c, int64_t* n_prog_classes, int64_t* 
   return BLOCH_OK;
 }
 
+namespace {
+// spin shard [b[r], b[r+1]) of rank r among k: np.linspace(0, n, k + 1).astype(int), as
+// partition_blocks (engine.py:229-251) and parallel.shard_bounds compute it
+std::vector<int64_t> linspace_bounds(int64_t n, int k) {
+  std::vector<int64_t> b(static_cast<size_t>(k) + 1);
+  const double step = static_cast<double>(n) / static_cast<double>(k);
+  for (int i = 0; i < k; ++i) b[i] = static_cast<int64_t>(static_cast<double>(i) * step);
+  b[k] = n;
+  return b;
+}
+
+// bloch_compute_block on a device-set context: contiguous shards, one per device, computed
+// concurrently (each sub-context on its own device and stream); the partial k-spaces are pulled
+// to the first device (peer copies over NVLink) and summed there in rank order.
+int compute_multi(bloch_ctx* c, int64_t n, const double* pos, const double* mx, const double* my, const double* mz,
+                  const double* t1, const double* t2, const double* m0, const double* domega, const double* weight,
+                  int32_t n_coils, double* echoes_out, double* snaps_out, uint8_t* snap_present, uint32_t flags) {
+  if (flags & BLOCH_IN_DEVICE) return fail(BLOCH_E_INVALID, "a device-set context takes host spin arrays");
+  const bloch::Program& P = c->prog;
+  const int k = static_cast<int>(c->subs.size());
+  const int64_t G = static_cast<int64_t>(P.n_acq) * P.max_samples;
+  const int64_t len = G * n_coils * 2;  // doubles of one partial k-space
+  const int64_t n_snap = snaps_out ? P.n_snap : 0;
+  const bool out_dev = flags & BLOCH_OUT_DEVICE;
+  const std::vector<int64_t> b = linspace_bounds(n, k);
+  try {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    ck(cudaEventRecord(c->ev[0], c->stream), "event");
+    c->sub_echo.resize(k);
+    c->sub_snap.resize(k);
+    c->sub_done.resize(k, nullptr);
+    c->sub_kernel_ms.assign(k, 0.f);
+    c->sub_device_ms.assign(k, 0.f);
+    std::vector<double> wtmp;
+    for (int r = 0; r < k; ++r) {
+      bloch_ctx* sub = c->subs[r];
+      const int64_t lo = b[r], nr = b[r + 1] - b[r];
+      ck(cudaSetDevice(sub->device), "cudaSetDevice");
+      if (!c->sub_done[r]) ck(cudaEventCreateWithFlags(&c->sub_done[r], cudaEventDisableTiming), "event");
+      double* e = static_cast<double*>(c->sub_echo[r].ensure(static_cast<size_t>(std::max<int64_t>(1, len)) * 8));
+      double* sn = n_snap ? static_cast<double*>(c->sub_snap[r].ensure(static_cast<size_t>(std::max<int64_t>(
+                                1, n_snap * nr * 3)) * 8))
+                          : nullptr;
+      const double* w = nullptr;
+      if (weight && n_coils == 1) {
+        w = weight + 2 * lo;
+      } else if (weight) {  // [coil][spin] -> this shard's [coil][spin]
+        wtmp.assign(static_cast<size_t>(n_coils * nr * 2), 0.0);
+        for (int cc = 0; cc < n_coils; ++cc)
+          memcpy(wtmp.data() + cc * nr * 2, weight + (cc * n + lo) * 2, static_cast<size_t>(nr) * 16);
+        w = wtmp.data();
+      }
+      const int st = bloch_compute_block(sub, nr, pos + 3 * lo, mx + lo, my + lo, mz + lo, t1 + lo, t2 + lo,
+                                         m0 + lo, domega + lo, w, n_coils, e, sn, r == 0 ? snap_present : nullptr,
+                                         BLOCH_OUT_DEVICE | BLOCH_NO_SYNC);
+      if (st != BLOCH_OK) return fail(st, "device " + std::to_string(sub->device) + " (rank " + std::to_string(r) +
+                                              "): " + g_err);
+      if (n_snap && nr > 0)  // this shard's rows of every snapshot, in place (rank order = block order)
+        ck(cudaMemcpy2DAsync(snaps_out + lo * 3, static_cast<size_t>(n) * 24, sn, static_cast<size_t>(nr) * 24,
+                             static_cast<size_t>(nr) * 24, static_cast<size_t>(n_snap), cudaMemcpyDefault,
+                             sub->stream),
+           "snapshot copy");
+      ck(cudaEventRecord(c->sub_done[r], sub->stream), "event");
+    }
+    // the one exchange: partial k-spaces to the first device, summed in rank order
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    double* gath = static_cast<double*>(c->gather.ensure(static_cast<size_t>(std::max<int64_t>(1, len * k)) * 8));
+    for (int r = 0; r < k; ++r) {
+      ck(cudaStreamWaitEvent(c->stream, c->sub_done[r], 0), "wait");
+      if (len)
+        ck(cudaMemcpyPeerAsync(gath + r * len, c->device, c->sub_echo[r].p, c->subs[r]->device,
+                               static_cast<size_t>(len) * 8, c->stream),
+           "peer copy");
+    }
+    double* d_out = out_dev ? echoes_out : static_cast<double*>(c->echo.ensure(static_cast<size_t>(std::max<int64_t>(1, len)) * 8));
+    if (len) ck(bloch::launch_sum_rows(gath, k, len, d_out, c->stream), "sum kernel");
+    if (!out_dev && len)
+      ck(cudaMemcpyAsync(echoes_out, d_out, static_cast<size_t>(len) * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaEventRecord(c->ev[3], c->stream), "event");
+    c->launches = 1;
+    if (!(flags & BLOCH_NO_SYNC)) {
+      ck(cudaStreamSynchronize(c->stream), "sync");
+      float mk = 0.f;
+      for (int r = 0; r < k; ++r) {
+        float km = 0.f, dm = 0.f;
+        int32_t l = 0;
+        bloch_last_timing(c->subs[r], &km, &dm, &l);
+        c->sub_kernel_ms[r] = km;
+        c->sub_device_ms[r] = dm;
+        mk = std::max(mk, km);
+        c->launches += l;
+      }
+      c->kernel_ms = mk;
+      ck(cudaEventElapsedTime(&c->device_ms, c->ev[0], c->ev[3]), "elapsed");
+    }
+    for (int i = 0; snap_present && i < P.n_snap; ++i) snap_present[i] = c->snap_present[i];
+    c->last_launch[0] = c->subs[0]->last_launch[0];
+    for (int i = 1; i < 5; ++i) c->last_launch[i] = c->subs[0]->last_launch[i];
+  } catch (const std::exception& ex) {
+    return fail(BLOCH_E_CUDA, ex.what());
+  }
+  return BLOCH_OK;
+}
+}  // namespace
+
+int bloch_create_multi(const int32_t* devices, int32_t n_devices, int precision, bloch_ctx** out) {
+  if (!out) return fail(BLOCH_E_INVALID, "out is NULL");
+  *out = nullptr;
+  if (!devices || n_devices < 1 || n_devices > bloch::kMaxDevices) return fail(BLOCH_E_INVALID, "need 1..64 devices");
+  bloch_ctx* c = nullptr;
+  int st = bloch_create(devices[0], precision, &c);
+  if (st != BLOCH_OK) return st;
+  for (int32_t r = 0; r < n_devices; ++r) {
+    bloch_ctx* sub = nullptr;
+    st = bloch_create(devices[r], precision, &sub);
+    if (st != BLOCH_OK) {
+      const std::string msg = g_err;
+      bloch_destroy(c);
+      return fail(st, "device " + std::to_string(devices[r]) + ": " + msg);
+    }
+    c->subs.push_back(sub);
+    if (devices[r] != devices[0]) {  // NVLink peer access for the reduction's copies (they work without it)
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, devices[0], devices[r]);
+      if (can) {
+        cudaSetDevice(devices[0]);
+        const cudaError_t e = cudaDeviceEnablePeerAccess(devices[r], 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+          bloch_destroy(c);
+          return fail(BLOCH_E_CUDA, std::string("peer access: ") + cudaGetErrorString(e));
+        }
+        cudaGetLastError();
+      }
+    }
+  }
+  *out = c;
+  return BLOCH_OK;
+}
+
+int bloch_device_count_of(const bloch_ctx* c, int32_t* n_devices, int32_t* devices) {
+  if (!c || !n_devices) return fail(BLOCH_E_INVALID, "NULL argument");
+  *n_devices = c->subs.empty() ? 1 : static_cast<int32_t>(c->subs.size());
+  if (devices) {
+    if (c->subs.empty())
+      devices[0] = c->device;
+    else
+      for (size_t i = 0; i < c->subs.size(); ++i) devices[i] = c->subs[i]->device;
+  }
+  return BLOCH_OK;
+}
+
+int bloch_last_device_times(const bloch_ctx* c, int32_t capacity, float* kernel_ms, float* device_ms) {
+  if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
+  if (c->subs.empty()) {
+    float k = 0.f, d = 0.f;
+    int32_t l = 0;
+    bloch_last_timing(c, &k, &d, &l);
+    if (capacity >= 1) {
+      if (kernel_ms) kernel_ms[0] = k;
+      if (device_ms) device_ms[0] = d;
+    }
+    return BLOCH_OK;
+  }
+  for (int32_t i = 0; i < capacity && i < static_cast<int32_t>(c->sub_kernel_ms.size()); ++i) {
+    if (kernel_ms) kernel_ms[i] = c->sub_kernel_ms[i];
+    if (device_ms) device_ms[i] = c->sub_device_ms[i];
+  }
+  return BLOCH_OK;
+}
+
 int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double* mx,
                         const double* my, const double* mz, const double* t1, const double* t2,
                         const double* m0, const double* domega, const double* weight,
                         int32_t n_coils, double* echoes_out, double* snaps_out,
                         uint8_t* snap_present, uint32_t flags) {
   if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
+  if (!c->subs.empty()) {
+    if (!c->has_prog) return fail(BLOCH_E_STATE, "bloch_set_tables must be called first");
+    if (n < 0) return fail(BLOCH_E_INVALID, "n < 0");
+    if (n_coils < 1 || n_coils > 8) return fail(BLOCH_E_INVALID, "n_coils must be in [1, 8]");
+    if (n_coils > 1 && !weight) return fail(BLOCH_E_INVALID, "n_coils > 1 requires a weight array");
+    if (n > 0 && (!pos || !mx || !my || !mz || !t1 || !t2 || !m0 || !domega))
+      return fail(BLOCH_E_INVALID, "NULL spin array");
+    if (static_cast<int64_t>(c->prog.n_acq) * c->prog.max_samples > 0 && !echoes_out)
+      return fail(BLOCH_E_INVALID, "echoes_out is NULL");
+    return compute_multi(c, n, pos, mx, my, mz, t1, t2, m0, domega, weight, n_coils, echoes_out, snaps_out,
+                         snap_present, flags);
+  }
   if (!c->has_prog) return fail(BLOCH_E_STATE, "bloch_set_tables must be called first");
   if (c->device == BLOCH_HOST_ONLY) return fail(BLOCH_E_STATE, "host-only context cannot compute");
   if (n < 0) return fail(BLOCH_E_INVALID, "n < 0");
@@ -487,6 +706,7 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
     key.n_coils = n_coils;
     key.flags = flags & ~BLOCH_NO_SYNC;
     key.gen = c->prog_gen;
+    key.alloc = g_alloc_gen.load();
     key.st = c->stream;
   }
   bool capturing = false;
@@ -677,12 +897,14 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
         }
         if (seg_slots > 0) {
           const int64_t* sg = c->d_sample_g.as<int64_t>() + g.sample_begin;
+          const int fold_rows = static_cast<int>(rows);  // every warp's row, in a fixed order
+          const int64_t row_stride = seg_slots * 2;
           if (v.prec == 32)
-            ck(bloch::launch_reduce<float>(c->partial.as<float>(), static_cast<int>(rows), seg_slots, n_coils, ncp,
+            ck(bloch::launch_reduce<float>(c->partial.as<float>(), fold_rows, row_stride, seg_slots, n_coils, ncp,
                                            sg, G, d_echo, st),
                "reduce kernel");
           else
-            ck(bloch::launch_reduce<double>(c->partial.as<double>(), static_cast<int>(rows), seg_slots, n_coils,
+            ck(bloch::launch_reduce<double>(c->partial.as<double>(), fold_rows, row_stride, seg_slots, n_coils,
                                             ncp, sg, G, d_echo, st),
                "reduce kernel");
           c->launches++;
@@ -711,7 +933,10 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       c->graph_launches = c->launches;
       ck(cudaGraphLaunch(c->graph_exec, st), "graph launch");
     }
-    if (graphable) c->last_key = key;
+    if (graphable) {
+      c->last_key = key;
+      c->last_key.alloc = g_alloc_gen.load();  // the buffers this call sized: the next identical call captures
+    }
     if (!(flags & BLOCH_NO_SYNC)) {
       ck(cudaStreamSynchronize(st), "stream sync");
       ck(cudaEventElapsedTime(&kms, c->ev[1], c->ev[2]), "elapsed");
@@ -804,6 +1029,7 @@ int bloch_rasterize(bloch_ctx* c, const bloch_box_t* boxes, int32_t n_boxes, con
 
 int bloch_set_kernel_gate(bloch_ctx* c, void* wait_event, void* signal_event) {
   if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
+  if (!c->subs.empty()) return fail(BLOCH_E_STATE, "not available on a device-set context");
   c->gate_wait = static_cast<cudaEvent_t>(wait_event);
   c->gate_signal = static_cast<cudaEvent_t>(signal_event);
   c->drop_graph();
@@ -813,6 +1039,10 @@ int bloch_set_kernel_gate(bloch_ctx* c, void* wait_event, void* signal_event) {
 int bloch_synchronize(bloch_ctx* c) {
   if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
   if (c->device == BLOCH_HOST_ONLY) return BLOCH_OK;
+  for (bloch_ctx* sub : c->subs) {
+    const int st = bloch_synchronize(sub);
+    if (st != BLOCH_OK) return st;
+  }
   cudaSetDevice(c->device);
   const cudaError_t e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return fail(BLOCH_E_CUDA, std::string("stream sync: ") + cudaGetErrorString(e));

@@ -26,6 +26,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "kernels.h"
 #include "program.h"
 
@@ -108,7 +110,6 @@ struct Strip {
     }
   }
 };
-
 
 // ---------------------------------------------------------------------------
 // spin state (shared memory, [3][S][blockDim] fp64) and per-spin constants
@@ -431,7 +432,6 @@ __device__ __forceinline__ void window_chunk_mc2(float (&ur)[S], float (&ui)[S],
 // fp32 recurrence it replaces.  Lane (g = lane/4, t = lane%4) needs z^g and
 // u z^(8 g) of spin t; it forms them from z by squarings.
 
-constexpr int kMmaMinWindow = 32;  // shorter windows use the recurrence path
 
 struct cf {
   float r, i;
@@ -501,7 +501,7 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1
 // (the swizzle makes both the staging stores and the k-block loads
 // conflict-free), then z^64 per spin.
 constexpr int kStageFloat4 = 8 * 32;
-constexpr int kStageBytes = kStageFloat4 * 16 + 32 * 8 + 32 * 32;  // + z^64 per lane + cp.async slot (Cpre, z: 16 B used of 32)
+constexpr int kStageBytes = kStageFloat4 * 16 + 32 * 8 + 32 * 16;  // + z^64 per lane + cp.async slot (Cpre, z) per lane
 __device__ __forceinline__ int stage_idx(int g, int q) { return g * 32 + (q ^ ((g & 1) << 2)); }
 
 // One lane's spin into the stage: its 8 powers z^g and 8 values u z^(8g).
@@ -600,7 +600,7 @@ __device__ __forceinline__ void mma_round(const float4* __restrict__ st, const f
 template <int NC>
 struct McStage {
   static constexpr int kW = 32 * NC * 8;                            // one weight buffer: [lane spin][coil] float2
-  static constexpr int kBytes = kStageFloat4 * 16 + 2 * kW + 32 * 32;  // + cp.async slot (Cpre, z)
+  static constexpr int kBytes = kStageFloat4 * 16 + 2 * kW + 32 * 16;  // + cp.async slot (Cpre, z) per lane
 };
 
 __device__ __forceinline__ void stage_spin_mc(float4* __restrict__ st, int lane, cf u, cf z) {
@@ -1664,9 +1664,12 @@ __global__ void weights_f32_kernel(int64_t n, int ncp, const double2* __restrict
   }
 }
 
+// fixed-order fp64 fold of `rows` partial rows spaced row_stride elements apart (every warp row, or
+// one folded row per CTA) into the echo layout out[c][sample_g[s]][re, im]
 template <typename R>
-__global__ void reduce_partials_kernel(const R* __restrict__ part, int rows, int64_t n_slots, int nc, int ncp,
-                                       const int64_t* __restrict__ sample_g, int64_t G, double* __restrict__ out) {
+__global__ void reduce_partials_kernel(const R* __restrict__ part, int rows, int64_t row_stride, int64_t n_slots,
+                                       int nc, int ncp, const int64_t* __restrict__ sample_g, int64_t G,
+                                       double* __restrict__ out) {
   const int64_t total = n_slots * 2;
   for (int64_t t = gtid(); t < total; t += gstride()) {
     const int64_t sl = t >> 1;
@@ -1675,7 +1678,7 @@ __global__ void reduce_partials_kernel(const R* __restrict__ part, int rows, int
     const int c = static_cast<int>(sl % ncp);
     if (c >= nc) continue;
     double acc = 0.0;
-    for (int b = 0; b < rows; ++b) acc += static_cast<double>(part[static_cast<int64_t>(b) * total + t]);
+    for (int b = 0; b < rows; ++b) acc += static_cast<double>(part[static_cast<int64_t>(b) * row_stride + t]);
     out[(static_cast<int64_t>(c) * G + sample_g[s]) * 2 + comp] = acc;
   }
 }
@@ -1693,15 +1696,26 @@ size_t integrate_smem_bytes(int threads) {
   return static_cast<size_t>(3 * S * threads) * sizeof(double) + static_cast<size_t>(threads / 32) * stage;
 }
 
+// the opt-in shared-memory limit is a per-device function attribute: track what was allowed per
+// (kernel instance, device), under a lock (contexts on several devices or threads share the instances)
+static std::mutex g_smem_mu;
+
 template <typename R, int S, int NC, bool kFull, int BD>
 static cudaError_t launch_bd(const KParams& kp, int grid, int threads, cudaStream_t stream) {
   const size_t smem = integrate_smem_bytes<R, S, NC>(threads);
-  static size_t smem_set = 48 * 1024;  // raise the opt-in limit only when needed (not inside a graph capture)
-  if (smem > smem_set) {
-    cudaError_t e = cudaFuncSetAttribute(integrate_kernel<R, S, NC, kFull, BD>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    smem_set = smem;
+  static size_t smem_set[kMaxDevices] = {};  // raise the limit only when needed (not inside a graph capture)
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  {
+    std::lock_guard<std::mutex> lk(g_smem_mu);
+    if (smem > 48 * 1024 && smem > smem_set[dev]) {
+      e = cudaFuncSetAttribute(integrate_kernel<R, S, NC, kFull, BD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+      smem_set[dev] = smem;
+    }
   }
   integrate_kernel<R, S, NC, kFull, BD><<<grid, threads, smem, stream>>>(kp);
   return cudaGetLastError();
@@ -1776,14 +1790,28 @@ cudaError_t launch_weights_f32(int64_t n, int ncp, const double* w, float2* out,
   return cudaGetLastError();
 }
 
+__global__ void sum_rows_kernel(const double* __restrict__ rows, int n_rows, int64_t len, double* __restrict__ out) {
+  for (int64_t t = gtid(); t < len; t += gstride()) {
+    double acc = rows[t];
+    for (int r = 1; r < n_rows; ++r) acc += rows[static_cast<int64_t>(r) * len + t];
+    out[t] = acc;
+  }
+}
+
+cudaError_t launch_sum_rows(const double* rows, int n_rows, int64_t len, double* out, cudaStream_t stream) {
+  if (len == 0) return cudaSuccess;
+  sum_rows_kernel<<<grid_for(len, 256), 256, 0, stream>>>(rows, n_rows, len, out);
+  return cudaGetLastError();
+}
+
 template <typename R>
-cudaError_t launch_reduce(const R* part, int rows, int64_t n_slots, int nc, int ncp, const int64_t* sample_g,
-                          int64_t G, double* out, cudaStream_t stream) {
+cudaError_t launch_reduce(const R* part, int rows, int64_t row_stride, int64_t n_slots, int nc, int ncp,
+                          const int64_t* sample_g, int64_t G, double* out, cudaStream_t stream) {
   const int64_t total = n_slots * 2;
   if (total == 0) return cudaSuccess;
   const int64_t blocks = (total + 255) / 256;
   reduce_partials_kernel<R><<<static_cast<int>(blocks < 65535 ? blocks : 65535), 256, 0, stream>>>(
-      part, rows, n_slots, nc, ncp, sample_g, G, out);
+      part, rows, row_stride, n_slots, nc, ncp, sample_g, G, out);
   return cudaGetLastError();
 }
 
@@ -1804,9 +1832,9 @@ cudaError_t kernel_attrs(int* max_threads, int* regs) {
 BLOCH_FOR_EACH_VARIANT(BLOCH_INST)
 #undef BLOCH_INST
 
-template cudaError_t launch_reduce<float>(const float*, int, int64_t, int, int, const int64_t*, int64_t, double*,
-                                          cudaStream_t);
-template cudaError_t launch_reduce<double>(const double*, int, int64_t, int, int, const int64_t*, int64_t, double*,
-                                           cudaStream_t);
+template cudaError_t launch_reduce<float>(const float*, int, int64_t, int64_t, int, int, const int64_t*, int64_t,
+                                          double*, cudaStream_t);
+template cudaError_t launch_reduce<double>(const double*, int, int64_t, int64_t, int, int, const int64_t*, int64_t,
+                                           double*, cudaStream_t);
 
 }  // namespace bloch

@@ -7,6 +7,8 @@
 
 namespace bloch {
 
+constexpr int kMaxDevices = 64;  // per-device launch state (shared-memory opt-in) is kept for this many
+
 // per-spin constants, one 64-byte record (4 x 16-byte loads)
 struct alignas(16) SpinConst {
   double x, y, z, dw;  // position (m), off-resonance (rad/s)
@@ -103,8 +105,10 @@ cudaError_t launch_train_table(int64_t n, int n_cls, const TrainClass* tc, const
 cudaError_t launch_pad_weights(int64_t n, int nc, int ncp, const double* w, double* out,
                                cudaStream_t stream);
 cudaError_t launch_weights_f32(int64_t n, int ncp, const double* w, float2* out, cudaStream_t stream);
+// out[t] = sum_r rows[r * len + t] in rank order (fp64): the device-set context's one reduction
+cudaError_t launch_sum_rows(const double* rows, int n_rows, int64_t len, double* out, cudaStream_t stream);
 template <typename R>
-cudaError_t launch_reduce(const R* part, int grid, int64_t n_slots, int nc, int ncp,
+cudaError_t launch_reduce(const R* part, int rows, int64_t row_stride, int64_t n_slots, int nc, int ncp,
                           const int64_t* sample_g, int64_t G, double* out, cudaStream_t stream);
 
 }  // namespace bloch

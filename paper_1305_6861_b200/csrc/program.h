@@ -146,5 +146,6 @@ constexpr int kChunkSlots = 8;   // ADC slots reduced per warp transpose (sample
 constexpr int kMinWindow = 4;    // shortest uniform run compiled as OP_WINDOW
 constexpr int kMinChirp = 3;     // shortest linear-increment run compiled as OP_CHIRP
 constexpr int kMinTrain = 4;     // shortest pulse+interval run compiled as OP_RFTRAIN
+constexpr int kMmaMinWindow = 32;  // fp32 windows this long run on the tensor cores (shorter: the recurrence)
 
 }  // namespace bloch

@@ -299,15 +299,27 @@ MAX_COILS = 8  # receive coils per device call (bloch_compute_block); more run a
 
 
 class BlochEngine:
-    """One libbloch_b200 context: a CUDA device, a state precision, the uploaded tables."""
+    """One libbloch_b200 context: a CUDA device (or a device set), a state precision, the uploaded tables.
 
-    def __init__(self, device: int = 0, precision: int = 32):
+    ``devices=[d0, d1, ...]`` opens a device-set context (bloch_create_multi): ``compute`` shards the
+    block over the devices with the reference's np.linspace bounds (engine.py:229-251), runs the shards
+    concurrently and sums the partial k-spaces on ``d0`` in rank order — the reference's worker pool
+    (engine.py:540-595) with one GPU per worker."""
+
+    def __init__(self, device: int = 0, precision: int = 32, devices: Optional[List[int]] = None):
         lib = _capi.load()
         self._lib = lib
-        self.device = int(device)
         self.precision = int(precision)
         h = ctypes.c_void_p()
-        _capi.check(lib.bloch_create(self.device, self.precision, ctypes.byref(h)), "bloch_create")
+        if devices is not None and len(devices) > 1:
+            self.devices = [int(d) for d in devices]
+            arr = (ctypes.c_int32 * len(self.devices))(*self.devices)
+            _capi.check(lib.bloch_create_multi(arr, len(self.devices), self.precision, ctypes.byref(h)),
+                        "bloch_create_multi")
+        else:
+            self.devices = [int(devices[0]) if devices else int(device)]
+            _capi.check(lib.bloch_create(self.devices[0], self.precision, ctypes.byref(h)), "bloch_create")
+        self.device = self.devices[0]
         self._h = h
         self._tables_ref = None
         self._flat = None
@@ -365,6 +377,14 @@ class BlochEngine:
         k, d, n = ctypes.c_float(), ctypes.c_float(), ctypes.c_int32()
         _capi.check(self._lib.bloch_last_timing(self._h, ctypes.byref(k), ctypes.byref(d), ctypes.byref(n)), "timing")
         return {"kernel_ms": k.value, "device_ms": d.value, "launches": n.value}
+
+    def device_times(self) -> Dict[int, Dict[str, float]]:
+        """Per-device integrator / whole-call device time (ms) of the last synchronous call, rank order
+        (bloch_last_device_times): the reference's per-worker busy time (engine.py:516-525)."""
+        k = len(self.devices)
+        km, dm = (ctypes.c_float * k)(), (ctypes.c_float * k)()
+        _capi.check(self._lib.bloch_last_device_times(self._h, k, km, dm), "bloch_last_device_times")
+        return {r: {"device": self.devices[r], "kernel_ms": km[r], "device_ms": dm[r]} for r in range(k)}
 
     def last_launch(self) -> Dict[str, int]:
         """Shape of the last integrator launch: precision bits, spins per thread, coil-group width,
@@ -559,21 +579,25 @@ def _unit_weight(wc: np.ndarray, chunk: int = 1 << 15) -> bool:
     return True
 
 
-_ENGINES: Dict[Tuple[int, int], BlochEngine] = {}
+_ENGINES: Dict[Tuple, BlochEngine] = {}
 
 
 def default_device() -> int:
     return int(os.environ.get("LOCAL_RANK", "0"))
 
 
-def get_engine(device: Optional[int] = None, precision: Optional[int] = None) -> BlochEngine:
-    """Process-wide engine per (device, precision); precision from BLOCH_PRECISION (32)."""
-    dev = default_device() if device is None else int(device)
+def get_engine(device: Optional[int] = None, precision: Optional[int] = None,
+               devices: Optional[List[int]] = None) -> BlochEngine:
+    """Process-wide engine per (device or device set, precision); precision from BLOCH_PRECISION (32)."""
     prec = int(os.environ.get("BLOCH_PRECISION", "32")) if precision is None else int(precision)
-    key = (dev, prec)
+    if devices is not None and len(devices) > 1:
+        key = (tuple(int(d) for d in devices), prec)
+    else:
+        dev = int(devices[0]) if devices else (default_device() if device is None else int(device))
+        key = (dev, prec)
     eng = _ENGINES.get(key)
     if eng is None:
-        eng = BlochEngine(dev, prec)
+        eng = BlochEngine(precision=prec, devices=list(key[0]) if isinstance(key[0], tuple) else [key[0]])
         _ENGINES[key] = eng
     return eng
 
@@ -632,6 +656,7 @@ class RunMetrics:
     hardware: str
     kernel_ms: float = 0.0
     events_per_spin: int = 0
+    device_ms: Dict[int, float] = field(default_factory=dict)  # per GPU (rank order), whole-call device time
 
 
 @dataclass
@@ -660,6 +685,14 @@ class Experiment:
     spin_cap: int = DEFAULT_SPIN_CAP
     precision: int = 32
     device: Optional[int] = None
+    devices: Optional[Tuple[int, ...]] = None  # > 1: a device set, the spins sharded over the GPUs
+
+
+def _busy(eng, wall: float) -> Dict[int, float]:
+    """busy_fraction per worker (engine.py:516-525): each GPU's device time over the wall time."""
+    if wall <= 0:
+        return {}
+    return {r: t["device_ms"] / 1e3 / wall for r, t in eng.device_times().items()}
 
 
 def run(exp: Experiment) -> RunResult:
@@ -688,7 +721,7 @@ def run(exp: Experiment) -> RunResult:
         raise InvalidParameter("the phantom rasterized to zero spins")
     arrays = build_spin_arrays(spins, exp.system)
     tables = precompute_sequence_tables(exp.sequence, gamma=exp.system.gamma, snapshot_times=exp.snapshot_times)
-    eng = get_engine(exp.device, exp.precision)
+    eng = get_engine(exp.device, exp.precision, devices=list(exp.devices) if exp.devices else None)
     t_k = time.perf_counter()
     echo_sum, snaps = eng.compute(
         tables, arrays.pos, arrays.mx, arrays.my, arrays.mz, arrays.t1, arrays.t2, arrays.m0, arrays.domega,
@@ -708,9 +741,10 @@ def run(exp: Experiment) -> RunResult:
     timing = eng.last_timing()
     metrics = RunMetrics(
         wall_time_s=wall, spin_count=n_spins, throughput=n_spins / wall if wall > 0 else math.inf,
-        workers=1, blocks=1, busy_fraction={0: busy / wall} if wall > 0 else {},
-        hardware=f"{platform.machine()} cuda:{eng.device} sm_100a", kernel_ms=timing["kernel_ms"],
-        events_per_spin=eng.program_stats()["events"],
+        workers=len(eng.devices), blocks=len(eng.devices), busy_fraction=_busy(eng, wall),
+        hardware=f"{platform.machine()} cuda:{','.join(map(str, eng.devices))} sm_100a", kernel_ms=timing["kernel_ms"],
+        events_per_spin=eng.program_stats()["events"], device_ms={r: t["device_ms"] for r, t in
+                                                                   eng.device_times().items()},
     )
     snapshots = [
         (t, snaps[i] if snaps[i] is not None else np.zeros((0, 3))) for i, t in enumerate(tables.snapshot_times)
@@ -764,9 +798,9 @@ def _run_device_scene(exp: Experiment, spacing, wall_start: float) -> RunResult:
     timing = eng.last_timing()
     metrics = RunMetrics(
         wall_time_s=wall, spin_count=n_spins, throughput=n_spins / wall if wall > 0 else math.inf,
-        workers=1, blocks=1, busy_fraction={0: busy / wall} if wall > 0 else {},
+        workers=1, blocks=1, busy_fraction=_busy(eng, wall),
         hardware=f"{platform.machine()} cuda:{eng.device} sm_100a", kernel_ms=timing["kernel_ms"],
-        events_per_spin=eng.program_stats()["events"],
+        events_per_spin=eng.program_stats()["events"], device_ms={0: timing["device_ms"]},
     )
     snapshots = [(t, snap_host[i] if present[i] else np.zeros((0, 3))) for i, t in enumerate(tables.snapshot_times)]
     return RunResult(echoes=records, metrics=metrics, snapshots=snapshots, spin_count=n_spins, spacing=spacing)

@@ -25,21 +25,49 @@ def test_reference_arm_contract():
     assert d["impl"] == "reference"
     assert d["metric"] == "isochromat-event updates/s" and d["unit"] == d["metric"]
     assert d["value"] > 0 and d["higher_is_better"] is True
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert d["cpu_baseline"]["kind"] in ("port", "reference") and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     assert d["config"]["events_per_spin"] == 4480
+    assert d["n_gpus"] == 1 and d["scaling"] == "strong"
+
+
+def test_spawn_path_runs_one_rank_per_gpu_dry():
+    """`python bench.py --gpus 2` (no torchrun env) re-launches itself with 2 ranks; --dry runs the
+    plumbing (np.linspace shards, one gloo reduce, max-over-ranks time) without a GPU."""
+    d = _run(["--gpus", "2", "--dry", "--config", "0", "--steps", "2", "--warmup", "0", "--quiet"])
+    assert d["n_gpus"] == 2 and d["dry"] is True and d["scaling"] == "strong"
+    assert d["spins_reduced"] == d["config"]["spins_total"] == 2444  # the two shards cover the config once
+    assert d["config"]["parallelism"] == "spin-shards x2"
+
+
+def test_reference_arm_config_dict_matches_ours():
+    """Both arms build their `config` object with the same function from the same workload."""
+    ref = _run(["--impl", "reference", "--gpus", "2", "--config", "0", "--steps", "1", "--warmup", "0",
+                "--cpu-spins-per-core", "8", "--quiet"])
+    ours = _run(["--gpus", "2", "--dry", "--config", "0", "--steps", "1", "--warmup", "0", "--quiet"])
+    assert ref["config"] == ours["config"]
+    assert ref["n_gpus"] == ours["n_gpus"] == 2
+
+
+def test_world_size_mismatch_is_an_error():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry", "--quiet"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert out.returncode != 0 and "WORLD_SIZE" in out.stderr
 
 
 @pytest.mark.gpu
 def test_gpu_arm_contract():
-    d = _run(["--config", "0", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--quiet"])
+    d = _run(["--config", "0", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-per-config",
+              "--no-projection", "--quiet"])
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
               "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
         assert k in d, k
     assert d["steps"] == 3 and d["warmup"] == 3 and d["n_gpus"] == 1
     assert d["value"] > 0 and d["gpu_launches"] >= 3 * 3
     r = d["roofline"]
-    assert r["peak"] > 0 and r["achieved"] > 0 and abs(r["frac"] - r["roofline_ms"] / r["kernel_ms"]) < 1e-9
+    assert r["peak"] > 0 and r["achieved"] > 0 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert abs(r["frac"] - r["tensor_floor_ms"] / r["kernel_ms"]) < 1e-9 and r["model_frac"] > 0
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["config"]["workload"] == "cfg0_se64"

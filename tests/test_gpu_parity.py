@@ -208,6 +208,47 @@ def test_graph_replay_of_repeated_device_calls():
 
 
 @pytest.mark.gpu
+def test_graph_not_replayed_after_buffer_reallocation():
+    """A, A (captured), A (replayed), then B with more spins (the context's scratch buffers grow, i.e. are
+    freed and reallocated), then A again: the graph recorded before the reallocation holds dead pointers
+    and must not be replayed; A's result stays bit-identical throughout."""
+    import torch
+
+    from paper_1305_6861_b200 import configs
+    from paper_1305_6861_b200.engine import BlochEngine
+
+    eng = BlochEngine(0, 32)
+    w = configs.make(0)
+    big = configs.make(1).subset(40)  # ~17k spins: larger than config 0's 2,444
+    dev = torch.device("cuda", 0)
+
+    def dev_ptrs(b):
+        d = {k: torch.from_numpy(np.ascontiguousarray(getattr(b, k), dtype=np.float64)).to(dev)
+             for k in ("pos", "mx", "my", "mz", "t1", "t2", "m0", "domega")}
+        p = {k: v.data_ptr() for k, v in d.items()}
+        p["weight"] = 0
+        return d, p
+
+    t = precompute_sequence_tables(w.sequence)
+    f = eng.set_tables(t)
+    out = torch.zeros(f["n_acq"] * f["max_ns"] * 2, dtype=torch.float64, device=dev)
+    da, pa = dev_ptrs(w.block)
+    db, pb = dev_ptrs(big.block)
+
+    def call(p, n):
+        eng.compute_device(t, p, n, 1, out.data_ptr(), sync=True)
+        return out.cpu().numpy().copy()
+
+    first = call(pa, w.block.n)
+    for _ in range(2):  # second call captured, third replayed
+        assert np.array_equal(call(pa, w.block.n), first)
+    call(pb, big.block.n)  # B: every per-spin scratch buffer grows
+    for _ in range(3):  # A again: re-enqueued, re-captured, replayed — never the stale graph
+        assert np.array_equal(call(pa, w.block.n), first)
+    eng.close()
+
+
+@pytest.mark.gpu
 def test_pipeline_matches_synchronous_compute():
     """Double-buffered Pipeline submissions give the same k-space and final M as synchronous calls."""
     import torch

@@ -145,3 +145,27 @@ def test_oracle_vs_kt_engine():
         spin = np.asarray(e).ravel()[: g[f"seq{i}_kt"].size] / n
         worst = max(worst, np.linalg.norm(spin - g[f"seq{i}_kt"]) / np.linalg.norm(spin))
     assert worst <= 1e-6 and math.isfinite(worst)
+
+
+@pytest.mark.parametrize("index", [1, 3])
+def test_full_size_golden_pinned_by_oracle(index):
+    """The full-size goldens (make_golden_full.py: every spin of the config through the reference's own
+    process pool) agree with the oracle on a sample of their stored final-magnetisation rows, run here
+    through the whole event stream, and carry the config's spin count (the GPU test's reference)."""
+    import os
+
+    path = os.path.join(os.path.dirname(__file__), "golden", f"full_cfg{index}.npz")
+    if not os.path.exists(path):
+        pytest.skip("full-size golden not generated")
+    g = dict(np.load(path))
+    w = configs.make(index)
+    b = w.block
+    assert int(g["n_spins"]) == b.n
+    stride = int(g["m_stride"])
+    rows = np.arange(0, g["m_sub"].shape[0], max(1, g["m_sub"].shape[0] // 24))[:24]
+    idx = rows * stride
+    t = O.precompute_tables(w.sequence, snapshot_times=(float(g["snapshot_time"]),))
+    _, s = O.compute_block(t, b.pos[idx], b.mx[idx], b.my[idx], b.mz[idx], b.t1[idx], b.t2[idx], b.m0[idx],
+                           b.domega[idx], np.asarray(b.weight)[idx])
+    np.testing.assert_allclose(s[0], g["m_sub"][rows], rtol=0, atol=1e-12)
+    assert np.isclose(g["m_sum"].sum(), g["m_sub"].sum() * stride, rtol=0.2)  # the checksum is of the whole array
