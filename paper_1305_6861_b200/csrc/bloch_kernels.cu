@@ -111,6 +111,25 @@ struct Strip {
   }
 };
 
+// L2 priority of the progression running factors (read, advanced and rewritten at every occurrence
+// of the class, ~1000 times per spin on config 2): evict_last keeps the RMW in L2 while the streamed
+// partial rows (evict_first) and the read-only planes pass through; without it the factors were
+// evicted between occurrences and re-fetched from DRAM (ncu: 26 GB of DRAM traffic per launch)
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ double2 ld_keep(const double2* p, uint64_t pol) {
+  double2 v;
+  asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_keep(double2* p, double2 v, uint64_t pol) {
+  asm volatile("st.global.cg.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
+               : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // spin state (shared memory, [3][S][blockDim] fp64) and per-spin constants
 // ---------------------------------------------------------------------------
@@ -654,6 +673,50 @@ __device__ __forceinline__ void mma_round_mc(const float4* __restrict__ st, cons
   }
 }
 
+// Eight coils: the coils go into the MMA's M dimension instead.  For the 8 samples n of MMA m
+// (k = 64 j + 8 m + n) and a k-block of 4 spins,
+//   D[(c, re/im)][n] += sum_s [[Re w_cs, -Im w_cs], [Im w_cs, Re w_cs]] (Re v_sn, Im v_sn),  v_sn = u_s z_s^k
+// so A is the spin's coil weights (prepared once per k-block, shared by the tile's 8 MMAs) and B the
+// per-sample value u z^k, shared by all coils and advanced by z^8 from one MMA to the next — instead
+// of forming and splitting w_c V for every coil of every k-block.  The stage holds (u z^(64 j + g), z^8)
+// per (g, spin): lane (g, t) feeds sample n = g of spin 4 kb + t, and holds coil g of samples 2t, 2t + 1.
+__device__ __forceinline__ void stage_spin_mc8(float4* __restrict__ st, int lane, cf u, cf z) {
+  const cf z8 = csq(csq(csq(z)));
+  cf v = u;
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    st[stage_idx(g, lane)] = make_float4(v.r, v.i, z8.r, z8.i);
+    v = cmul(v, z);
+  }
+}
+
+__device__ __forceinline__ void mma_round_mc8(const float4* __restrict__ st, const float2* __restrict__ wst, int lane,
+                                              float (&acc)[8][4]) {
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll 1
+  for (int kb = 0; kb < 8; ++kb) {
+    const int q = 4 * kb + t;
+    const float4 e = st[stage_idx(g, q)];  // u z^(64 j + g) of spin q, z^8
+    const float2 w = wst[q * 8 + g];        // receive weight of coil g for spin q
+    uint32_t arh, arl, aih, ail;
+    split_tf32(w.x, arh, arl);
+    split_tf32(w.y, aih, ail);
+    const uint32_t naih = aih ^ 0x80000000u, nail = ail ^ 0x80000000u;
+    const uint32_t c0 = pack_bf16(arh, naih), c1 = pack_bf16(aih, arh), c2 = pack_bf16(arl, nail),
+                   c3 = pack_bf16(ail, arl);
+    float2 v = make_float2(e.x, e.y);
+    const float2 nz = make_float2(-e.w, e.z), zz = make_float2(e.z, e.w), m1 = make_float2(-1.f, -1.f);
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const uint32_t brh = __float_as_uint(v.x) & 0xffffe000u, bih = __float_as_uint(v.y) & 0xffffe000u;
+      const float2 lo = __ffma2_rn(make_float2(__uint_as_float(brh), __uint_as_float(bih)), m1, v);
+      mma_tf32(acc[m], arh, aih, naih, arh, brh, bih);
+      mma_bf16(acc[m], c0, c1, c2, c3, pack_bf16(__float_as_uint(lo.x), __float_as_uint(lo.y)), pack_bf16(brh, bih));
+      if (m < 7) v = __ffma2_rn(make_float2(v.y, v.y), nz, __fmul2_rn(make_float2(v.x, v.x), zz));
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // tabulated chirps in the fp32 mode
 // ---------------------------------------------------------------------------
@@ -859,6 +922,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
       } else if (pg >= 0) {  // one member of an interval progression: C, then C *= q^adv
         const int adv = __ldg(&op->flags);  // 0 (last member), 1 or 2
         double2* prun = kp.planes + static_cast<int64_t>(__ldg(&op->pl[0])) * kp.n;
+        const uint64_t l2pol = l2_evict_last();
         const double2 *pq = plane(kp, op, adv == 2 ? 2 : 1), *pab = plane(kp, op, 3);  // q or q^2
 #pragma unroll
         for (int g0 = 0; g0 < S; g0 += G) {
@@ -866,7 +930,7 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
 #pragma unroll
           for (int g = 0; g < G; ++g) {
             const int64_t i = sp.act(g0 + g) ? sp.idx(g0 + g) : 0;
-            c[g] = __ldcg(prun + i);  // running factor: L2-coherent (rewritten below)
+            c[g] = ld_keep(prun + i, l2pol);  // running factor: L2-coherent (rewritten below), kept in L2
             ab[g] = __ldg(pab + i);
             q[g] = adv ? __ldg(pq + i) : make_double2(1.0, 0.0);
           }
@@ -878,8 +942,8 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
             sp.my(s) = c[g].x * y + c[g].y * x;
             sp.mz(s) = fma(sp.mz(s), ab[g].x, ab[g].y);
             if (adv && sp.act(s))
-              __stcg(prun + sp.idx(s), make_double2(c[g].x * q[g].x - c[g].y * q[g].y,
-                                                      c[g].x * q[g].y + c[g].y * q[g].x));
+              st_keep(prun + sp.idx(s), make_double2(c[g].x * q[g].x - c[g].y * q[g].y,
+                                                       c[g].x * q[g].y + c[g].y * q[g].x), l2pol);
           }
         }
       } else {
@@ -1211,16 +1275,31 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
                   sp.mz(r) = fma(sp.mz(r), E.x, c.m0 * (1.0 - E.x));
                 }
               }
-              stage_spin_mc(st, lane, u, z);
-              __syncwarp();
-              mma_round_mc<NC>(st, wbuf + (r & 1) * 32 * NC, lane, acc);
+              if constexpr (NC == 8) {
+                stage_spin_mc8(st, lane, u, z);
+                __syncwarp();
+                mma_round_mc8(st, wbuf + (r & 1) * 32 * NC, lane, acc);
+              } else {
+                stage_spin_mc(st, lane, u, z);
+                __syncwarp();
+                mma_round_mc<NC>(st, wbuf + (r & 1) * 32 * NC, lane, acc);
+              }
               __syncwarp();
             }
-            const int k1 = 64 * j + 16 * t + g, k2 = k1 + 8;
+            if constexpr (NC == 8) {  // acc[m]: coil g of samples 64 j + 8 m + 2 t (+1)
 #pragma unroll
-            for (int c = 0; c < NC; ++c) {
-              if (k1 < cnt) __stcs(out + static_cast<int64_t>(s0 + k1) * NC + c, make_float2(acc[c][0], acc[c][2]));
-              if (k2 < cnt) __stcs(out + static_cast<int64_t>(s0 + k2) * NC + c, make_float2(acc[c][1], acc[c][3]));
+              for (int m = 0; m < 8; ++m) {
+                const int k1 = 64 * j + 8 * m + 2 * t, k2 = k1 + 1;
+                if (k1 < cnt) __stcs(out + static_cast<int64_t>(s0 + k1) * NC + g, make_float2(acc[m][0], acc[m][2]));
+                if (k2 < cnt) __stcs(out + static_cast<int64_t>(s0 + k2) * NC + g, make_float2(acc[m][1], acc[m][3]));
+              }
+            } else {
+              const int k1 = 64 * j + 16 * t + g, k2 = k1 + 8;
+#pragma unroll
+              for (int c = 0; c < NC; ++c) {
+                if (k1 < cnt) __stcs(out + static_cast<int64_t>(s0 + k1) * NC + c, make_float2(acc[c][0], acc[c][2]));
+                if (k2 < cnt) __stcs(out + static_cast<int64_t>(s0 + k2) * NC + c, make_float2(acc[c][1], acc[c][3]));
+              }
             }
           }
           if (tb) {

@@ -80,3 +80,18 @@ def test_kspace_precision_4096(index):
     err_k, err_m = O.rel_l2(o_e, g_e), O.rel_l2(o_s[0], g_s[0])
     print(f"cfg{index}: {sub.n} spins, k-space rel L2 {err_k:.2e}, final M rel L2 {err_m:.2e}")
     assert err_k <= 2e-5 and err_m <= 1e-9
+
+
+@pytest.mark.parametrize("index", [1, 2, 3, 4])
+def test_full_lattice_subset_vs_oracle(index):
+    """bench.py --full-lattice (background PD 0.1, all 1,048,576 lattice sites emit a spin, the count
+    BASELINE.json states): a rasterisation-order subset through the full event stream vs the oracle."""
+    w = configs.make(index, full_lattice=True)
+    assert w.n_spins == 1_048_576
+    b = w.block
+    sub = _sub(b, slice(0, None, b.n // 2048))
+    tables = precompute_sequence_tables(w.sequence, snapshot_times=(w.sequence.end_time,))
+    g_e, g_s = compute_block(tables, sub)
+    ot = O.precompute_tables(w.sequence, snapshot_times=(w.sequence.end_time,))
+    o_e, o_s = O.compute_block(ot, sub.pos, sub.mx, sub.my, sub.mz, sub.t1, sub.t2, sub.m0, sub.domega, sub.weight)
+    assert O.rel_l2(o_e, g_e) <= 2e-5 and O.rel_l2(o_s[0], g_s[0]) <= 1e-9

@@ -4,7 +4,7 @@
 for c in ${CONFIGS:-1}; do
   for r in $(seq ${ROUNDS:-3}); do
     for v in ${VARIANTS:-A B}; do
-      BLOCH_LIB=$PWD/ab/lib$v.so python bench.py --config $c --steps ${STEPS:-10} --warmup 3 --no-cpu-baseline --e2e-steps 1 --quiet \
+      BLOCH_LIB=$PWD/ab/lib$v.so python bench.py --config $c --steps ${STEPS:-10} --warmup 3 --no-cpu-baseline --no-per-config --no-projection --e2e-steps 1 --quiet \
         | python -c "import json,sys; d=json.load(sys.stdin); print('cfg$c $v kernel_ms %.3f' % d['kernel_ms_per_step'])"
     done
   done

@@ -12,7 +12,7 @@
 #include <vector>
 #include <complex>
 
-#include "../../paper_1305_6861_b200/csrc/wgemm.cuh"
+#include "wgemm.cuh"
 
 int main(int argc, char** argv) {
   const int R = argc > 1 ? atoi(argv[1]) : 256, NS = argc > 2 ? atoi(argv[2]) : 256;
