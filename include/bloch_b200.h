@@ -252,6 +252,20 @@ int bloch_last_launch(const bloch_ctx* ctx, int32_t* prec, int32_t* spins_per_th
  * memory and each range's samples folded before the next: the results are bit-identical. */
 int bloch_last_segments(const bloch_ctx* ctx, int32_t* segments);
 
+/* Window contraction (fp32 mode, one receive coil; replaces the per-sample weighted sum of
+ * engine.py:303-305 for long tabulated windows).  The uniform ADC windows of one rotation class
+ * share the per-sample factor z of every spin, so their samples are one complex product over the
+ * spins, S[w][k] = sum_s U[w][s] z_s^k: the integrator stores each window's entry magnetisation U
+ * and the product runs on the tensor cores (tcgen05, TMEM accumulators; three bf16 passes).
+ * `enable` = 0 keeps every window in the integrator (per-warp sums).  Default: enabled. */
+int bloch_set_contraction(bloch_ctx* ctx, int32_t enable);
+
+/* Phases of the last bloch_compute_block (ms, CUDA events): the integrator launches with their
+ * fold, and the window contractions with theirs; the window groups contracted and the samples they
+ * produced (0 when the call ran without the contraction). */
+int bloch_last_phases(const bloch_ctx* ctx, float* integrate_ms, float* contract_ms, int32_t* n_groups,
+                      int64_t* contracted_samples);
+
 
 #ifdef __cplusplus
 }

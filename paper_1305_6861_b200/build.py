@@ -18,8 +18,8 @@ CSRC = os.path.join(HERE, "csrc")
 LIB_NAME = "libbloch_b200.so"
 LIB_PATH = os.path.join(HERE, LIB_NAME)
 
-SOURCES = ["bloch_kernels.cu", "bloch_capi.cu", "program.cpp", "raster_kernels.cu"]
-HEADERS = ["kernels.h", "program.h", "program_host.h", "raster.h"]
+SOURCES = ["bloch_kernels.cu", "bloch_capi.cu", "program.cpp", "raster_kernels.cu", "contract_kernels.cu"]
+HEADERS = ["kernels.h", "program.h", "program_host.h", "raster.h", "contract.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

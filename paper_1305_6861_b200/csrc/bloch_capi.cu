@@ -14,6 +14,7 @@
 #include <string>
 
 #include "../../include/bloch_b200.h"
+#include "contract.h"
 #include "kernels.h"
 #include "program_host.h"
 #include "raster.h"
@@ -83,7 +84,7 @@ struct bloch_ctx {
   int n_sm = 148;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // call start, kernels start/end, call end, integrator end
   bloch::Program prog;
   bool has_prog = false;
   std::vector<uint8_t> snap_present;
@@ -91,6 +92,12 @@ struct bloch_ctx {
   DevBuf in_pos, in_mx, in_my, in_mz, in_t1, in_t2, in_m0, in_dw, in_w;
   DevBuf sc, wpad, w32;
   DevBuf partial, echo, snaps, relax, planetab, planetab32, traintab;
+  // window contraction (contract.h): deferred-window program, U rows, split-K partials
+  DevBuf d_dops, d_dsample_g, d_urow_out0, uhi, ulo, cpart;
+  bool contraction = true;
+  float integrate_ms = 0.f, contract_ms = 0.f;
+  int32_t last_groups = 0;
+  int64_t last_csamples = 0;
 
   DevBuf raster_scratch;
   std::vector<unsigned char> raster_staging;
@@ -160,32 +167,47 @@ int64_t op_samples(const bloch::DevOp& op) {
   }
 }
 
-// Cut the program so that each segment's partial rows (bytes_per_sample per recorded sample) stay
-// within the budget: BLOCH_PARTIAL_BUDGET_MB, default 24 GiB.  Samples are contiguous in op order
-// (compact ids follow the walk), so a segment is an op range plus a sample range.  An op is never
-// split; one op larger than the budget gets a segment of its own.
-std::vector<Segment> plan_segments(const bloch::Program& P, int64_t bytes_per_sample) {
+int64_t partial_budget_bytes() {
   static const int64_t budget = [] {
     const char* e = getenv("BLOCH_PARTIAL_BUDGET_MB");
     const double mb = e ? atof(e) : 24.0 * 1024.0;
     return std::max<int64_t>(1, static_cast<int64_t>(mb * 1048576.0));
   }();
+  return budget;
+}
+
+// integrator / contraction split of the last call's kernel time (events 1 -> 4 -> 2)
+void phase_times(bloch_ctx* c) {
+  float a = 0.f, b = 0.f;
+  if (cudaEventElapsedTime(&a, c->ev[1], c->ev[4]) != cudaSuccess) a = 0.f;
+  if (cudaEventElapsedTime(&b, c->ev[4], c->ev[2]) != cudaSuccess) b = 0.f;
+  cudaGetLastError();
+  c->integrate_ms = a;
+  c->contract_ms = c->last_groups > 0 ? b : 0.f;
+}
+
+// Cut the program so that each segment's partial rows (bytes_per_sample per recorded sample) stay
+// within the budget: BLOCH_PARTIAL_BUDGET_MB, default 24 GiB.  Samples are contiguous in op order
+// (compact ids follow the walk), so a segment is an op range plus a sample range.  An op is never
+// split; one op larger than the budget gets a segment of its own.
+std::vector<Segment> plan_segments(const std::vector<bloch::DevOp>& ops, int64_t bytes_per_sample) {
+  const int64_t budget = partial_budget_bytes();
   const int64_t cap = std::max<int64_t>(1, budget / std::max<int64_t>(1, bytes_per_sample));
   std::vector<Segment> segs;
   Segment cur{0, 0, 0, 0};
   int64_t next_sample = 0;
-  for (int32_t o = 0; o < static_cast<int32_t>(P.ops.size()); ++o) {
-    const int64_t k = op_samples(P.ops[o]);
+  for (int32_t o = 0; o < static_cast<int32_t>(ops.size()); ++o) {
+    const int64_t k = op_samples(ops[o]);
     if (k > 0 && cur.n_samples > 0 && cur.n_samples + k > cap) {
       cur.op_end = o;
       segs.push_back(cur);
       cur = Segment{o, o, next_sample, 0};
     }
-    if (k > 0 && cur.n_samples == 0) cur.sample_begin = P.ops[o].s0;
+    if (k > 0 && cur.n_samples == 0) cur.sample_begin = ops[o].s0;
     cur.n_samples += k;
     next_sample = cur.sample_begin + cur.n_samples;
   }
-  cur.op_end = static_cast<int32_t>(P.ops.size());
+  cur.op_end = static_cast<int32_t>(ops.size());
   segs.push_back(cur);
   return segs;
 }
@@ -372,7 +394,8 @@ int bloch_destroy(bloch_ctx* c) {
   c->drop_graph();
   for (DevBuf* b : {&c->d_ops, &c->d_gev, &c->d_mats, &c->d_sample_g, &c->d_relax_t, &c->relax, &c->d_planes, &c->planetab, &c->planetab32, &c->in_pos, &c->in_mx, &c->in_my, &c->in_mz,
                     &c->in_t1, &c->in_t2, &c->in_m0, &c->in_dw, &c->in_w, &c->sc, &c->wpad, &c->w32, &c->partial,
-                    &c->echo, &c->snaps, &c->d_train_cls, &c->traintab, &c->state, 
+                    &c->echo, &c->snaps, &c->d_train_cls, &c->traintab, &c->state, &c->d_dops, &c->d_dsample_g,
+                    &c->d_urow_out0, &c->uhi, &c->ulo, &c->cpart,
                     &c->raster_scratch})
     b->release();
   for (auto& ev : c->ev)
@@ -437,6 +460,9 @@ int bloch_set_tables(bloch_ctx* c, int32_t n_es, const int64_t* es_ev_offset,
       upload(c->d_train_cls, prog.train_classes.data(), prog.train_classes.size() * sizeof(bloch::TrainClass),
              c->stream);
       upload(c->d_sample_g, prog.sample_g.data(), prog.sample_g.size() * sizeof(int64_t), c->stream);
+      upload(c->d_dops, prog.dops.data(), prog.dops.size() * sizeof(bloch::DevOp), c->stream);
+      upload(c->d_dsample_g, prog.dsample_g.data(), prog.dsample_g.size() * sizeof(int64_t), c->stream);
+      upload(c->d_urow_out0, prog.urow_out0.data(), prog.urow_out0.size() * sizeof(int64_t), c->stream);
       ck(cudaStreamSynchronize(c->stream), "set_tables sync");
     }
     c->snap_present.assign(static_cast<size_t>(n_snap), 0);
@@ -720,6 +746,7 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
         ck(cudaStreamSynchronize(st), "stream sync");
         ck(cudaEventElapsedTime(&c->kernel_ms, c->ev[1], c->ev[2]), "elapsed");
         ck(cudaEventElapsedTime(&c->device_ms, c->ev[0], c->ev[3]), "elapsed");
+        phase_times(c);
       }
       if (snap_present)
         for (int32_t i = 0; i < P.n_snap; ++i) snap_present[i] = c->snap_present[i];
@@ -815,13 +842,21 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
     }
     // 4. integrator + ordered fold
     float kms = 0.f;
+    c->last_groups = 0;
+    c->last_csamples = 0;
     if (n > 0) {
+      // the window contraction: fp32 mode, one receive coil, U rows within the partial budget
+      const int64_t urows = static_cast<int64_t>(P.urow_out0.size());
+      const int64_t uwords = bloch::contract_u_words(urows, n);
+      const bool defer = c->contraction && c->precision == BLOCH_PREC_F32 && n_coils == 1 && !P.groups.empty() &&
+                         2 * uwords * 4 <= partial_budget_bytes();
+      const std::vector<bloch::DevOp>& OPS = defer ? P.dops : P.ops;
       int max_window = 0;
-      for (const bloch::DevOp& op : P.ops)
+      for (const bloch::DevOp& op : OPS)
         if (op.kind == bloch::OP_WINDOW) max_window = std::max(max_window, static_cast<int>(op.count));
       Variant v = pick_variant(c->precision, n, ncp, c->n_sm, max_window);
       v.full = false;
-      for (const bloch::DevOp& op : P.ops)
+      for (const bloch::DevOp& op : OPS)
         if (op.kind == bloch::OP_RFTRAIN || op.kind == bloch::OP_CHIRP || op.kind == bloch::OP_GSAMP) v.full = true;
       int max_t = 512, min_b = 1;
       variant_shape(v, &max_t, &min_b);
@@ -844,7 +879,7 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       // acquisition on a large block can exceed the device.  The op stream is cut into segments
       // whose samples fit the budget; each runs as its own launch (state handed over in fp64
       // through global memory, bit-identical to one launch) followed by the fold of its samples.
-      const std::vector<Segment> segs = plan_segments(P, rows * ncp * 2 * static_cast<int64_t>(rsz));
+      const std::vector<Segment> segs = plan_segments(OPS, rows * ncp * 2 * static_cast<int64_t>(rsz));
       int64_t max_seg_slots = 1;
       for (const Segment& g : segs) max_seg_slots = std::max<int64_t>(max_seg_slots, g.n_samples * ncp);
       c->partial.ensure(static_cast<size_t>(rows * max_seg_slots * 2) * rsz);
@@ -852,9 +887,32 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       if (segs.size() > 1) {
         c->state.ensure(static_cast<size_t>(6) * nd);  // two ping-pong (mx, my, mz) sets
       }
+      // contraction buffers (sized before any capture: the first call of a shape allocates)
+      std::vector<bloch::ContractPlan> cplans;
+      if (defer) {
+        c->uhi.ensure(static_cast<size_t>(uwords) * 4);
+        c->ulo.ensure(static_cast<size_t>(uwords) * 4);
+        size_t cb = 0;
+        for (const bloch::WinGroup& g : P.groups) {
+          cplans.push_back(bloch::contract_plan(g.count, g.n_windows, n, c->n_sm));
+          bloch::ContractJob j0{};
+          j0.W = g.n_windows;
+          j0.K = g.count;
+          cb = std::max(cb, bloch::contract_part_bytes(cplans.back(), j0));
+        }
+        c->cpart.ensure(cb);
+      }
       bloch::KParams kp{};
-      kp.ops = c->d_ops.as<bloch::DevOp>();
-      kp.n_ops = static_cast<int32_t>(P.ops.size());
+      kp.ops = defer ? c->d_dops.as<bloch::DevOp>() : c->d_ops.as<bloch::DevOp>();
+      kp.n_ops = static_cast<int32_t>(OPS.size());
+      kp.uhi = defer ? c->uhi.as<uint32_t>() : nullptr;
+      kp.ulo = defer ? c->ulo.as<uint32_t>() : nullptr;
+      kp.urows = urows;
+      if (defer && (n & 15)) {  // the last 16-spin block's padding words: zero (the product reads them)
+        const size_t off = static_cast<size_t>(n / 16) * urows * 16 * 4, len = static_cast<size_t>(urows) * 16 * 4;
+        ck(cudaMemsetAsync(c->uhi.as<char>() + off, 0, len, st), "memset U");
+        ck(cudaMemsetAsync(c->ulo.as<char>() + off, 0, len, st), "memset U");
+      }
       kp.spins_per_cta = static_cast<int32_t>(spc);
       kp.gev = c->d_gev.as<bloch::GEv>();
       kp.mats = c->d_mats.as<double>();
@@ -890,13 +948,13 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
         kp.mz1 = hand_over ? state + (k & 1) * 3 * n + 2 * n : nullptr;
         ck(dispatch(v, kp, static_cast<int>(grid), static_cast<int>(threads), st), "integrate kernel");
         c->launches++;
-        if (!hand_over) {  // after the last integrator launch (the fold of its samples follows)
+        if (!hand_over && !defer) {  // after the last integrator launch (the fold of its samples follows)
           if (c->gate_signal) ck(cudaEventRecord(c->gate_signal, st), "gate signal");
           ck(cudaEventRecordWithFlags(c->ev[2], st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault),
              "event");
         }
         if (seg_slots > 0) {
-          const int64_t* sg = c->d_sample_g.as<int64_t>() + g.sample_begin;
+          const int64_t* sg = (defer ? c->d_dsample_g : c->d_sample_g).as<int64_t>() + g.sample_begin;
           const int fold_rows = static_cast<int>(rows);  // every warp's row, in a fixed order
           const int64_t row_stride = seg_slots * 2;
           if (v.prec == 32)
@@ -910,11 +968,43 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
           c->launches++;
         }
       }
+      ck(cudaEventRecordWithFlags(c->ev[4], st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault), "event");
+      if (defer) {  // 5. the window groups on the tensor cores (every U row is written: the last segment ran)
+        for (size_t gi = 0; gi < P.groups.size(); ++gi) {
+          const bloch::WinGroup& g = P.groups[gi];
+          const bloch::PlaneDesc& zd = P.planes[g.zplane];
+          bloch::ContractJob j{};
+          j.sc = c->sc.as<bloch::SpinConst>();
+          j.n = n;
+          j.T = zd.T;
+          j.d[0] = zd.d[0];
+          j.d[1] = zd.d[1];
+          j.d[2] = zd.d[2];
+          j.tw = zd.tw;
+          j.K = g.count;
+          j.W = g.n_windows;
+          j.row0 = g.row0;
+          j.uhi = c->uhi.as<uint32_t>();
+          j.ulo = c->ulo.as<uint32_t>();
+          j.rows = urows;
+          j.part = c->cpart.as<float>();
+          j.out0 = c->d_urow_out0.as<int64_t>() + g.row0;
+          j.echo = d_echo;
+          ck(bloch::launch_contract(j, cplans[gi], st), "contraction kernel");
+          c->launches += 2;
+        }
+        c->last_groups = static_cast<int32_t>(P.groups.size());
+        c->last_csamples = P.n_deferred_samples;
+        if (c->gate_signal) ck(cudaEventRecord(c->gate_signal, st), "gate signal");
+        ck(cudaEventRecordWithFlags(c->ev[2], st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault),
+           "event");
+      }
     } else {
       ck(cudaEventRecordWithFlags(c->ev[1], st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault), "event");
       ck(cudaEventRecordWithFlags(c->ev[2], st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault), "event");
+      ck(cudaEventRecordWithFlags(c->ev[4], st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault), "event");
     }
-    // 5. outputs to the host
+    // 6. outputs to the host
     if (!out_dev) {
       if (echo_bytes) ck(cudaMemcpyAsync(echoes_out, d_echo, echo_bytes, cudaMemcpyDeviceToHost, st), "D2H echoes");
       if (d_snap) ck(cudaMemcpyAsync(snaps_out, d_snap, snap_bytes, cudaMemcpyDeviceToHost, st), "D2H snapshots");
@@ -942,6 +1032,7 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       ck(cudaEventElapsedTime(&kms, c->ev[1], c->ev[2]), "elapsed");
       c->kernel_ms = kms;
       ck(cudaEventElapsedTime(&c->device_ms, c->ev[0], c->ev[3]), "elapsed");
+      phase_times(c);
     }
     if (snap_present)
       for (int32_t i = 0; i < P.n_snap; ++i) snap_present[i] = c->snap_present[i];
@@ -952,6 +1043,25 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
     if (capturing) abandon_capture(c);
     return fail(BLOCH_E_CUDA, ex.what());
   }
+  return BLOCH_OK;
+}
+
+int bloch_set_contraction(bloch_ctx* c, int32_t enable) {
+  if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
+  c->contraction = enable != 0;
+  for (bloch_ctx* sub : c->subs) sub->contraction = enable != 0;
+  c->drop_graph();
+  return BLOCH_OK;
+}
+
+int bloch_last_phases(const bloch_ctx* c, float* integrate_ms, float* contract_ms, int32_t* n_groups,
+                      int64_t* contracted_samples) {
+  if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
+  const bloch_ctx* s = c->subs.empty() ? c : c->subs[0];
+  if (integrate_ms) *integrate_ms = s->integrate_ms;
+  if (contract_ms) *contract_ms = s->contract_ms;
+  if (n_groups) *n_groups = s->last_groups;
+  if (contracted_samples) *contracted_samples = s->last_csamples;
   return BLOCH_OK;
 }
 

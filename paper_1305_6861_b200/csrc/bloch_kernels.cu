@@ -28,6 +28,7 @@
 
 #include <mutex>
 
+#include "contract.h"
 #include "kernels.h"
 #include "program.h"
 
@@ -959,6 +960,57 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
           q[0] = sp.mx(s);
           q[1] = sp.my(s);
           q[2] = sp.mz(s);
+        }
+      }
+      continue;
+    }
+
+    if (kind == OP_UWIN) {  // deferred window (contract.h): store u for the contraction, apply the exit
+      const int lead = __ldg(&op->aux), pre = __ldg(&op->pre);
+      if constexpr (!kFull) {
+        if (pre >= 0) apply_pre<S>(kp, sp, pre, __ldg(&op->tmode));
+      }
+      const int64_t row = __ldg(&op->s0);
+      const double2 *pc = plane(kp, op, 2), *pab = plane(kp, op, 3);
+      const int pcp = __ldg(&op->pl[0]), pz = __ldg(&op->pl[1]);
+      constexpr int G = S < 4 ? S : 4;
+#pragma unroll
+      for (int g0 = 0; g0 < S; g0 += G) {
+        double2 c[G], ab[G], cp[G], zz[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const int64_t i = sp.act(g0 + g) ? sp.idx(g0 + g) : 0;
+          c[g] = __ldg(pc + i);
+          ab[g] = __ldg(pab + i);
+          if constexpr (sizeof(R) == 4) {  // Cpre and z are PL_SAMPLE planes: float2 in the fp32 mode
+            const float2 a = __ldg(plane32_at(kp, pcp, i)), b = __ldg(plane32_at(kp, pz, i));
+            cp[g] = make_double2(a.x, a.y);
+            zz[g] = make_double2(b.x, b.y);
+          } else {
+            cp[g] = __ldg(plane_at(kp, pcp, i));
+            zz[g] = __ldg(plane_at(kp, pz, i));
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const int s = g0 + g;
+          const double x = sp.mx(s), y = sp.my(s);
+          if (sp.act(s)) {
+            double ur = cp[g].x * x - cp[g].y * y, ui = cp[g].x * y + cp[g].y * x;
+            if (!lead) {  // the first sample follows one interval
+              const double t = ur * zz[g].x - ui * zz[g].y;
+              ui = ur * zz[g].y + ui * zz[g].x;
+              ur = t;
+            }
+            uint32_t hi, lo;
+            contract_split(ur, ui, hi, lo);
+            const int64_t q = contract_u_index(kp.urows, row, sp.idx(s));
+            __stcs(kp.uhi + q, hi);  // streamed: read back by the contraction
+            __stcs(kp.ulo + q, lo);
+          }
+          sp.mx(s) = c[g].x * x - c[g].y * y;
+          sp.my(s) = c[g].x * y + c[g].y * x;
+          sp.mz(s) = fma(sp.mz(s), ab[g].x, ab[g].y);
         }
       }
       continue;

@@ -1,0 +1,463 @@
+// The ADC window contraction on tcgen05 (contract.h): warp-specialised, one CTA per SM.
+//
+//   warp 0     TMA producer: the U tile of each 16-spin stage (hi and lo, SWIZZLE_64B) -> smem
+//   warp 1     TMEM owner; lane 0 issues the MMAs (3 bf16 passes per 16-element K step) and
+//              commits each stage back to its producers
+//   warps 2-5  generate the A tile of each stage (z^k of 16 spins for the CTA's samples, split
+//              into bf16 hi/lo, real-embedded, written in the SWIZZLE_64B layout the MMA reads),
+//              then read the accumulators out of TMEM into the split-K partial rows
+//
+// Pipelines: full_u (TMA tx bytes), full_z (4 generator-warp arrivals) -> MMA -> empty
+// (tcgen05.commit) -> producers; acc_full (final commit) -> epilogue.  No CTA barrier inside
+// the stage loop.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <mutex>
+#include <string>
+
+#include "contract.h"
+
+namespace bloch {
+namespace ct {
+
+constexpr int kGenWarps = 8;               // A generators (and accumulator drains)
+constexpr int kThreads = 64 + 32 * kGenWarps;
+constexpr int kStageSpins = 16;            // K = 32 bf16 = 64 B per operand row (one SWIZZLE_64B row)
+constexpr int kRowBytes = 64;
+constexpr int kTileBytes = 128 * kRowBytes;  // one 128-row operand tile: 8 KB
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.b32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+// K-major SWIZZLE_64B operand: 64-B rows, 8-row groups 512 B apart (SBO), sm_100 descriptor version 1
+__device__ __forceinline__ uint64_t sw64_desc(uint32_t addr) {
+  return static_cast<uint64_t>((addr >> 4) & 0x3fff) | (static_cast<uint64_t>(1) << 16) |
+         (static_cast<uint64_t>(512 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) | (static_cast<uint64_t>(4) << 61);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ double reduce_2pi(double th) {
+  const double k = rint(th * 0.15915494309189535);
+  return fma(-k, 2.4492935982947064e-16, fma(-k, 6.283185307179586, th));
+}
+// z^m = exp(-m a) exp(-i m th), fp64 phase reduction, fp32 result
+__device__ __forceinline__ float2 zpow(double th, double a, int m) {
+  const float ph = static_cast<float>(reduce_2pi(static_cast<double>(m) * th));
+  const float amp = __expf(-static_cast<float>(static_cast<double>(m) * a));
+  float s, c;
+  __sincosf(ph, &s, &c);
+  return make_float2(amp * c, -amp * s);
+}
+// bf16 hi part (round to nearest: Veltkamp split keeping 8 significant bits) and the residual
+__device__ __forceinline__ void split_bf16(float x, float& hi, float& lo) {
+  const float c = __fmul_rn(x, 65537.0f);
+  hi = __fsub_rn(c, __fsub_rn(c, x));
+  lo = __fsub_rn(x, hi);
+}
+__device__ __forceinline__ uint32_t pack2(float lo_elem, float hi_elem) {  // bf16x2: (element 2s, element 2s+1)
+  return __byte_perm(__float_as_uint(lo_elem), __float_as_uint(hi_elem), 0x7632);
+}
+
+}  // namespace ct
+
+template <int MT>
+__global__ void __launch_bounds__(ct::kThreads, 1)
+    contract_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo,
+                    const ContractJob j, const ContractPlan p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-B aligned base (the swizzle pattern is anchored on 512-B boundaries); derived from smem_raw so
+  // that the stores below stay STS
+  unsigned char* smem = smem_raw + ((1024u - (ct::smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = p.nw, depth = p.depth;
+  const int a_bytes = MT * ct::kTileBytes;           // one of A hi / A lo
+  const int b_bytes = nw * ct::kRowBytes;            // one of B hi / B lo
+  const int stage_bytes = 2 * a_bytes + 2 * b_bytes;
+  auto A = [&](int s, int part) { return smem + s * stage_bytes + part * a_bytes; };
+  auto B = [&](int s, int part) { return smem + s * stage_bytes + 2 * a_bytes + part * b_bytes; };
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + depth * stage_bytes);
+  uint64_t* full_u = bars;
+  uint64_t* full_z = bars + depth;
+  uint64_t* empty = bars + 2 * depth;
+  uint64_t* acc_full = bars + 3 * depth;   // MMA -> drain: a segment's accumulation is complete
+  uint64_t* acc_empty = bars + 3 * depth + 1;  // drain -> MMA: the accumulator has been read out
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * depth + 2);
+
+  const int tk = blockIdx.x % p.tiles_k;
+  const int rest = blockIdx.x / p.tiles_k;
+  const int tw = rest % p.tiles_w, kc = rest / p.tiles_w;
+  const int k0 = tk * 64 * MT, w0 = tw * nw;
+  const int64_t total_st = (j.n + ct::kStageSpins - 1) / ct::kStageSpins;
+  const int64_t st0 = static_cast<int64_t>(kc) * p.stages;
+  const int nst = static_cast<int>(min(static_cast<int64_t>(p.stages), total_st - st0));
+  const int seg = p.seg;
+  auto seg_end = [&](int e) { return min((e + 1) * seg, nst) - 1; };  // last stage of segment e
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < depth; ++s) {
+      ct::mbar_init(full_u + s, 1);
+      ct::mbar_init(full_z + s, ct::kGenWarps);
+      ct::mbar_init(empty + s, 1);
+    }
+    ct::mbar_init(acc_full, 1);
+    ct::mbar_init(acc_empty, ct::kGenWarps);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ct::smem_u32(tmem_slot)),
+                 "r"(p.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&map_hi) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&map_lo) : "memory");
+      for (int t = 0; t < nst; ++t) {
+        const int s = t % depth;
+        if (t >= depth) ct::mbar_wait(empty + s, ((t / depth) - 1) & 1);
+        ct::mbar_expect_tx(full_u + s, 2u * static_cast<uint32_t>(b_bytes));
+        const int blk = static_cast<int>(st0 + t);  // 16-spin block = stage
+        ct::tma_load_3d(B(s, 0), &map_hi, full_u + s, 0, j.row0 + w0, blk);
+        ct::tma_load_3d(B(s, 1), &map_lo, full_u + s, 0, j.row0 + w0, blk);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(nw >> 3) << 17) |
+                             (static_cast<uint32_t>(128 >> 4) << 24);
+      for (int t = 0; t < nst; ++t) {
+        const int s = t % depth;
+        const uint32_t ph = (t / depth) & 1;
+        const int e = t / seg;
+        const bool first = t == e * seg;  // a segment starts: overwrite the accumulator
+        if (first && e > 0) ct::mbar_wait(acc_empty, (e - 1) & 1);  // segment e-1 has been read out
+        ct::mbar_wait(full_u + s, ph);
+        ct::mbar_wait(full_z + s, ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t bh = ct::smem_u32(B(s, 0)), bl = ct::smem_u32(B(s, 1));
+        if (!(p.dbg & 2)) {
+#pragma unroll
+          for (int m = 0; m < MT; ++m) {
+            const uint32_t ah = ct::smem_u32(A(s, 0)) + m * ct::kTileBytes, al = ct::smem_u32(A(s, 1)) + m * ct::kTileBytes;
+            const uint32_t d = tmem + static_cast<uint32_t>(m * nw);
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {  // two K steps of 16 bf16 (32 B) per 64-B row
+              const uint32_t o = ks * 32;
+              const uint32_t acc = (!first || ks > 0) ? 1u : 0u;
+              ct::mma_bf16(d, ct::sw64_desc(ah + o), ct::sw64_desc(bh + o), idesc, acc);
+              ct::mma_bf16(d, ct::sw64_desc(ah + o), ct::sw64_desc(bl + o), idesc, 1u);
+              ct::mma_bf16(d, ct::sw64_desc(al + o), ct::sw64_desc(bh + o), idesc, 1u);
+            }
+          }
+        }
+        ct::mma_commit(empty + s);
+        if (t == seg_end(e)) ct::mma_commit(acc_full);
+      }
+    }
+  } else {
+    // ---- generators: warp q owns samples [8 MT q, 8 MT (q+1)) of the tile, lanes 0-15 the even ones
+    // and lanes 16-31 the odd ones (of spin lane & 15), so one STS.32 of the warp covers two rows 64 B
+    // apart in bank space: conflict-free in the swizzled layout
+    const int q = warp - 2, half = lane >> 4, sl = lane & 15;
+    constexpr int kSamp = 64 * MT / ct::kGenWarps;  // samples per warp per stage
+    constexpr int kVals = kSamp / 2;                // per lane
+    const int m = (kSamp * q) >> 6;
+    const int rr0 = ((kSamp * q) & 63) + half;
+    const int kfirst = k0 + kSamp * q + half;  // absolute sample of value 0
+    const uint32_t off0 = m * ct::kTileBytes + 128 * rr0 + ((sl & 3) << 2);
+    const uint32_t ch_e = (((sl >> 2) ^ half) << 4), ch_o = (((sl >> 2) ^ (half ^ 2)) << 4);
+    // ---- drain of accumulation segment e: TMEM lanes of this warp's quarter (two warps per quarter,
+    // half of the columns each) -> partial slot (chunk, e); the MMA of the next segment waits for the
+    // generator warps' acc_empty arrivals
+    const int quarter = warp & 3, colh = q >> 2;
+    const int row = 32 * quarter + lane;  // accumulator row: sample k0 + 64 m + row / 2, component row & 1
+    auto drain = [&](int e) {
+      ct::mbar_wait(acc_full, e & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      float* slot = j.part + (static_cast<int64_t>(kc) * p.segs + e) * j.W * j.K * 2;
+      for (int mm = 0; mm < MT; ++mm) {
+        const int k = k0 + 64 * mm + (row >> 1);
+        for (int c0 = 16 * colh; c0 < nw; c0 += 32) {
+          uint32_t r[16];
+          const uint32_t addr = tmem + (static_cast<uint32_t>(32 * quarter) << 16) + static_cast<uint32_t>(mm * nw + c0);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+              : "r"(addr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (k < j.K) {
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+              const int w = w0 + c0 + c;
+              if (w < j.W) slot[(static_cast<int64_t>(w) * j.K + k) * 2 + (row & 1)] = __uint_as_float(r[c]);
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) ct::mbar_arrive(acc_empty);
+    };
+    // per-spin constants of the next stage are loaded one stage ahead
+    auto load_sc = [&](int t, double2& a, double2& b, double2& c) {
+      const int64_t i = (st0 + t) * ct::kStageSpins + sl;
+      if (t < nst && i < j.n) {
+        const double2* pc = reinterpret_cast<const double2*>(j.sc + i);
+        a = __ldg(pc);      // (x, y)
+        b = __ldg(pc + 1);  // (z, dw)
+        c = __ldg(pc + 3);  // (r2, pad)
+      } else {
+        a = b = c = make_double2(0.0, 0.0);
+      }
+    };
+    double2 na, nb, nc;
+    load_sc(0, na, nb, nc);
+    int e_next = 0;  // next segment to drain
+    for (int t = 0; t < nst; ++t) {
+      const double2 ca = na, cb = nb, cc = nc;
+      load_sc(t + 1, na, nb, nc);
+      const int s = t % depth;
+      if (t >= depth) {
+        ct::mbar_wait(empty + s, ((t / depth) - 1) & 1);
+        // stage t - depth completed: when it closed a segment, read that accumulator out now
+        // (the MMA has the next depth - 1 stages in hand while it waits)
+        if (t - depth == seg_end(e_next)) drain(e_next++);
+      }
+      if (p.dbg & 1) {
+        __syncwarp();
+        if (lane == 0) ct::mbar_arrive(full_z + s);
+        continue;
+      }
+      float2 P = make_float2(0.f, 0.f), Q = make_float2(0.f, 0.f);
+      if ((st0 + t) * ct::kStageSpins + sl < j.n) {
+        const double th = fma(cb.x, j.d[2], fma(ca.y, j.d[1], ca.x * j.d[0])) + cb.y * j.tw;
+        const double a = j.T != 0.0 ? j.T * cc.x : 0.0;  // as plane_kernel: no decay without duration
+        P = ct::zpow(th, a, kfirst);
+        Q = ct::zpow(th, a, 2);
+      }
+      unsigned char* ah = A(s, 0);
+      unsigned char* ae = ah + off0 + ch_e;
+      unsigned char* ao = ah + off0 + ch_o;
+#pragma unroll
+      for (int v = 0; v < kVals; ++v) {
+        // bf16 hi parts rounded to nearest (Veltkamp, both components packed) and the residuals
+        // (scalar __fmul_rn: never contracted into the following subtraction, which would void the split)
+        const float2 c = make_float2(__fmul_rn(P.x, 65537.0f), __fmul_rn(P.y, 65537.0f));
+        const float2 d = __fadd2_rn(c, make_float2(-P.x, -P.y));
+        const float2 hi = __fadd2_rn(c, make_float2(-d.x, -d.y));
+        const float2 lo = __fadd2_rn(P, make_float2(-hi.x, -hi.y));
+        unsigned char* o = ((v & 1) ? ao : ae) + 256 * v;
+        // row (k, re) = [Re z^k, -Im z^k], row (k, im) = [Im z^k, Re z^k]
+        *reinterpret_cast<uint32_t*>(o) = ct::pack2(hi.x, -hi.y);
+        *reinterpret_cast<uint32_t*>(o + 64) = ct::pack2(hi.y, hi.x);
+        *reinterpret_cast<uint32_t*>(o + a_bytes) = ct::pack2(lo.x, -lo.y);
+        *reinterpret_cast<uint32_t*>(o + a_bytes + 64) = ct::pack2(lo.y, lo.x);
+        const float nx = P.x * Q.x - P.y * Q.y;
+        P.y = P.x * Q.y + P.y * Q.x;
+        P.x = nx;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) ct::mbar_arrive(full_z + s);
+    }
+    while (e_next * seg < nst) drain(e_next++);  // the remaining segments
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols) : "memory");
+}
+
+// fixed-order fp64 fold of the partial slots (spin chunk major, segment minor) into the echo array
+// (stored, not added); chunk c holds ceil(stages_c / seg) segments
+__global__ void contract_fold_kernel(const float* __restrict__ part, int chunks, int segs, int seg, int stages,
+                                     int64_t total_st, int W, int K, const int64_t* __restrict__ out0,
+                                     double* __restrict__ echo) {
+  const int64_t per = static_cast<int64_t>(W) * K * 2;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < per;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t w = t / (2 * K), r = t - w * 2 * K;
+    double acc = 0.0;
+    for (int c = 0; c < chunks; ++c) {
+      const int64_t nst = min(static_cast<int64_t>(stages), total_st - static_cast<int64_t>(c) * stages);
+      const int ns = static_cast<int>((nst + seg - 1) / seg);
+      for (int e = 0; e < ns; ++e) acc += static_cast<double>(part[(static_cast<int64_t>(c) * segs + e) * per + t]);
+    }
+    echo[(out0[w] + (r >> 1)) * 2 + (r & 1)] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+
+ContractPlan contract_plan(int K, int W, int64_t n, int n_sm) {
+  ContractPlan p{};
+  p.nw = ((W + 15) / 16) * 16;
+  if (p.nw > 256) p.nw = 256;
+  if (p.nw < 16) p.nw = 16;
+  const int ktiles64 = (K + 63) / 64;
+  p.mt = 1;
+  for (int m : {4, 2}) {
+    if (m * p.nw <= 512 && m <= ktiles64) {
+      p.mt = m;
+      break;
+    }
+  }
+  p.tmem_cols = 32;
+  while (p.tmem_cols < p.mt * p.nw) p.tmem_cols <<= 1;
+  const int stage = 2 * p.mt * ct::kTileBytes + 2 * p.nw * ct::kRowBytes;
+  const int budget = 227 * 1024 - 1024 - 256;  // alignment slack, barriers
+  p.depth = budget / stage;
+  if (p.depth > 4) p.depth = 4;
+  if (p.depth < 2) p.depth = 2;
+  p.smem = p.depth * stage + 1024 + 256;
+  p.dbg = 0;
+  p.tiles_k = (K + 64 * p.mt - 1) / (64 * p.mt);
+  p.tiles_w = (W + p.nw - 1) / p.nw;
+  const int64_t total_st = (n + ct::kStageSpins - 1) / ct::kStageSpins;
+  int64_t chunks = n_sm / (p.tiles_k * p.tiles_w);
+  if (chunks < 1) chunks = 1;
+  if (chunks > total_st) chunks = total_st > 0 ? total_st : 1;
+  const int64_t per = (total_st + chunks - 1) / chunks;
+  p.stages = static_cast<int>(per > 0 ? per : 1);
+  p.chunks = static_cast<int>((total_st + p.stages - 1) / p.stages);
+  if (p.chunks < 1) p.chunks = 1;
+  // accumulation segments: at most kMaxSegs per chunk (partial volume), at least kSegStages stages each
+  constexpr int kSegStages = 128, kMaxSegs = 8;
+  static const int seg_env = [] {
+    const char* e = getenv("BLOCH_CONTRACT_SEG");
+    return e ? atoi(e) : 0;
+  }();
+  p.seg = seg_env > 0 ? seg_env : std::max(kSegStages, (p.stages + kMaxSegs - 1) / kMaxSegs);
+  p.segs = (p.stages + p.seg - 1) / p.seg;
+  return p;
+}
+
+size_t contract_part_bytes(const ContractPlan& p, const ContractJob& j) {
+  return static_cast<size_t>(p.chunks) * p.segs * j.W * j.K * 2 * sizeof(float);
+}
+
+namespace {
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+cudaError_t make_map(CUtensorMap* m, const uint32_t* base, const ContractJob& j, int nw) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  // [block][row][32 bf16]: one 64-B row per (block, window)
+  const cuuint64_t dims[3] = {32, static_cast<cuuint64_t>(j.rows), static_cast<cuuint64_t>((j.n + 15) / 16)};
+  const cuuint64_t strides[2] = {64, static_cast<cuuint64_t>(j.rows) * 64};
+  const cuuint32_t box[3] = {32, static_cast<cuuint32_t>(nw), 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<uint32_t*>(base), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+std::mutex g_contract_mu;
+
+template <int MT>
+cudaError_t launch_mt(const CUtensorMap& mh, const CUtensorMap& ml, const ContractJob& j, const ContractPlan& p,
+                      cudaStream_t st) {
+  static int smem_set[kMaxDevices] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  {
+    std::lock_guard<std::mutex> lk(g_contract_mu);
+    if (p.smem > smem_set[dev]) {
+      e = cudaFuncSetAttribute(contract_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem);
+      if (e != cudaSuccess) return e;
+      smem_set[dev] = p.smem;
+    }
+  }
+  const int grid = p.tiles_k * p.tiles_w * p.chunks;
+  contract_kernel<MT><<<grid, ct::kThreads, p.smem, st>>>(mh, ml, j, p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_contract(const ContractJob& j, const ContractPlan& p, cudaStream_t st) {
+  if (j.n <= 0 || j.W <= 0 || j.K <= 0) return cudaSuccess;
+  CUtensorMap mh, ml;
+  cudaError_t e = make_map(&mh, j.uhi, j, p.nw);
+  if (e == cudaSuccess) e = make_map(&ml, j.ulo, j, p.nw);
+  if (e != cudaSuccess) return e;
+  switch (p.mt) {
+    case 4: e = launch_mt<4>(mh, ml, j, p, st); break;
+    case 2: e = launch_mt<2>(mh, ml, j, p, st); break;
+    default: e = launch_mt<1>(mh, ml, j, p, st); break;
+  }
+  if (e != cudaSuccess) return e;
+  const int64_t per = static_cast<int64_t>(j.W) * j.K * 2;
+  const int64_t blocks = (per + 255) / 256;
+  const int64_t total_st = (j.n + ct::kStageSpins - 1) / ct::kStageSpins;
+  contract_fold_kernel<<<static_cast<int>(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(
+      j.part, p.chunks, p.segs, p.seg, p.stages, total_st, j.W, j.K, j.out0, j.echo);
+  return cudaGetLastError();
+}
+
+}  // namespace bloch

@@ -38,6 +38,9 @@ struct KParams {
   const float2* planes32;        // fp32 mode: [n_planes][n] float2 copies of the PL_SAMPLE planes (same ids)
   const double* train;           // [n_train][n][12]: train-class affine propagators (train_table_kernel)
   const float2* w32;             // fp32 multi-coil weights, spin-major [n][NC] (tensor-core windows), or nullptr
+  uint32_t* uhi;                 // OP_UWIN: U of bf16x2 (Re, Im) words, hi part (contract.h, contract_u_index)
+  uint32_t* ulo;                 //          lo part
+  int64_t urows;                 //          U rows
 };
 
 // Launch shape per variant: max threads per CTA and min resident CTAs per SM

@@ -56,6 +56,7 @@ void find_chirp_classes(Program& prog);
 void fuse_pulses(Program& prog);
 void find_train_classes(Program& prog);
 void assign_planes(Program& prog);
+void defer_windows(Program& prog);
 
 void compile_program(const TablesView& t, Program& prog) {
   prog = Program();
@@ -487,6 +488,61 @@ void fuse_intervals(Program& prog, const std::function<int32_t(double)>& relax_c
   find_train_classes(prog);
   fuse_pulses(prog);
   assign_planes(prog);
+  defer_windows(prog);
+}
+
+// The deferred-window view (program.h OP_UWIN, contract.h): every tabulated window of at least
+// kMinDeferWindow samples is grouped by (z plane, sample count); its samples are then formed by one
+// tensor-core product per group instead of per-warp sums in the integrator.  U rows are numbered group
+// by group, in op order inside a group.  The remaining sampled ops keep their samples under new
+// compact ids (dsample_g), so the integrator's partial rows only hold those.
+void defer_windows(Program& prog) {
+  prog.dops.clear();
+  prog.dsample_g.clear();
+  prog.groups.clear();
+  prog.urow_out0.clear();
+  prog.n_deferred_samples = 0;
+  std::map<std::pair<int32_t, int32_t>, int32_t> gid;
+  std::vector<std::vector<size_t>> members;
+  for (size_t k = 0; k < prog.ops.size(); ++k) {
+    const DevOp& op = prog.ops[k];
+    if (op.kind != OP_WINDOW || op.rot < 0 || op.count < kMinDeferWindow) continue;
+    const auto key = std::make_pair(op.pl[1], op.count);
+    auto f = gid.find(key);
+    if (f == gid.end()) {
+      f = gid.emplace(key, static_cast<int32_t>(prog.groups.size())).first;
+      prog.groups.push_back(WinGroup{op.pl[1], op.count, 0, 0});
+      members.emplace_back();
+    }
+    members[f->second].push_back(k);
+  }
+  std::vector<int32_t> row_of(prog.ops.size(), -1);
+  int32_t row = 0;
+  for (size_t g = 0; g < prog.groups.size(); ++g) {
+    prog.groups[g].row0 = row;
+    prog.groups[g].n_windows = static_cast<int32_t>(members[g].size());
+    for (size_t k : members[g]) {
+      const DevOp& op = prog.ops[k];
+      const int64_t first = prog.sample_g[op.s0];
+      for (int32_t q = 1; q < op.count; ++q)
+        if (prog.sample_g[op.s0 + q] != first + q) throw std::logic_error("window samples not contiguous");
+      prog.urow_out0.push_back(first);
+      prog.n_deferred_samples += op.count;
+      row_of[k] = row++;
+    }
+  }
+  for (size_t k = 0; k < prog.ops.size(); ++k) {
+    DevOp op = prog.ops[k];
+    if (row_of[k] >= 0) {
+      op.kind = OP_UWIN;
+      op.s0 = row_of[k];
+    } else if (op.kind == OP_WINDOW || op.kind == OP_CHIRP || op.kind == OP_GSAMP) {
+      const int32_t s0 = static_cast<int32_t>(prog.dsample_g.size());
+      for (int32_t q = 0; q < op.count; ++q) prog.dsample_g.push_back(prog.sample_g[op.s0 + q]);
+      op.s0 = s0;
+    }
+    prog.dops.push_back(op);
+  }
 }
 
 // A hard pulse followed by an interval or a window is applied by that op

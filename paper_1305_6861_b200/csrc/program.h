@@ -37,7 +37,11 @@
 
 namespace bloch {
 
-enum OpKind : int32_t { OP_ROT = 1, OP_EVENT = 2, OP_GSAMP = 3, OP_WINDOW = 4, OP_CHIRP = 5, OP_RFTRAIN = 6 };
+enum OpKind : int32_t { OP_ROT = 1, OP_EVENT = 2, OP_GSAMP = 3, OP_WINDOW = 4, OP_CHIRP = 5, OP_RFTRAIN = 6, OP_UWIN = 7 };
+// OP_UWIN (the deferred-window program, Program::dops): a tabulated OP_WINDOW whose samples are formed
+// afterwards by the tensor-core contraction (contract.h).  The integrator stores the window's entry
+// magnetisation u = Cpre m (times z without a leading no-op sample) as bf16 hi/lo words in U row `s0`
+// and applies the window's exit propagator (C, (A, B)); `aux`, `pre`, `tmode`, `rot`, `pl` as OP_WINDOW.
 
 // flags of an interval (OP_EVENT.count, GEv.flags)
 enum : int32_t { EV_MOVE = 1, EV_RELAX = 2 };
@@ -147,5 +151,15 @@ constexpr int kMinWindow = 4;    // shortest uniform run compiled as OP_WINDOW
 constexpr int kMinChirp = 3;     // shortest linear-increment run compiled as OP_CHIRP
 constexpr int kMinTrain = 4;     // shortest pulse+interval run compiled as OP_RFTRAIN
 constexpr int kMmaMinWindow = 32;  // fp32 windows this long run on the tensor cores (shorter: the recurrence)
+constexpr int kMinDeferWindow = 16;  // tabulated windows this long are deferred to the contraction (OP_UWIN)
+
+// The windows of one rotation class (same z plane, same sample count) contracted as one product
+// (contract.h): U rows [row0, row0 + n_windows) in op order.
+struct WinGroup {
+  int32_t zplane;     // plane id of the per-sample factor z
+  int32_t count;      // samples per window
+  int32_t row0;       // first U row
+  int32_t n_windows;  // windows (U rows)
+};
 
 }  // namespace bloch

@@ -39,6 +39,13 @@ struct Program {
   int64_t n_chirp_ops = 0, n_chirp_samples = 0, n_train_ops = 0, n_train_pairs = 0;
   int64_t n_fused_windows = 0, n_fused_intervals = 0, n_prog_intervals = 0, n_fused_pulses = 0;
   int64_t n_train_class_ops = 0;  // RF trains applied from the train table
+  // deferred-window view of the same program (defer_windows): tabulated windows of >= kMinDeferWindow
+  // samples become OP_UWIN; every other sampled op keeps its samples, renumbered compactly (dsample_g)
+  std::vector<DevOp> dops;
+  std::vector<int64_t> dsample_g;
+  std::vector<WinGroup> groups;
+  std::vector<int64_t> urow_out0;  // per U row: output index (acq * max_samples + first sample)
+  int64_t n_deferred_samples = 0;
 };
 
 // Throws std::invalid_argument on malformed tables.

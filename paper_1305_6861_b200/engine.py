@@ -400,6 +400,20 @@ class BlochEngine:
         _capi.check(self._lib.bloch_last_segments(self._h, ctypes.byref(v)), "bloch_last_segments")
         return v.value
 
+    def set_contraction(self, enable: bool) -> None:
+        """Window contraction on the tensor cores (bloch_set_contraction; fp32 mode, one coil): the long
+        tabulated ADC windows of a rotation class form one product over spins instead of per-warp sums
+        (replaces engine.py:303-305 for those windows).  On by default."""
+        _capi.check(self._lib.bloch_set_contraction(self._h, 1 if enable else 0), "bloch_set_contraction")
+
+    def last_phases(self) -> Dict[str, float]:
+        """Integrator vs window-contraction device time (ms) of the last call, the window groups
+        contracted and the samples they produced (bloch_last_phases)."""
+        a, b, g, k = ctypes.c_float(), ctypes.c_float(), ctypes.c_int32(), ctypes.c_int64()
+        _capi.check(self._lib.bloch_last_phases(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(g),
+                                                ctypes.byref(k)), "bloch_last_phases")
+        return {"integrate_ms": a.value, "contract_ms": b.value, "groups": g.value, "contracted_samples": k.value}
+
     def set_stream(self, stream_ptr: int) -> None:
         """Run on an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream); 0 = own stream."""
         _capi.check(self._lib.bloch_set_stream(self._h, ctypes.c_void_p(int(stream_ptr) or None)), "bloch_set_stream")

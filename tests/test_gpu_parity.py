@@ -294,3 +294,38 @@ def test_more_coils_than_one_call_takes(precision):
     for a, r in zip(s, ref_s):
         if r is not None:
             assert rel_l2(r, a) <= STATE_TOL[precision]
+
+
+# --- the window contraction (contract.h) and the integrator's own window sums, both against the goldens ---
+
+
+@pytest.mark.parametrize("name", SMALL + CONFIGS)
+def test_gpu_window_sums_without_contraction(name):
+    """fp32 mode with the contraction switched off: every window summed by the integrator's warps."""
+    from paper_1305_6861_b200.engine import get_engine
+
+    rec = load_golden(name)
+    eng = get_engine(0, 32)
+    eng.set_contraction(False)
+    try:
+        echoes, snaps = compute_block(_tables(name, rec), _block(rec), precision=32)
+        assert eng.last_phases()["groups"] == 0
+    finally:
+        eng.set_contraction(True)
+    err = echo_error(rec, echoes)
+    assert err <= KSPACE_TOL[32], f"{name} k-space rel L2 {err:.3e}"
+    for i, e in enumerate(snapshot_errors(rec, snaps)):
+        assert e <= STATE_TOL[32], f"{name} snapshot {i} rel L2 {e:.3e}"
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "se16_box", "tse16", "epi16"])
+def test_gpu_contraction_runs_and_matches(name):
+    """The long tabulated windows of these programs go through the tensor-core contraction."""
+    from paper_1305_6861_b200.engine import get_engine
+
+    rec = load_golden(name)
+    eng = get_engine(0, 32)
+    echoes, _ = compute_block(_tables(name, rec), _block(rec), precision=32)
+    ph = eng.last_phases()
+    assert ph["groups"] >= 1 and ph["contracted_samples"] > 0, ph
+    assert echo_error(rec, echoes) <= KSPACE_TOL[32]
