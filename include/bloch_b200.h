@@ -260,6 +260,11 @@ int bloch_last_segments(const bloch_ctx* ctx, int32_t* segments);
  * `enable` = 0 keeps every window in the integrator (per-warp sums).  Default: enabled. */
 int bloch_set_contraction(bloch_ctx* ctx, int32_t enable);
 
+/* The compiled program's window groups (one contraction each), the samples they produce and the
+ * samples the integrator still sums itself when the contraction runs (host-only contexts too). */
+int bloch_program_groups(const bloch_ctx* ctx, int32_t* n_groups, int64_t* contracted_samples,
+                         int64_t* integrator_samples);
+
 /* Phases of the last bloch_compute_block (ms, CUDA events): the integrator launches with their
  * fold, and the window contractions with theirs; the window groups contracted and the samples they
  * produced (0 when the call ran without the contraction). */

@@ -93,7 +93,7 @@ struct bloch_ctx {
   DevBuf sc, wpad, w32;
   DevBuf partial, echo, snaps, relax, planetab, planetab32, traintab;
   // window contraction (contract.h): deferred-window program, U rows, split-K partials
-  DevBuf d_dops, d_dsample_g, d_urow_out0, uhi, ulo, cpart;
+  DevBuf d_dops, d_dsample_g, d_urow_out0, uhi, ulo, cpart, ztab, zqtab;
   bool contraction = true;
   float integrate_ms = 0.f, contract_ms = 0.f;
   int32_t last_groups = 0;
@@ -395,7 +395,7 @@ int bloch_destroy(bloch_ctx* c) {
   for (DevBuf* b : {&c->d_ops, &c->d_gev, &c->d_mats, &c->d_sample_g, &c->d_relax_t, &c->relax, &c->d_planes, &c->planetab, &c->planetab32, &c->in_pos, &c->in_mx, &c->in_my, &c->in_mz,
                     &c->in_t1, &c->in_t2, &c->in_m0, &c->in_dw, &c->in_w, &c->sc, &c->wpad, &c->w32, &c->partial,
                     &c->echo, &c->snaps, &c->d_train_cls, &c->traintab, &c->state, &c->d_dops, &c->d_dsample_g,
-                    &c->d_urow_out0, &c->uhi, &c->ulo, &c->cpart,
+                    &c->d_urow_out0, &c->uhi, &c->ulo, &c->cpart, &c->ztab, &c->zqtab,
                     &c->raster_scratch})
     b->release();
   for (auto& ev : c->ev)
@@ -901,6 +901,8 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
           cb = std::max(cb, bloch::contract_part_bytes(cplans.back(), j0));
         }
         c->cpart.ensure(cb);
+        c->ztab.ensure(static_cast<size_t>(n) * sizeof(float4));
+        c->zqtab.ensure(static_cast<size_t>(n) * sizeof(float2));
       }
       bloch::KParams kp{};
       kp.ops = defer ? c->d_dops.as<bloch::DevOp>() : c->d_ops.as<bloch::DevOp>();
@@ -990,8 +992,10 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
           j.part = c->cpart.as<float>();
           j.out0 = c->d_urow_out0.as<int64_t>() + g.row0;
           j.echo = d_echo;
+          j.zt = c->ztab.as<float4>();
+          j.zq = c->zqtab.as<float2>();
           ck(bloch::launch_contract(j, cplans[gi], st), "contraction kernel");
-          c->launches += 2;
+          c->launches += 3;
         }
         c->last_groups = static_cast<int32_t>(P.groups.size());
         c->last_csamples = P.n_deferred_samples;
@@ -1051,6 +1055,16 @@ int bloch_set_contraction(bloch_ctx* c, int32_t enable) {
   c->contraction = enable != 0;
   for (bloch_ctx* sub : c->subs) sub->contraction = enable != 0;
   c->drop_graph();
+  return BLOCH_OK;
+}
+
+int bloch_program_groups(const bloch_ctx* c, int32_t* n_groups, int64_t* contracted_samples,
+                         int64_t* integrator_samples) {
+  if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
+  if (!c->has_prog) return fail(BLOCH_E_STATE, "no tables uploaded");
+  if (n_groups) *n_groups = static_cast<int32_t>(c->prog.groups.size());
+  if (contracted_samples) *contracted_samples = c->prog.n_deferred_samples;
+  if (integrator_samples) *integrator_samples = static_cast<int64_t>(c->prog.dsample_g.size());
   return BLOCH_OK;
 }
 

@@ -47,7 +47,11 @@ struct ContractJob {
   float* part;          // [chunks * segs][W][K][2] partial sums per (spin chunk, accumulation segment)
   const int64_t* out0;  // [W] complex index (coil 0) of each window's first sample in the echo array
   double* echo;         // echo array (complex128), samples stored
+  float4* zt;           // [n] scratch: per-spin (theta_hi, theta_lo, a, 0), theta = phase per sample mod 2 pi
+  float2* zq;           // [n] scratch: per-spin z^2
 };
+
+constexpr int kContractMaxSamples = 4096;  // windows up to this long (the fp32 phase k theta_hi is exact)
 
 struct ContractPlan {
   int mt;          // 64-sample M-tiles per CTA (1, 2, 4)

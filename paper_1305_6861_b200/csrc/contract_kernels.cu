@@ -78,13 +78,18 @@ __device__ __forceinline__ double reduce_2pi(double th) {
   const double k = rint(th * 0.15915494309189535);
   return fma(-k, 2.4492935982947064e-16, fma(-k, 6.283185307179586, th));
 }
-// z^m = exp(-m a) exp(-i m th), fp64 phase reduction, fp32 result
-__device__ __forceinline__ float2 zpow(double th, double a, int m) {
-  const float ph = static_cast<float>(reduce_2pi(static_cast<double>(m) * th));
-  const float amp = __expf(-static_cast<float>(static_cast<double>(m) * a));
-  float s, c;
-  __sincosf(ph, &s, &c);
-  return make_float2(amp * c, -amp * s);
+// z^k = exp(-k a) exp(-i k theta) in fp32 from the tabulated (theta_hi, theta_lo, a): theta_hi has 12
+// significant bits, so k theta_hi is exact for k < 4096; the 2 pi reduction is exact up to 2pi_lo
+__device__ __forceinline__ float2 zpow32(float4 t, float k) {
+  const float p = k * t.x;
+  const float nn = __fadd_rn(__fmaf_rn(p, 0.15915494309189535f, 12582912.0f), -12582912.0f);  // rint(p / 2 pi)
+  float r = __fmaf_rn(-nn, 6.28125f, p);                   // exact: nn and 6.28125 are short
+  r = __fmaf_rn(-nn, 0.0019353071795864769f, r);           // 2 pi - 6.28125
+  r = __fmaf_rn(k, t.y, r);
+  float sn, cs;
+  __sincosf(r, &sn, &cs);
+  const float amp = __expf(-k * t.z);
+  return make_float2(amp * cs, -amp * sn);
 }
 // bf16 hi part (round to nearest: Veltkamp split keeping 8 significant bits) and the residual
 __device__ __forceinline__ void split_bf16(float x, float& hi, float& lo) {
@@ -210,6 +215,7 @@ __global__ void __launch_bounds__(ct::kThreads, 1)
     const int kfirst = k0 + kSamp * q + half;  // absolute sample of value 0
     const uint32_t off0 = m * ct::kTileBytes + 128 * rr0 + ((sl & 3) << 2);
     const uint32_t ch_e = (((sl >> 2) ^ half) << 4), ch_o = (((sl >> 2) ^ (half ^ 2)) << 4);
+    const uint32_t sw = half ? 64u : 0u;  // offset of this half's first store (the im row for the odd half)
     // ---- drain of accumulation segment e: TMEM lanes of this warp's quarter (two warps per quarter,
     // half of the columns each) -> partial slot (chunk, e); the MMA of the next segment waits for the
     // generator warps' acc_empty arrivals
@@ -243,24 +249,26 @@ __global__ void __launch_bounds__(ct::kThreads, 1)
       __syncwarp();
       if (lane == 0) ct::mbar_arrive(acc_empty);
     };
-    // per-spin constants of the next stage are loaded one stage ahead
-    auto load_sc = [&](int t, double2& a, double2& b, double2& c) {
+    // per-spin phase tables of the next stage are loaded one stage ahead
+    auto load_z = [&](int t, float4& zt, float2& zq) {
       const int64_t i = (st0 + t) * ct::kStageSpins + sl;
       if (t < nst && i < j.n) {
-        const double2* pc = reinterpret_cast<const double2*>(j.sc + i);
-        a = __ldg(pc);      // (x, y)
-        b = __ldg(pc + 1);  // (z, dw)
-        c = __ldg(pc + 3);  // (r2, pad)
+        zt = __ldg(j.zt + i);
+        zq = __ldg(j.zq + i);
       } else {
-        a = b = c = make_double2(0.0, 0.0);
+        zt = make_float4(0.f, 0.f, 0.f, 0.f);
+        zq = make_float2(0.f, 0.f);
       }
     };
-    double2 na, nb, nc;
-    load_sc(0, na, nb, nc);
+    float4 nzt;
+    float2 nzq;
+    load_z(0, nzt, nzq);
+    const float kf = static_cast<float>(kfirst);
     int e_next = 0;  // next segment to drain
     for (int t = 0; t < nst; ++t) {
-      const double2 ca = na, cb = nb, cc = nc;
-      load_sc(t + 1, na, nb, nc);
+      const float4 czt = nzt;
+      const float2 czq = nzq;
+      load_z(t + 1, nzt, nzq);
       const int s = t % depth;
       if (t >= depth) {
         ct::mbar_wait(empty + s, ((t / depth) - 1) & 1);
@@ -275,10 +283,8 @@ __global__ void __launch_bounds__(ct::kThreads, 1)
       }
       float2 P = make_float2(0.f, 0.f), Q = make_float2(0.f, 0.f);
       if ((st0 + t) * ct::kStageSpins + sl < j.n) {
-        const double th = fma(cb.x, j.d[2], fma(ca.y, j.d[1], ca.x * j.d[0])) + cb.y * j.tw;
-        const double a = j.T != 0.0 ? j.T * cc.x : 0.0;  // as plane_kernel: no decay without duration
-        P = ct::zpow(th, a, kfirst);
-        Q = ct::zpow(th, a, 2);
+        P = ct::zpow32(czt, kf);
+        Q = czq;
       }
       unsigned char* ah = A(s, 0);
       unsigned char* ae = ah + off0 + ch_e;
@@ -292,11 +298,14 @@ __global__ void __launch_bounds__(ct::kThreads, 1)
         const float2 hi = __fadd2_rn(c, make_float2(-d.x, -d.y));
         const float2 lo = __fadd2_rn(P, make_float2(-hi.x, -hi.y));
         unsigned char* o = ((v & 1) ? ao : ae) + 256 * v;
-        // row (k, re) = [Re z^k, -Im z^k], row (k, im) = [Im z^k, Re z^k]
-        *reinterpret_cast<uint32_t*>(o) = ct::pack2(hi.x, -hi.y);
-        *reinterpret_cast<uint32_t*>(o + 64) = ct::pack2(hi.y, hi.x);
-        *reinterpret_cast<uint32_t*>(o + a_bytes) = ct::pack2(lo.x, -lo.y);
-        *reinterpret_cast<uint32_t*>(o + a_bytes + 64) = ct::pack2(lo.y, lo.x);
+        // row (k, re) = [Re z^k, -Im z^k], row (k, im) = [Im z^k, Re z^k]; the odd half-warp stores
+        // its im row first, so each STS covers banks 0-15 with one half and 16-31 with the other
+        const uint32_t hre = ct::pack2(hi.x, -hi.y), him = ct::pack2(hi.y, hi.x);
+        const uint32_t lre = ct::pack2(lo.x, -lo.y), lim = ct::pack2(lo.y, lo.x);
+        *reinterpret_cast<uint32_t*>(o + sw) = half ? him : hre;
+        *reinterpret_cast<uint32_t*>(o + (64 - sw)) = half ? hre : him;
+        *reinterpret_cast<uint32_t*>(o + a_bytes + sw) = half ? lim : lre;
+        *reinterpret_cast<uint32_t*>(o + a_bytes + (64 - sw)) = half ? lre : lim;
         const float nx = P.x * Q.x - P.y * Q.y;
         P.y = P.x * Q.y + P.y * Q.x;
         P.x = nx;
@@ -311,6 +320,26 @@ __global__ void __launch_bounds__(ct::kThreads, 1)
   __syncthreads();
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols) : "memory");
+}
+
+// per-spin phase tables of one job (fp64 in, fp32 out): theta = pos . d + dw tw (plane_kernel's
+// expression) reduced mod 2 pi and split into a 12-significant-bit head and the rest; a = T r2;
+// z^2 = exp(-2 a) exp(-2 i theta)
+__global__ void contract_prep_kernel(const SpinConst* __restrict__ sc, int64_t n, double T, double d0, double d1,
+                                     double d2, double tw, float4* __restrict__ zt, float2* __restrict__ zq) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const SpinConst c = sc[i];
+    const double th = ct::reduce_2pi(fma(c.z, d2, fma(c.y, d1, c.x * d0)) + c.dw * tw);
+    const float hi = __uint_as_float(__float_as_uint(static_cast<float>(th)) & 0xfffff000u);
+    const float lo = static_cast<float>(th - static_cast<double>(hi));
+    const double a = T != 0.0 ? T * c.r2 : 0.0;  // as plane_kernel: no decay without duration
+    zt[i] = make_float4(hi, lo, static_cast<float>(a), 0.f);
+    double s2, c2;
+    sincos(ct::reduce_2pi(2.0 * th), &s2, &c2);
+    const double e2 = exp(-2.0 * a);
+    zq[i] = make_float2(static_cast<float>(e2 * c2), static_cast<float>(-e2 * s2));
+  }
 }
 
 // fixed-order fp64 fold of the partial slots (spin chunk major, segment minor) into the echo array
@@ -442,6 +471,12 @@ cudaError_t launch_mt(const CUtensorMap& mh, const CUtensorMap& ml, const Contra
 
 cudaError_t launch_contract(const ContractJob& j, const ContractPlan& p, cudaStream_t st) {
   if (j.n <= 0 || j.W <= 0 || j.K <= 0) return cudaSuccess;
+  if (j.K > kContractMaxSamples) return cudaErrorInvalidValue;
+  {
+    const int64_t blocks = (j.n + 255) / 256;
+    contract_prep_kernel<<<static_cast<int>(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(
+        j.sc, j.n, j.T, j.d[0], j.d[1], j.d[2], j.tw, j.zt, j.zq);
+  }
   CUtensorMap mh, ml;
   cudaError_t e = make_map(&mh, j.uhi, j, p.nw);
   if (e == cudaSuccess) e = make_map(&ml, j.ulo, j, p.nw);

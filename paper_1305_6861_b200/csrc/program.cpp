@@ -506,7 +506,7 @@ void defer_windows(Program& prog) {
   std::vector<std::vector<size_t>> members;
   for (size_t k = 0; k < prog.ops.size(); ++k) {
     const DevOp& op = prog.ops[k];
-    if (op.kind != OP_WINDOW || op.rot < 0 || op.count < kMinDeferWindow) continue;
+    if (op.kind != OP_WINDOW || op.rot < 0 || op.count < kMinDeferWindow || op.count > kMaxDeferWindow) continue;
     const auto key = std::make_pair(op.pl[1], op.count);
     auto f = gid.find(key);
     if (f == gid.end()) {

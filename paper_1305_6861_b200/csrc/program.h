@@ -151,7 +151,8 @@ constexpr int kMinWindow = 4;    // shortest uniform run compiled as OP_WINDOW
 constexpr int kMinChirp = 3;     // shortest linear-increment run compiled as OP_CHIRP
 constexpr int kMinTrain = 4;     // shortest pulse+interval run compiled as OP_RFTRAIN
 constexpr int kMmaMinWindow = 32;  // fp32 windows this long run on the tensor cores (shorter: the recurrence)
-constexpr int kMinDeferWindow = 16;  // tabulated windows this long are deferred to the contraction (OP_UWIN)
+constexpr int kMinDeferWindow = 16;    // tabulated windows this long are deferred to the contraction (OP_UWIN)
+constexpr int kMaxDeferWindow = 4096;  // ... up to this long (contract.h kContractMaxSamples)
 
 // The windows of one rotation class (same z plane, same sample count) contracted as one product
 // (contract.h): U rows [row0, row0 + n_windows) in op order.

@@ -371,6 +371,10 @@ class BlochEngine:
         _capi.check(self._lib.bloch_program_classes(self._h, *[ctypes.byref(v) for v in cls]), "bloch_program_classes")
         out.update(zip(("prog_classes", "chirp_classes", "train_classes", "train_class_ops", "planes"),
                        (v.value for v in cls)))
+        g, cs, rs = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()
+        _capi.check(self._lib.bloch_program_groups(self._h, ctypes.byref(g), ctypes.byref(cs), ctypes.byref(rs)),
+                    "bloch_program_groups")
+        out.update(window_groups=g.value, contracted_samples=cs.value, integrator_samples=rs.value)
         return out
 
     def last_timing(self) -> Dict[str, float]:

@@ -80,6 +80,20 @@ def test_compile_configs(host_engine, index):
     assert st["window_samples"] + st["chirp_samples"] <= st["samples"]
     assert st["rot"] == counts["rot"]
     assert st["rot_classes"] <= 64
+    # deferred-window view: every sample is either contracted or still summed by the integrator
+    assert st["contracted_samples"] + st["integrator_samples"] == st["samples"]
+    assert st["window_groups"] >= 1  # every config reads out in long uniform windows
+
+
+@pytest.mark.parametrize("index,groups,integrator", [(0, 1, 0), (1, 1, 0), (2, 1, 0), (4, 1, 0)])
+def test_window_groups_of_configs(host_engine, index, groups, integrator):
+    """Spin-echo / TSE / stimulated-echo readouts: one group per readout class, nothing left to the
+    integrator's per-warp sums (configs 0-2 and 4: one readout gradient)."""
+    host_engine.set_tables(precompute_sequence_tables(configs.make(index).sequence))
+    st = host_engine.program_stats()
+    assert st["window_groups"] == groups
+    assert st["integrator_samples"] == integrator
+    assert st["contracted_samples"] == st["window_samples"]
 
 
 def test_compile_detects_structure(host_engine):

@@ -83,6 +83,8 @@ int main(int argc, char** argv) {
   j.rows = rows;
   j.out0 = d_out0;
   j.echo = d_echo;
+  cudaMalloc(&j.zt, n * sizeof(float4));
+  cudaMalloc(&j.zq, n * sizeof(float2));
   ContractPlan p = contract_plan(K, W, n, n_sm);
   if (getenv("CONTRACT_DBG")) p.dbg = atoi(getenv("CONTRACT_DBG"));
   cudaMalloc(&d_part, contract_part_bytes(p, j));
