@@ -23,13 +23,20 @@ with the reference's np.linspace bounds (partition_blocks, engine.py:229-251).
   -> C-ABI bloch_compute_block, pinned host buffers): every step copies the
   spin arrays host->device and the k-space and final magnetisation
   device->host.  This is the headline against the reference arm.
-* ``roofline``: the integrator against the tensor pipe it runs on (mma.sync:
-  per spin-sample-coil one tf32 m16n8k8 pass + one bf16 m16n8k16 pass = 8
-  tf32-rate MAC, peak 512 MAC/clk/SM measured, profiles/r1_mma_microbench.txt),
-  plus the issue-slot floor from the committed ncu counters of this build
-  (profiles/ncu_counters.json) and the SURVEY §8d FP32/MUFU model as
-  ``model_frac`` (a model of the reference's per-event arithmetic, which the
-  closed-form windows do not execute, so it exceeds 1).
+* ``roofline``: the dominant kernel of the step.  With the window contraction
+  (fp32 mode) a step is two kernels: the integrator (the spin state through
+  the event stream; the long ADC windows only store their entry magnetisation
+  U) and the contraction (every window group's samples as one bf16x3 product
+  on tcgen05).  ``roofline`` is the integrator against HBM (algorithmic bytes:
+  staged spins, each plane once, U, final state; ``traffic`` = ncu DRAM bytes
+  of this build, profiles/ncu_counters.json) with its issue-slot fraction;
+  ``roofline_contraction`` is the contraction against the measured bf16
+  tensor peak (MEASURED_PEAKS.json): 3 passes x 4 real MAC per complex term.
+  Without the contraction (fp64 mode, or windows it does not take) the
+  integrator's own tensor-core windows are charged against the measured
+  mma.sync rate (512 MAC/clk/SM).  The SURVEY §8d FP32/MUFU model stays as
+  ``model_frac`` (the reference's per-event arithmetic, which the closed
+  forms do not execute, so it exceeds 1).
 * ``per_config``: value / kernel ms / fracs of configs 0-4 (device-resident,
   same world and sharding) — the other configurations on the same box.
 * ``strong_scaling_projection`` (N = 1): device time of the 1/2, 1/4, 1/8
@@ -341,15 +348,17 @@ def dry_run(args, world, rank):
 
 
 def _peaks():
-    f_max, hbm = 1965.0, None
+    f_max, hbm, bf16 = 1965.0, None, None
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             mp = json.load(fh)
         f_max = float(mp.get("sm_max_mhz", f_max))
         hbm = float(mp.get("hbm_gbs")) if mp.get("hbm_gbs") else None
+        bf16 = float(mp.get("bf16_tflops")) if mp.get("bf16_tflops") else None
     except Exception:
         pass
-    return f_max, hbm
+    # B200_PROFILING.md fallbacks when the driver-written file is absent
+    return f_max, hbm or 6500.0, bf16 or 1650.0
 
 
 def _lib_sha():
@@ -378,45 +387,66 @@ def _ncu_counters(config_index, lib_sha):
     return rec
 
 
-def roofline(counts, pstats, n_local, C, t_kernel_s, n_sm, f_max_mhz, config_index, lib_sha, precision, hbm_peak):
-    """The integrator's floors: tensor pipe (measured mma.sync rate), issue slots (ncu), and the §8d model."""
+def roofline(counts, pstats, n_local, C, t_kernel_s, n_sm, f_max_mhz, config_index, lib_sha, precision, hbm_peak,
+             t_integ_s=None, t_contract_s=None, bf16_peak=None):
+    """Floors of the step's kernels: the integrator against HBM (algorithmic bytes) and its issue slots (ncu
+    counters of this build), the window contraction against the measured bf16 tensor peak, the §8d model."""
     f = f_max_mhz * 1e6
-    w_mma = n_local * pstats["window_samples"] * C * 8 if precision == 32 else 0
-    p_mma = n_sm * MMA_MAC_PER_CLK_SM * f
-    t_tensor = w_mma / p_mma
+    contracted = pstats.get("contracted_samples", 0) if (t_contract_s or 0) > 0 else 0
+    t_integ = t_integ_s if t_integ_s else t_kernel_s
     w_fp32 = n_local * (9 * counts["rot"] + 12 * counts["prec_relax"] + 9 * counts["prec"] + 4 * C * counts["adc"])
     w_mufu = n_local * 2 * (counts["prec_relax"] + counts["prec"])
     t_model = max(w_fp32 / (n_sm * 128 * f), w_mufu / (n_sm * 16 * f))
     rec = _ncu_counters(config_index, lib_sha)
     t_issue = rec["inst_executed"] / (n_sm * 4 * f) if rec and rec.get("inst_executed") else None
     traffic = (rec.get("dram_read") or 0) + (rec.get("dram_write") or 0) if rec else None
+    # integrator algorithmic bytes: SpinConst (64 B) + initial state (24 B) + every plane once (16 B) + the U words of
+    # the contracted windows (8 B per window) + final state (24 B) per spin
+    n_windows = pstats.get("window_ops", 0) if contracted else 0
+    alg = n_local * (64 + 24 + 16 * pstats.get("planes", 0) + 8 * n_windows + 24)
+    # the integrator's own tensor-core windows (no contraction): 8 tf32-rate MAC per spin-sample-coil on mma.sync
+    w_mma = n_local * pstats["window_samples"] * C * 8 if (precision == 32 and not contracted) else 0
+    t_tensor = w_mma / (n_sm * MMA_MAC_PER_CLK_SM * f)
     out = {
-        "bound": "tensor",
-        "achieved": 2 * w_mma / t_kernel_s / 1e12,
-        "peak": 2 * p_mma / 1e12,
-        "unit": "TFLOP/s",
-        "frac": t_tensor / t_kernel_s,
+        "kernel": "integrate_kernel",
+        "bound": "hbm",
+        "achieved": alg / t_integ / 1e9,
+        "peak": hbm_peak,
+        "unit": "GB/s",
+        "frac": (alg / t_integ / 1e9 / hbm_peak) if hbm_peak else None,
         "traffic": traffic,
-        "peak_source": f"mma.sync tf32 m16n8k8, {MMA_MAC_PER_CLK_SM} MAC/clk/SM measured (profiles/"
-                       f"r1_mma_microbench.txt) x {n_sm} SM x {f_max_mhz:.0f} MHz; work = 8 tf32-rate MAC per "
-                       "spin-sample-coil (tf32 hi*hi + one bf16 k16 pass for both cross terms)",
-        "issue_frac": t_issue / t_kernel_s if t_issue else None,
-        "issue_source": (f"ncu smsp__inst_executed.sum {rec['inst_executed']:.4g} per launch / (4 x {n_sm} x f), "
-                         f"profiles/ncu_counters.json ({rec.get('source', '')})") if t_issue else
-                        "no ncu counters for this build/config",
-        "floor_frac": max(t_tensor, t_issue or 0.0) / t_kernel_s,
+        "algorithmic_bytes": alg,
+        "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
+        "traffic_source": (f"ncu dram__bytes_read.sum + dram__bytes_write.sum per launch, profiles/ncu_counters.json "
+                           f"({rec.get('source', '')})") if traffic else "no ncu counters for this build/config",
+        "issue_frac": t_issue / t_integ if t_issue else None,
+        "tensor_frac": t_tensor / t_integ if w_mma else None,
+        "tensor_note": (f"mma.sync tf32 m16n8k8, {MMA_MAC_PER_CLK_SM} MAC/clk/SM measured x {n_sm} SM x "
+                        f"{f_max_mhz:.0f} MHz; 8 tf32-rate MAC per spin-sample-coil") if w_mma else None,
         "model_frac": t_model / t_kernel_s,
         "model": "SURVEY §8d: T* = max(W_fp32 / (SM 128 f), W_mufu / (SM 16 f)), W_fp32 = N(9 rot + 12 prec_relax + "
                  "9 prec + 4C adc), W_mufu = 2N(prec_relax + prec) — the reference's per-event arithmetic; the "
-                 "engine's closed-form windows do less, so model_frac > 1",
-        "kernel_ms": t_kernel_s * 1e3,
-        "tensor_floor_ms": t_tensor * 1e3,
+                 "engine's closed forms do less, so model_frac > 1",
+        "kernel_ms": t_integ * 1e3,
+        "step_kernel_ms": t_kernel_s * 1e3,
         "issue_floor_ms": t_issue * 1e3 if t_issue else None,
         "model_ms": t_model * 1e3,
-        "hbm": ({"achieved_gbs": traffic / t_kernel_s / 1e9, "peak_gbs": hbm_peak,
-                 "frac": traffic / t_kernel_s / 1e9 / hbm_peak} if traffic and hbm_peak else None),
     }
-    return out
+    contraction = None
+    if contracted and t_contract_s:
+        macs = 3 * 4 * n_local * contracted * C  # bf16 hi*hi + hi*lo + lo*hi, 4 real MAC per complex term
+        contraction = {
+            "kernel": "contract_kernel (+ prep, fold)",
+            "bound": "tensor",
+            "achieved": 2 * macs / t_contract_s / 1e12,
+            "peak": bf16_peak,
+            "unit": "TFLOP/s",
+            "frac": (2 * macs / t_contract_s / 1e12 / bf16_peak) if bf16_peak else None,
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops (cuBLAS bf16 8192^3, burst)",
+            "work": "3 bf16 passes x 4 real MAC per (spin, contracted sample, coil)",
+            "kernel_ms": t_contract_s * 1e3,
+        }
+    return out, contraction
 
 
 class Runner:
@@ -498,14 +528,17 @@ class Runner:
         if clocks is not None:
             clocks.mark()
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-        kernel_ms, launches = [], 0
+        kernel_ms, launches, integ_ms, contract_ms = [], 0, [], []
         for k in range(steps):
             self.flush.fill_(float(k))  # untimed: evict the L2 between steps
             ev[k][0].record(self.stream)
             step()
             ev[k][1].record(self.stream)
             t = self.eng.last_timing()  # waits for this step's work
+            ph = self.eng.last_phases()
             kernel_ms.append(t["kernel_ms"])
+            integ_ms.append(ph["integrate_ms"])
+            contract_ms.append(ph["contract_ms"])
             launches += t["launches"]
         torch.cuda.synchronize()
         if self.world > 1:
@@ -514,9 +547,11 @@ class Runner:
             clocks.mark()
             clocks.stop()
         step_ms = [a.elapsed_time(b) for a, b in ev]
-        tot = torch.tensor([sum(step_ms), sum(kernel_ms)], dtype=torch.float64, device=self.dev)
+        tot = torch.tensor([sum(step_ms), sum(kernel_ms), sum(integ_ms), sum(contract_ms)], dtype=torch.float64,
+                           device=self.dev)
         if self.world > 1:
             dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+        self.last_phase_s = (tot[2].item() / 1e3, tot[3].item() / 1e3)
         return tot[0].item() / 1e3, tot[1].item() / 1e3, launches
 
 
@@ -550,7 +585,7 @@ def main(argv=None):
     torch.cuda.set_device(local_rank)
     run = Runner(local_rank, args.precision, world, rank, args.scaling)
     dev = run.dev
-    f_max, hbm_peak = _peaks()
+    f_max, hbm_peak, bf16_peak = _peaks()
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     lib_sha = _lib_sha()
 
@@ -567,6 +602,7 @@ def main(argv=None):
 
     clocks = ClockSampler(local_rank)
     t_total_s, t_kernel_s, launches = run.timed(p, args.steps, args.warmup, clocks)
+    t_integ, t_contract = (x / args.steps for x in run.last_phase_s)
     value = n_total * E * args.steps / t_total_s
     launch_shape = run.eng.last_launch()
     t_kernel = t_kernel_s / args.steps
@@ -638,18 +674,21 @@ def main(argv=None):
     h2d = sum(a.nbytes for a in h.values()) + (0 if p["unit_w"] else p["wt"].nbytes)
     d2h = out_e.nbytes + out_s.nbytes
 
-    roof = roofline(counts, pstats, n_local, C, t_kernel, n_sm, f_max, w.index, lib_sha, args.precision, hbm_peak)
+    roof, roof_c = roofline(counts, pstats, n_local, C, t_kernel, n_sm, f_max, w.index, lib_sha, args.precision,
+                            hbm_peak, t_integ, t_contract, bf16_peak)
     line = {
         "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_total_s * 1e3 / args.steps, "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None,
-        "dtype": ("f64 spin state/phase; f32 ADC sums (tf32 hi*hi + bf16 cross terms on the tensor cores), "
-                  "f64 fold" if args.precision == 32 else "f64"),
+        "dtype": ("f64 spin state/phase; ADC sums: bf16x3-split products with f32 accumulation on tcgen05 "
+                  "(window contraction), f64 fold" if args.precision == 32 else "f64"),
         "data": "synthetic (seeded, BASELINE.json config recipe)",
         "config": config_dict(w, world, E, counts, args.scaling, args.full_lattice),
         "spins_per_rank": n_local,
         "program": pstats,
         "roofline": roof,
+        "roofline_contraction": roof_c,
+        "phases_ms": {"integrate": t_integ * 1e3, "contract": t_contract * 1e3},
         "integrator_launch": launch_shape,
         "e2e": {"value": e2e_value, "unit": METRIC, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "steps": e2e_steps, "path": e2e_path},
@@ -673,11 +712,14 @@ def main(argv=None):
             ps = run.eng.program_stats()
             st = max(3, min(args.steps, 10))
             tt, tk, _ = run.timed(pc, st, 2)
-            rc = roofline(cc, ps, pc["n"], pc["C"], tk / st, n_sm, f_max, c, lib_sha, args.precision, hbm_peak)
+            ti, tc = (x / st for x in run.last_phase_s)
+            rc, rcc = roofline(cc, ps, pc["n"], pc["C"], tk / st, n_sm, f_max, c, lib_sha, args.precision, hbm_peak,
+                               ti, tc, bf16_peak)
             per[f"config{c}"] = {"workload": wc.name, "spins_total": nt, "events_per_spin": cc["events"],
                                  "value": nt * cc["events"] * st / tt, "ms_per_step": tt * 1e3 / st,
-                                 "kernel_ms": tk * 1e3 / st, "frac": rc["frac"], "issue_frac": rc["issue_frac"],
-                                 "model_frac": rc["model_frac"],
+                                 "kernel_ms": tk * 1e3 / st, "integrate_ms": ti * 1e3, "contract_ms": tc * 1e3,
+                                 "frac": rc["frac"], "issue_frac": rc["issue_frac"],
+                                 "contraction_frac": rcc["frac"] if rcc else None, "model_frac": rc["model_frac"],
                                  "spins_per_thread": run.eng.last_launch()["spins_per_thread"]}
             del pc
         line["per_config"] = per

@@ -265,6 +265,13 @@ int bloch_set_contraction(bloch_ctx* ctx, int32_t enable);
 int bloch_program_groups(const bloch_ctx* ctx, int32_t* n_groups, int64_t* contracted_samples,
                          int64_t* integrator_samples);
 
+/* The compiled op stream (diagnostics): for op i < min(n_ops, capacity) of the plain (deferred = 0) or
+ * deferred-window (deferred = 1) program, its kind (program.h OpKind), sample count / flags, rotation /
+ * chirp / train class, progression class, fused pulse and its four plane ids (pl: 4 per op).  Any
+ * output may be NULL; *n_ops receives the op count. */
+int bloch_program_ops(const bloch_ctx* ctx, int32_t deferred, int32_t capacity, int32_t* n_ops, int32_t* kind,
+                      int32_t* count, int32_t* rot, int32_t* prg, int32_t* pre, int32_t* pl);
+
 /* Phases of the last bloch_compute_block (ms, CUDA events): the integrator launches with their
  * fold, and the window contractions with theirs; the window groups contracted and the samples they
  * produced (0 when the call ran without the contraction). */

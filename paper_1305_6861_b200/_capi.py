@@ -88,6 +88,7 @@ SIGNATURES = {
     "bloch_last_segments": (c_int, [c_void_p, POINTER(c_int32)]),
     "bloch_set_contraction": (c_int, [c_void_p, c_int32]),
     "bloch_program_groups": (c_int, [c_void_p, POINTER(c_int32), POINTER(c_int64), POINTER(c_int64)]),
+    "bloch_program_ops": (c_int, [c_void_p, c_int32, c_int32] + [POINTER(c_int32)] * 7),
     "bloch_last_phases": (c_int, [c_void_p, POINTER(c_float), POINTER(c_float), POINTER(c_int32), POINTER(c_int64)]),
     "bloch_synchronize": (c_int, [c_void_p]),
     "bloch_set_kernel_gate": (c_int, [c_void_p, c_void_p, c_void_p]),

@@ -148,6 +148,7 @@ namespace {
 struct Variant {
   int prec, S, NC;
   bool full = true;  // program uses RF trains / chirps / generic sampled events
+  bool win = true;   // program has (non-deferred) OP_WINDOW ops
 };
 
 // a contiguous op range and the contiguous compact samples it records
@@ -259,7 +260,7 @@ template <typename R, int S, int NC>
 void shape_one(const Variant& v, int* max_t, int* min_b) {
   if (v.prec == int(8 * sizeof(R)) && v.S == S && v.NC == NC) {
     *max_t = bloch::KernelTraits<R, S, NC>::kMaxThreads;
-    *min_b = bloch::KernelTraits<R, S, NC>::kMinBlocks;
+    *min_b = v.win ? bloch::KernelTraits<R, S, NC>::kMinBlocks : bloch::KernelTraits<R, S, NC>::kMinBlocksNoWin;
   }
 }
 
@@ -277,7 +278,7 @@ cudaError_t dispatch_one(const Variant& v, const bloch::KParams& kp, int grid, i
                          cudaStream_t st, bool* matched) {
   if (v.prec == int(8 * sizeof(R)) && v.S == S && v.NC == NC) {
     *matched = true;
-    return bloch::launch_integrate<R, S, NC>(kp, grid, threads, st, v.full);
+    return bloch::launch_integrate<R, S, NC>(kp, grid, threads, st, v.full, v.win);
   }
   return cudaSuccess;
 }
@@ -848,7 +849,7 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       // the window contraction: fp32 mode, one receive coil, U rows within the partial budget
       const int64_t urows = static_cast<int64_t>(P.urow_out0.size());
       const int64_t uwords = bloch::contract_u_words(urows, n);
-      const bool defer = c->contraction && c->precision == BLOCH_PREC_F32 && n_coils == 1 && !P.groups.empty() &&
+      const bool defer = c->contraction && c->precision == BLOCH_PREC_F32 && !P.groups.empty() &&
                          2 * uwords * 4 <= partial_budget_bytes();
       const std::vector<bloch::DevOp>& OPS = defer ? P.dops : P.ops;
       int max_window = 0;
@@ -858,6 +859,9 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       v.full = false;
       for (const bloch::DevOp& op : OPS)
         if (op.kind == bloch::OP_RFTRAIN || op.kind == bloch::OP_CHIRP || op.kind == bloch::OP_GSAMP) v.full = true;
+      v.win = v.full || v.prec != 32;
+      for (const bloch::DevOp& op : OPS)
+        if (op.kind == bloch::OP_WINDOW) v.win = true;
       int max_t = 512, min_b = 1;
       variant_shape(v, &max_t, &min_b);
       const int64_t slots = int64_t(c->n_sm) * min_b;  // resident CTAs per wave
@@ -894,10 +898,11 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
         c->ulo.ensure(static_cast<size_t>(uwords) * 4);
         size_t cb = 0;
         for (const bloch::WinGroup& g : P.groups) {
-          cplans.push_back(bloch::contract_plan(g.count, g.n_windows, n, c->n_sm));
+          cplans.push_back(bloch::contract_plan(g.count, g.n_windows, n, c->n_sm, n_coils));
           bloch::ContractJob j0{};
           j0.W = g.n_windows;
           j0.K = g.count;
+          j0.C = n_coils;
           cb = std::max(cb, bloch::contract_part_bytes(cplans.back(), j0));
         }
         c->cpart.ensure(cb);
@@ -992,6 +997,10 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
           j.part = c->cpart.as<float>();
           j.out0 = c->d_urow_out0.as<int64_t>() + g.row0;
           j.echo = d_echo;
+          j.C = n_coils;
+          j.ncp = ncp;
+          j.w32 = n_coils > 1 ? c->w32.as<float2>() : nullptr;
+          j.G = G;
           j.zt = c->ztab.as<float4>();
           j.zq = c->zqtab.as<float2>();
           ck(bloch::launch_contract(j, cplans[gi], st), "contraction kernel");
@@ -1065,6 +1074,25 @@ int bloch_program_groups(const bloch_ctx* c, int32_t* n_groups, int64_t* contrac
   if (n_groups) *n_groups = static_cast<int32_t>(c->prog.groups.size());
   if (contracted_samples) *contracted_samples = c->prog.n_deferred_samples;
   if (integrator_samples) *integrator_samples = static_cast<int64_t>(c->prog.dsample_g.size());
+  return BLOCH_OK;
+}
+
+int bloch_program_ops(const bloch_ctx* c, int32_t deferred, int32_t capacity, int32_t* n_ops, int32_t* kind,
+                      int32_t* count, int32_t* rot, int32_t* prg, int32_t* pre, int32_t* pl) {
+  if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
+  if (!c->has_prog) return fail(BLOCH_E_STATE, "no tables uploaded");
+  const std::vector<bloch::DevOp>& ops = deferred ? c->prog.dops : c->prog.ops;
+  if (n_ops) *n_ops = static_cast<int32_t>(ops.size());
+  for (int32_t i = 0; i < capacity && i < static_cast<int32_t>(ops.size()); ++i) {
+    const bloch::DevOp& o = ops[i];
+    if (kind) kind[i] = o.kind;
+    if (count) count[i] = o.count;
+    if (rot) rot[i] = o.rot;
+    if (prg) prg[i] = o.prg;
+    if (pre) pre[i] = o.pre;
+    if (pl)
+      for (int k = 0; k < 4; ++k) pl[4 * i + k] = o.pl[k];
+  }
   return BLOCH_OK;
 }
 

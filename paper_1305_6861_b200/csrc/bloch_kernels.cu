@@ -843,8 +843,9 @@ __device__ __forceinline__ void chirp_f32(const KParams& kp, const DevOp* op, Sp
 // BD: the block size as a compile-time constant (0: blockDim.x).  The spin state
 // [3][S][bd] is addressed (component, slot) x bd + thread on every access; with a
 // constant bd those offsets are immediates.
-template <typename R, int S, int NC, bool kFull, int BD>
-__global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTraits<R, S, NC>::kMinBlocks)
+template <typename R, int S, int NC, bool kFull, int BD, bool kWin>
+__global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads,
+                                  kWin ? KernelTraits<R, S, NC>::kMinBlocks : KernelTraits<R, S, NC>::kMinBlocksNoWin)
     integrate_kernel(const KParams kp) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int kSampPerChunk = kChunkSlots / NC;
@@ -1247,8 +1248,8 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads, KernelTra
 
     }
 
-    // OP_WINDOW
-    {
+    // OP_WINDOW (compiled out of the kernels for programs whose windows are all deferred, OP_UWIN)
+    if constexpr (kWin) {
       const int cnt = __ldg(&op->count), lead = __ldg(&op->aux), s0 = __ldg(&op->s0) - kp.sample_base, rc = __ldg(&op->rot),
                 pre = __ldg(&op->pre);
       if constexpr (!kFull) {
@@ -1819,11 +1820,12 @@ __global__ void reduce_partials_kernel(const R* __restrict__ part, int rows, int
 // ---------------------------------------------------------------------------
 
 template <typename R, int S, int NC>
-size_t integrate_smem_bytes(int threads) {
-  // fp64 spin state [3][S][threads] + (fp32 single-coil) the tensor-core window stage, 16 B per spin
+size_t integrate_smem_bytes(int threads, bool win) {
+  // fp64 spin state [3][S][threads] + (fp32, programs with windows or chirps) the tensor-core window stage
   size_t stage = 0;
   if constexpr (sizeof(R) == 4 && NC == 1) stage = kStageBytes;
   if constexpr (sizeof(R) == 4 && NC >= 2) stage = McStage<NC>::kBytes;
+  if (!win) stage = 0;
   return static_cast<size_t>(3 * S * threads) * sizeof(double) + static_cast<size_t>(threads / 32) * stage;
 }
 
@@ -1831,9 +1833,9 @@ size_t integrate_smem_bytes(int threads) {
 // (kernel instance, device), under a lock (contexts on several devices or threads share the instances)
 static std::mutex g_smem_mu;
 
-template <typename R, int S, int NC, bool kFull, int BD>
+template <typename R, int S, int NC, bool kFull, int BD, bool kWin>
 static cudaError_t launch_bd(const KParams& kp, int grid, int threads, cudaStream_t stream) {
-  const size_t smem = integrate_smem_bytes<R, S, NC>(threads);
+  const size_t smem = integrate_smem_bytes<R, S, NC>(threads, kWin || kFull);
   static size_t smem_set[kMaxDevices] = {};  // raise the limit only when needed (not inside a graph capture)
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -1842,34 +1844,37 @@ static cudaError_t launch_bd(const KParams& kp, int grid, int threads, cudaStrea
   {
     std::lock_guard<std::mutex> lk(g_smem_mu);
     if (smem > 48 * 1024 && smem > smem_set[dev]) {
-      e = cudaFuncSetAttribute(integrate_kernel<R, S, NC, kFull, BD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      e = cudaFuncSetAttribute(integrate_kernel<R, S, NC, kFull, BD, kWin>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem));
       if (e != cudaSuccess) return e;
       smem_set[dev] = smem;
     }
   }
-  integrate_kernel<R, S, NC, kFull, BD><<<grid, threads, smem, stream>>>(kp);
+  integrate_kernel<R, S, NC, kFull, BD, kWin><<<grid, threads, smem, stream>>>(kp);
   return cudaGetLastError();
 }
 
 // the basic fp32 single-coil kernel with 8 spins per thread at its full block size (config 1's
 // launch) gets a constant-block-size instance: config 1 -1.0%; the kFull variant measured +2.8%
 // on config 3 with it, so it keeps the runtime block size
-template <typename R, int S, int NC, bool kFull>
+template <typename R, int S, int NC, bool kFull, bool kWin>
 static cudaError_t launch_one(const KParams& kp, int grid, int threads, cudaStream_t stream) {
 #ifndef BLOCH_NO_FIXED_BD
   constexpr int kMax = KernelTraits<R, S, NC>::kMaxThreads;
   if constexpr (sizeof(R) == 4 && NC == 1 && S == 8 && !kFull) {
-    if (threads == kMax) return launch_bd<R, S, NC, kFull, kMax>(kp, grid, threads, stream);
+    if (threads == kMax) return launch_bd<R, S, NC, kFull, kMax, kWin>(kp, grid, threads, stream);
   }
 #endif
-  return launch_bd<R, S, NC, kFull, 0>(kp, grid, threads, stream);
+  return launch_bd<R, S, NC, kFull, 0, kWin>(kp, grid, threads, stream);
 }
 
 template <typename R, int S, int NC>
-cudaError_t launch_integrate(const KParams& kp, int grid, int threads, cudaStream_t stream, bool full) {
-  return full ? launch_one<R, S, NC, true>(kp, grid, threads, stream)
-              : launch_one<R, S, NC, false>(kp, grid, threads, stream);
+cudaError_t launch_integrate(const KParams& kp, int grid, int threads, cudaStream_t stream, bool full, bool win) {
+  if constexpr (sizeof(R) == 4) {  // fp32 mode: programs of pulses, intervals and deferred windows only
+    if (!full && !win) return launch_one<R, S, NC, false, false>(kp, grid, threads, stream);
+  }
+  return full ? launch_one<R, S, NC, true, true>(kp, grid, threads, stream)
+              : launch_one<R, S, NC, false, true>(kp, grid, threads, stream);
 }
 
 static int grid_for(int64_t total, int threads) {
@@ -1949,7 +1954,7 @@ cudaError_t launch_reduce(const R* part, int rows, int64_t row_stride, int64_t n
 template <typename R, int S, int NC>
 cudaError_t kernel_attrs(int* max_threads, int* regs) {
   cudaFuncAttributes a;
-  cudaError_t e = cudaFuncGetAttributes(&a, integrate_kernel<R, S, NC, true, 0>);
+  cudaError_t e = cudaFuncGetAttributes(&a, integrate_kernel<R, S, NC, true, 0, true>);
   if (e != cudaSuccess) return e;
   *max_threads = a.maxThreadsPerBlock;
   *regs = a.numRegs;
@@ -1957,9 +1962,9 @@ cudaError_t kernel_attrs(int* max_threads, int* regs) {
 }
 
 #define BLOCH_INST(R, S, NC)                                                              \
-  template cudaError_t launch_integrate<R, S, NC>(const KParams&, int, int, cudaStream_t, bool); \
+  template cudaError_t launch_integrate<R, S, NC>(const KParams&, int, int, cudaStream_t, bool, bool); \
   template cudaError_t kernel_attrs<R, S, NC>(int*, int*);                                 \
-  template size_t integrate_smem_bytes<R, S, NC>(int);
+  template size_t integrate_smem_bytes<R, S, NC>(int, bool);
 BLOCH_FOR_EACH_VARIANT(BLOCH_INST)
 #undef BLOCH_INST
 

@@ -44,9 +44,13 @@ struct ContractJob {
   const uint32_t* uhi;  // U, spin-block major (contract_u_index): bf16x2 (Re, Im) words, hi part
   const uint32_t* ulo;  // lo part
   int64_t rows;         // rows (windows of every group) of the U arrays
-  float* part;          // [chunks * segs][W][K][2] partial sums per (spin chunk, accumulation segment)
+  float* part;          // [chunks * segs][C][W][K][2] partial sums per (spin chunk, accumulation segment)
   const int64_t* out0;  // [W] complex index (coil 0) of each window's first sample in the echo array
-  double* echo;         // echo array (complex128), samples stored
+  double* echo;         // echo array (complex128) [C][G], samples stored
+  int32_t C;            // receive coils: coil c's samples are sum_s w_cs U[w][s] z_s^k (w folded into A)
+  int32_t ncp;          // coil stride of w32
+  const float2* w32;    // [n][ncp] fp32 coil weights (C > 1; one coil carries its weight in U)
+  int64_t G;            // complex samples per coil in the echo array
   float4* zt;           // [n] scratch: per-spin (theta_hi, theta_lo, a, 0), theta = phase per sample mod 2 pi
   float2* zq;           // [n] scratch: per-spin z^2
 };
@@ -56,7 +60,8 @@ constexpr int kContractMaxSamples = 4096;  // windows up to this long (the fp32 
 struct ContractPlan {
   int mt;          // 64-sample M-tiles per CTA (1, 2, 4)
   int nw;          // windows per CTA (MMA N, multiple of 16, <= 256)
-  int tiles_k;     // CTA tiles along the samples
+  int tiles_k;     // CTA tiles along the samples (all coils: C x tiles per coil)
+  int tpc;         // CTA sample tiles per coil
   int tiles_w;     // CTA tiles along the windows
   int chunks;      // split-K chunks along the spins
   int stages;      // 16-spin stages per chunk
@@ -70,7 +75,7 @@ struct ContractPlan {
   int dbg;         // experiment hook: 1 = skip A generation stores, 2 = skip MMAs
 };
 
-ContractPlan contract_plan(int K, int W, int64_t n, int n_sm);
+ContractPlan contract_plan(int K, int W, int64_t n, int n_sm, int C = 1);
 size_t contract_part_bytes(const ContractPlan& p, const ContractJob& j);
 // the GEMM (partials) and the fold into the echo array, on `st`
 cudaError_t launch_contract(const ContractJob& j, const ContractPlan& p, cudaStream_t st);

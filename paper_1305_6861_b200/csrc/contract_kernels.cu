@@ -129,7 +129,8 @@ __global__ void __launch_bounds__(ct::kThreads, 1)
   const int tk = blockIdx.x % p.tiles_k;
   const int rest = blockIdx.x / p.tiles_k;
   const int tw = rest % p.tiles_w, kc = rest / p.tiles_w;
-  const int k0 = tk * 64 * MT, w0 = tw * nw;
+  const int coil = tk / p.tpc;
+  const int k0 = (tk - coil * p.tpc) * 64 * MT, w0 = tw * nw;
   const int64_t total_st = (j.n + ct::kStageSpins - 1) / ct::kStageSpins;
   const int64_t st0 = static_cast<int64_t>(kc) * p.stages;
   const int nst = static_cast<int>(min(static_cast<int64_t>(p.stages), total_st - st0));
@@ -224,7 +225,7 @@ __global__ void __launch_bounds__(ct::kThreads, 1)
     auto drain = [&](int e) {
       ct::mbar_wait(acc_full, e & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      float* slot = j.part + (static_cast<int64_t>(kc) * p.segs + e) * j.W * j.K * 2;
+      float* slot = j.part + ((static_cast<int64_t>(kc) * p.segs + e) * j.C + coil) * j.W * j.K * 2;
       for (int mm = 0; mm < MT; ++mm) {
         const int k = k0 + 64 * mm + (row >> 1);
         for (int c0 = 16 * colh; c0 < nw; c0 += 32) {
@@ -250,25 +251,26 @@ __global__ void __launch_bounds__(ct::kThreads, 1)
       if (lane == 0) ct::mbar_arrive(acc_empty);
     };
     // per-spin phase tables of the next stage are loaded one stage ahead
-    auto load_z = [&](int t, float4& zt, float2& zq) {
+    auto load_z = [&](int t, float4& zt, float2& zq, float2& wc) {
       const int64_t i = (st0 + t) * ct::kStageSpins + sl;
       if (t < nst && i < j.n) {
         zt = __ldg(j.zt + i);
         zq = __ldg(j.zq + i);
+        wc = j.C > 1 ? __ldg(j.w32 + i * j.ncp + coil) : make_float2(1.f, 0.f);
       } else {
         zt = make_float4(0.f, 0.f, 0.f, 0.f);
-        zq = make_float2(0.f, 0.f);
+        zq = wc = make_float2(0.f, 0.f);
       }
     };
     float4 nzt;
-    float2 nzq;
-    load_z(0, nzt, nzq);
+    float2 nzq, nwc;
+    load_z(0, nzt, nzq, nwc);
     const float kf = static_cast<float>(kfirst);
     int e_next = 0;  // next segment to drain
     for (int t = 0; t < nst; ++t) {
       const float4 czt = nzt;
-      const float2 czq = nzq;
-      load_z(t + 1, nzt, nzq);
+      const float2 czq = nzq, cwc = nwc;
+      load_z(t + 1, nzt, nzq, nwc);
       const int s = t % depth;
       if (t >= depth) {
         ct::mbar_wait(empty + s, ((t / depth) - 1) & 1);
@@ -283,7 +285,8 @@ __global__ void __launch_bounds__(ct::kThreads, 1)
       }
       float2 P = make_float2(0.f, 0.f), Q = make_float2(0.f, 0.f);
       if ((st0 + t) * ct::kStageSpins + sl < j.n) {
-        P = ct::zpow32(czt, kf);
+        const float2 z0 = ct::zpow32(czt, kf);
+        P = make_float2(cwc.x * z0.x - cwc.y * z0.y, cwc.x * z0.y + cwc.y * z0.x);  // the coil weight rides along
         Q = czq;
       }
       unsigned char* ah = A(s, 0);
@@ -345,19 +348,20 @@ __global__ void contract_prep_kernel(const SpinConst* __restrict__ sc, int64_t n
 // fixed-order fp64 fold of the partial slots (spin chunk major, segment minor) into the echo array
 // (stored, not added); chunk c holds ceil(stages_c / seg) segments
 __global__ void contract_fold_kernel(const float* __restrict__ part, int chunks, int segs, int seg, int stages,
-                                     int64_t total_st, int W, int K, const int64_t* __restrict__ out0,
+                                     int64_t total_st, int C, int W, int K, int64_t G, const int64_t* __restrict__ out0,
                                      double* __restrict__ echo) {
-  const int64_t per = static_cast<int64_t>(W) * K * 2;
+  const int64_t per = static_cast<int64_t>(C) * W * K * 2;
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < per;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t w = t / (2 * K), r = t - w * 2 * K;
+    const int64_t cw = t / (2 * K), r = t - cw * 2 * K;
+    const int64_t c = cw / W, w = cw - c * W;
     double acc = 0.0;
     for (int c = 0; c < chunks; ++c) {
       const int64_t nst = min(static_cast<int64_t>(stages), total_st - static_cast<int64_t>(c) * stages);
       const int ns = static_cast<int>((nst + seg - 1) / seg);
       for (int e = 0; e < ns; ++e) acc += static_cast<double>(part[(static_cast<int64_t>(c) * segs + e) * per + t]);
     }
-    echo[(out0[w] + (r >> 1)) * 2 + (r & 1)] = acc;
+    echo[(c * G + out0[w] + (r >> 1)) * 2 + (r & 1)] = acc;
   }
 }
 
@@ -365,7 +369,7 @@ __global__ void contract_fold_kernel(const float* __restrict__ part, int chunks,
 // host side
 // ---------------------------------------------------------------------------
 
-ContractPlan contract_plan(int K, int W, int64_t n, int n_sm) {
+ContractPlan contract_plan(int K, int W, int64_t n, int n_sm, int C) {
   ContractPlan p{};
   p.nw = ((W + 15) / 16) * 16;
   if (p.nw > 256) p.nw = 256;
@@ -387,7 +391,8 @@ ContractPlan contract_plan(int K, int W, int64_t n, int n_sm) {
   if (p.depth < 2) p.depth = 2;
   p.smem = p.depth * stage + 1024 + 256;
   p.dbg = 0;
-  p.tiles_k = (K + 64 * p.mt - 1) / (64 * p.mt);
+  p.tpc = (K + 64 * p.mt - 1) / (64 * p.mt);
+  p.tiles_k = C * p.tpc;
   p.tiles_w = (W + p.nw - 1) / p.nw;
   const int64_t total_st = (n + ct::kStageSpins - 1) / ct::kStageSpins;
   int64_t chunks = n_sm / (p.tiles_k * p.tiles_w);
@@ -409,7 +414,7 @@ ContractPlan contract_plan(int K, int W, int64_t n, int n_sm) {
 }
 
 size_t contract_part_bytes(const ContractPlan& p, const ContractJob& j) {
-  return static_cast<size_t>(p.chunks) * p.segs * j.W * j.K * 2 * sizeof(float);
+  return static_cast<size_t>(p.chunks) * p.segs * j.C * j.W * j.K * 2 * sizeof(float);
 }
 
 namespace {
@@ -471,7 +476,7 @@ cudaError_t launch_mt(const CUtensorMap& mh, const CUtensorMap& ml, const Contra
 
 cudaError_t launch_contract(const ContractJob& j, const ContractPlan& p, cudaStream_t st) {
   if (j.n <= 0 || j.W <= 0 || j.K <= 0) return cudaSuccess;
-  if (j.K > kContractMaxSamples) return cudaErrorInvalidValue;
+  if (j.K > kContractMaxSamples || j.C < 1 || (j.C > 1 && !j.w32)) return cudaErrorInvalidValue;
   {
     const int64_t blocks = (j.n + 255) / 256;
     contract_prep_kernel<<<static_cast<int>(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(
@@ -487,11 +492,11 @@ cudaError_t launch_contract(const ContractJob& j, const ContractPlan& p, cudaStr
     default: e = launch_mt<1>(mh, ml, j, p, st); break;
   }
   if (e != cudaSuccess) return e;
-  const int64_t per = static_cast<int64_t>(j.W) * j.K * 2;
+  const int64_t per = static_cast<int64_t>(j.C) * j.W * j.K * 2;
   const int64_t blocks = (per + 255) / 256;
   const int64_t total_st = (j.n + ct::kStageSpins - 1) / ct::kStageSpins;
   contract_fold_kernel<<<static_cast<int>(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(
-      j.part, p.chunks, p.segs, p.seg, p.stages, total_st, j.W, j.K, j.out0, j.echo);
+      j.part, p.chunks, p.segs, p.seg, p.stages, total_st, j.C, j.W, j.K, j.G, j.out0, j.echo);
   return cudaGetLastError();
 }
 

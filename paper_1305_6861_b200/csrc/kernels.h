@@ -49,11 +49,16 @@ template <typename R, int S, int NC>
 struct KernelTraits {
   static constexpr int kMaxThreads = 512;
   static constexpr int kMinBlocks = 1;
+  static constexpr int kMinBlocksNoWin = 1;  // the variant without window code (every window deferred)
 };
+#ifndef BLOCH_NOWIN_MINB
+#define BLOCH_NOWIN_MINB 2
+#endif
 template <>
 struct KernelTraits<float, 8, 1> {  // the fp32 single-coil workhorse: 2 CTAs x 10 warps per SM
   static constexpr int kMaxThreads = 320;   // measured: 1 x 16 warps 17.6 ms, 2 x 10 warps 14.1 ms,
   static constexpr int kMinBlocks = 2;      // 3 x 8 warps (80 regs, spills) 15.5 ms on config 1
+  static constexpr int kMinBlocksNoWin = BLOCH_NOWIN_MINB;
 };
 
 // (real type, spins per thread, coils) instantiated in bloch_kernels.cu
@@ -77,26 +82,29 @@ template <>
 struct KernelTraits<float, 4, 1> {  // long windows (>= 384 samples): 2 CTAs x 12 warps, 4 spins per thread
   static constexpr int kMaxThreads = 384;
   static constexpr int kMinBlocks = 2;
+  static constexpr int kMinBlocksNoWin = BLOCH_NOWIN_MINB;
 };
 
 template <>
 struct KernelTraits<float, 1, 1> {  // small blocks (spin shards): one spin per thread, 2 CTAs x 10 warps
   static constexpr int kMaxThreads = 320;
   static constexpr int kMinBlocks = 2;
+  static constexpr int kMinBlocksNoWin = BLOCH_NOWIN_MINB;
 };
 
 template <>
 struct KernelTraits<float, 1, 8> {  // small eight-coil blocks: one spin per thread
   static constexpr int kMaxThreads = 320;
   static constexpr int kMinBlocks = 2;
+  static constexpr int kMinBlocksNoWin = BLOCH_NOWIN_MINB;
 };
 
 template <typename R, int S, int NC>
-cudaError_t launch_integrate(const KParams& kp, int grid, int threads, cudaStream_t stream, bool full);
+cudaError_t launch_integrate(const KParams& kp, int grid, int threads, cudaStream_t stream, bool full, bool win);
 template <typename R, int S, int NC>
 cudaError_t kernel_attrs(int* max_threads, int* regs);
 template <typename R, int S, int NC>
-size_t integrate_smem_bytes(int threads);
+size_t integrate_smem_bytes(int threads, bool win);
 cudaError_t launch_prep(int64_t n, const double* pos, const double* dw, const double* m0, const double* t1,
                         const double* t2, SpinConst* sc, cudaStream_t stream);
 cudaError_t launch_relax_table(int64_t n, int n_cls, const double* T, const SpinConst* sc, double* out,

@@ -377,6 +377,20 @@ class BlochEngine:
         out.update(window_groups=g.value, contracted_samples=cs.value, integrator_samples=rs.value)
         return out
 
+    def program_ops(self, deferred: bool = False) -> Dict[str, np.ndarray]:
+        """The compiled op stream (bloch_program_ops): kind, count, rot, prg, pre and planes (n, 4) per op."""
+        n = ctypes.c_int32()
+        _capi.check(self._lib.bloch_program_ops(self._h, int(deferred), 0, ctypes.byref(n), *([None] * 6)),
+                    "bloch_program_ops")
+        k = n.value
+        out = {name: np.zeros(k, dtype=np.int32) for name in ("kind", "count", "rot", "prg", "pre")}
+        out["pl"] = np.zeros((k, 4), dtype=np.int32)
+        p32 = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+        _capi.check(self._lib.bloch_program_ops(self._h, int(deferred), k, ctypes.byref(n), p32(out["kind"]),
+                                                p32(out["count"]), p32(out["rot"]), p32(out["prg"]), p32(out["pre"]),
+                                                p32(out["pl"])), "bloch_program_ops")
+        return out
+
     def last_timing(self) -> Dict[str, float]:
         k, d, n = ctypes.c_float(), ctypes.c_float(), ctypes.c_int32()
         _capi.check(self._lib.bloch_last_timing(self._h, ctypes.byref(k), ctypes.byref(d), ctypes.byref(n)), "timing")

@@ -67,7 +67,10 @@ def test_gpu_arm_contract():
     assert d["value"] > 0 and d["gpu_launches"] >= 3 * 3
     r = d["roofline"]
     assert r["peak"] > 0 and r["achieved"] > 0 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
-    assert abs(r["frac"] - r["tensor_floor_ms"] / r["kernel_ms"]) < 1e-9 and r["model_frac"] > 0
+    assert r["bound"] == "hbm" and r["algorithmic_bytes"] > 0 and r["model_frac"] > 0
+    rc = d["roofline_contraction"]  # config 0's readouts go through the tensor-core contraction
+    assert rc["bound"] == "tensor" and rc["achieved"] > 0 and abs(rc["frac"] - rc["achieved"] / rc["peak"]) < 1e-9
+    assert d["phases_ms"]["contract"] > 0 and d["phases_ms"]["integrate"] > 0
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["config"]["workload"] == "cfg0_se64"

@@ -318,7 +318,7 @@ def test_gpu_window_sums_without_contraction(name):
         assert e <= STATE_TOL[32], f"{name} snapshot {i} rel L2 {e:.3e}"
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "se16_box", "tse16", "epi16"])
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "se16_box", "tse16", "epi16", "tse_2coil"])
 def test_gpu_contraction_runs_and_matches(name):
     """The long tabulated windows of these programs go through the tensor-core contraction."""
     from paper_1305_6861_b200.engine import get_engine

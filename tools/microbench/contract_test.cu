@@ -83,6 +83,10 @@ int main(int argc, char** argv) {
   j.rows = rows;
   j.out0 = d_out0;
   j.echo = d_echo;
+  j.C = 1;
+  j.ncp = 1;
+  j.w32 = nullptr;
+  j.G = static_cast<int64_t>(W) * K;
   cudaMalloc(&j.zt, n * sizeof(float4));
   cudaMalloc(&j.zq, n * sizeof(float2));
   ContractPlan p = contract_plan(K, W, n, n_sm);
