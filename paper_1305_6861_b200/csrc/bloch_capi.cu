@@ -213,37 +213,38 @@ std::vector<Segment> plan_segments(const std::vector<bloch::DevOp>& ops, int64_t
   return segs;
 }
 
-// pick (S, NC) for a block of n spins with ncp (power-of-two) coils; max_window: the longest
-// uniform ADC window of the program (samples)
-Variant pick_variant(int prec, int64_t n, int ncp, int n_sm, int max_window) {
+// pick (S, NC) for a block of n spins with ncp (power-of-two) coils.  win: the program keeps windows (or
+// chirps / generic samples) in the integrator; plane_bytes: the per-spin class tables (planes) of the call.
+Variant pick_variant(int prec, int64_t n, int ncp, int n_sm, bool win, int64_t plane_bytes) {
   if (prec == BLOCH_PREC_F32) {
-    static const int force_s = [] {  // experiment hook: BLOCH_F32_SPINS=2|4|8
+    static const int force_s = [] {  // experiment hook: BLOCH_F32_SPINS=1|2|4|8
       const char* e = getenv("BLOCH_F32_SPINS");
       return e ? atoi(e) : 0;
     }();
-    // the largest spins-per-thread that still keeps >= 16 warps per SM busy: a spin shard of a
-    // multi-GPU run (n / world) must not trade occupancy for per-thread reuse. Measured (B200):
-    // config 1 / 8 (87k spins) S=8 4.13 ms, S=4 3.00, S=2 1.95; config 1 / 4 S=8 5.23, S=4 3.68,
-    // S=2 3.63; the full config 1 (697k) S=8 10.25 vs S=4 10.90
-    auto fits = [&](int s) { return n >= int64_t(n_sm) * 16 * 32 * s; };
     if (ncp == 1) {
       if (force_s == 1 || force_s == 2 || force_s == 4 || force_s == 8) return {32, force_s, 1};
-      // long windows no longer favour 4 spins per thread since the 2-unit window products
-      // (config 2, 512-sample windows: S=8 26.6 ms vs S=4 27.3; it was 35.0 vs 38.1 with 3 tf32 passes)
-      (void)max_window;
-      if (fits(8)) return {32, 8, 1};
-      // below one wave of 4-spin threads, one spin per thread (more warps, more waves) wins every
-      // measured shard: config 1 / 4 2.72 vs 2.91 ms (S=2), / 8 1.35 vs 1.42, / 16 0.94 vs 1.16;
-      // config 2 / 8 4.37 vs 5.00; config 0 (2,444 spins) 0.17 vs 0.22
-      return {32, fits(4) ? 4 : 1, 1};
+      // One wave of 2 CTAs x 320 threads per SM at the smallest S that holds the block, then one step
+      // down when the planes overflow L2: two waves of S = 4 keep each wave's planes in L2.  Measured
+      // with the contraction (kernel ms, profiles/r2t_spins_sweep.txt), S = 8 / 4 / 2 / 1:
+      //   config 2 (749k, 204 MB of planes)   11.52 / 10.40 / 12.86 / 12.81
+      //   config 1 (698k,  89 MB)              3.27 /  3.56 /  4.14 /  4.00
+      //   config 2 / 4 (187k)                  4.57 /  3.41 /  2.93 /  4.04;  / 8: 3.53 / 2.60 / 2.14 / 2.01
+      //   config 1 / 4 (174k)                  1.67 /  1.20 /  1.05 /  1.43;  / 8: 1.33 / 0.99 / 0.83 / 0.76
+      // A program that keeps windows / chirps in the integrator (config 3) carries the window stage
+      // (less L1): one step more spins per thread, config 3 / 4 S = 4 1.94 vs S = 2 2.40, / 8 S = 2 1.26.
+      const int64_t wave = int64_t(n_sm) * 2 * 320;
+      int s = 1;
+      while (s < 8 && n > wave * s) s <<= 1;
+      if (win && s < 8) s <<= 1;
+      if (s == 8 && n * plane_bytes > (int64_t(100) << 20)) s = 4;
+      return {32, s, 1};
     }
     if (ncp == 8) {
       // eight coils carry 4x the accumulators per spin, so fewer warps already saturate: measured
-      // config 4 (274k) S=4 63.7 vs S=2 71.3 ms; config 4 / 2 S=4 42.2 vs S=2 37.0; / 8 33.1 vs 20.6
+      // (contraction on) config 4 (274k) S=4 7.87 vs S=2 8.14 ms; / 2 S=2 4.15 vs S=4 4.52;
+      // / 4 S=1 2.37 vs S=2 2.57; / 8 S=1 1.56 vs S=2 1.66
       if (force_s == 1 || force_s == 2 || force_s == 4) return {32, force_s, 8};
-      // and very small eight-coil shards one spin per thread: config 4 / 8 (34k) 7.42 vs 8.26 ms (S=2),
-      // but / 4 (69k) 12.66 vs 12.13
-      if (n < int64_t(n_sm) * 10 * 32) return {32, 1, 8};
+      if (n < int64_t(n_sm) * 16 * 32) return {32, 1, 8};
       return {32, n >= int64_t(n_sm) * 8 * 32 * 4 ? 4 : 2, 8};
     }
     return {32, 4, ncp};
@@ -852,16 +853,15 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       const bool defer = c->contraction && c->precision == BLOCH_PREC_F32 && !P.groups.empty() &&
                          2 * uwords * 4 <= partial_budget_bytes();
       const std::vector<bloch::DevOp>& OPS = defer ? P.dops : P.ops;
-      int max_window = 0;
-      for (const bloch::DevOp& op : OPS)
-        if (op.kind == bloch::OP_WINDOW) max_window = std::max(max_window, static_cast<int>(op.count));
-      Variant v = pick_variant(c->precision, n, ncp, c->n_sm, max_window);
-      v.full = false;
-      for (const bloch::DevOp& op : OPS)
-        if (op.kind == bloch::OP_RFTRAIN || op.kind == bloch::OP_CHIRP || op.kind == bloch::OP_GSAMP) v.full = true;
-      v.win = v.full || v.prec != 32;
-      for (const bloch::DevOp& op : OPS)
-        if (op.kind == bloch::OP_WINDOW) v.win = true;
+      bool full = false, win = c->precision != BLOCH_PREC_F32;
+      for (const bloch::DevOp& op : OPS) {
+        if (op.kind == bloch::OP_RFTRAIN || op.kind == bloch::OP_CHIRP || op.kind == bloch::OP_GSAMP) full = true;
+        if (op.kind == bloch::OP_WINDOW) win = true;
+      }
+      win = win || full;
+      Variant v = pick_variant(c->precision, n, ncp, c->n_sm, win, static_cast<int64_t>(P.planes.size()) * 16);
+      v.full = full;
+      v.win = win;
       int max_t = 512, min_b = 1;
       variant_shape(v, &max_t, &min_b);
       const int64_t slots = int64_t(c->n_sm) * min_b;  // resident CTAs per wave
