@@ -374,14 +374,15 @@ def _lib_sha():
         return None
 
 
-def _ncu_counters(config_index, lib_sha):
-    """Per-launch ncu counters of the integrator for this build (profiles/ncu_counters.json), or None."""
+def _ncu_counters(config_index, lib_sha, kernel=""):
+    """Per-launch ncu counters of the integrator (kernel="") or the contraction (kernel="_contract") for this
+    build (profiles/ncu_counters.json), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_counters.json")) as fh:
             d = json.load(fh)
     except Exception:
         return None
-    rec = d.get(f"config{config_index}")
+    rec = d.get(f"config{config_index}{kernel}")
     if not rec or (lib_sha and rec.get("lib_sha16") not in (None, lib_sha)):
         return None
     return rec
@@ -435,7 +436,10 @@ def roofline(counts, pstats, n_local, C, t_kernel_s, n_sm, f_max_mhz, config_ind
     contraction = None
     if contracted and t_contract_s:
         macs = 3 * 4 * n_local * contracted * C  # bf16 hi*hi + hi*lo + lo*hi, 4 real MAC per complex term
+        crec = _ncu_counters(config_index, lib_sha, "_contract")
         contraction = {
+            "traffic": ((crec.get("dram_read") or 0) + (crec.get("dram_write") or 0)) if crec else None,
+            "hmma_active_pct": crec.get("hmma_active_pct") if crec else None,
             "kernel": "contract_kernel (+ prep, fold)",
             "bound": "tensor",
             "achieved": 2 * macs / t_contract_s / 1e12,

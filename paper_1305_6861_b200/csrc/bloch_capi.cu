@@ -260,7 +260,7 @@ Variant pick_variant(int prec, int64_t n, int ncp, int n_sm, bool win, int64_t p
 template <typename R, int S, int NC>
 void shape_one(const Variant& v, int* max_t, int* min_b) {
   if (v.prec == int(8 * sizeof(R)) && v.S == S && v.NC == NC) {
-    *max_t = bloch::KernelTraits<R, S, NC>::kMaxThreads;
+    *max_t = v.win ? bloch::KernelTraits<R, S, NC>::kMaxThreads : bloch::KernelTraits<R, S, NC>::kMaxThreadsNoWin;
     *min_b = v.win ? bloch::KernelTraits<R, S, NC>::kMinBlocks : bloch::KernelTraits<R, S, NC>::kMinBlocksNoWin;
   }
 }
@@ -859,7 +859,15 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
         if (op.kind == bloch::OP_WINDOW) win = true;
       }
       win = win || full;
-      Variant v = pick_variant(c->precision, n, ncp, c->n_sm, win, static_cast<int64_t>(P.planes.size()) * 16);
+      // the L2 working set of the stream: planes read by at least 4 ops (a snapshot at the end, for one,
+      // splits the last window's class off: those planes are read once)
+      std::vector<int32_t> refs(P.planes.size(), 0);
+      for (const bloch::DevOp& op : OPS)
+        for (int k = 0; k < 4; ++k)
+          if (op.pl[k] >= 0 && op.pl[k] < static_cast<int32_t>(refs.size())) refs[op.pl[k]]++;
+      int64_t hot = 0;
+      for (int32_t r : refs) hot += r >= 4;
+      Variant v = pick_variant(c->precision, n, ncp, c->n_sm, win, hot * 16);
       v.full = full;
       v.win = win;
       int max_t = 512, min_b = 1;
@@ -1100,6 +1108,11 @@ int bloch_last_phases(const bloch_ctx* c, float* integrate_ms, float* contract_m
                       int64_t* contracted_samples) {
   if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
   const bloch_ctx* s = c->subs.empty() ? c : c->subs[0];
+  if (s->device != BLOCH_HOST_ONLY && s->ev[3]) {  // asynchronous calls: wait for the call's last event
+    cudaSetDevice(s->device);
+    if (cudaEventSynchronize(s->ev[3]) == cudaSuccess) phase_times(const_cast<bloch_ctx*>(s));
+    cudaGetLastError();
+  }
   if (integrate_ms) *integrate_ms = s->integrate_ms;
   if (contract_ms) *contract_ms = s->contract_ms;
   if (n_groups) *n_groups = s->last_groups;
@@ -1209,6 +1222,7 @@ int bloch_last_timing(const bloch_ctx* c, float* kernel_ms, float* device_ms, in
       float k = 0.f, d = 0.f;
       if (cudaEventElapsedTime(&k, c->ev[1], c->ev[2]) == cudaSuccess) const_cast<bloch_ctx*>(c)->kernel_ms = k;
       if (cudaEventElapsedTime(&d, c->ev[0], c->ev[3]) == cudaSuccess) const_cast<bloch_ctx*>(c)->device_ms = d;
+      phase_times(const_cast<bloch_ctx*>(c));
     }
     cudaGetLastError();
   }

@@ -135,22 +135,32 @@ __device__ __forceinline__ void st_keep(double2* p, double2 v, uint64_t pol) {
 // spin state (shared memory, [3][S][blockDim] fp64) and per-spin constants
 // ---------------------------------------------------------------------------
 
-template <int S>
+// kReg: the state lives in registers (every access indexed by an unrolled slot loop); the kernels
+// without window / chirp / train code use it, the others keep it in shared memory
+template <int S, bool kReg = false>
 struct Spins {
+  static constexpr int kS = S;
   double* sm;
   int64_t base;  // spin index of slot 0 of this thread
   int bd;
   int64_t n;
   int nact;      // active slots: idx(s) < n exactly for s < nact (idx grows with s)
+  double v[kReg ? 3 : 1][kReg ? S : 1];
   __device__ __forceinline__ int64_t idx(int s) const { return base + static_cast<int64_t>(s) * bd; }
   __device__ __forceinline__ bool act(int s) const { return s < nact; }
   __device__ __forceinline__ void init_active() {
     const int64_t left = n - base;
     nact = left <= 0 ? 0 : static_cast<int>(left >= static_cast<int64_t>(S) * bd ? S : (left + bd - 1) / bd);
   }
-  __device__ __forceinline__ double& mx(int s) { return sm[(0 * S + s) * bd + threadIdx.x]; }
-  __device__ __forceinline__ double& my(int s) { return sm[(1 * S + s) * bd + threadIdx.x]; }
-  __device__ __forceinline__ double& mz(int s) { return sm[(2 * S + s) * bd + threadIdx.x]; }
+  __device__ __forceinline__ double& mx(int s) {
+    if constexpr (kReg) return v[0][s]; else return sm[(0 * S + s) * bd + threadIdx.x];
+  }
+  __device__ __forceinline__ double& my(int s) {
+    if constexpr (kReg) return v[1][s]; else return sm[(1 * S + s) * bd + threadIdx.x];
+  }
+  __device__ __forceinline__ double& mz(int s) {
+    if constexpr (kReg) return v[2][s]; else return sm[(2 * S + s) * bd + threadIdx.x];
+  }
 };
 
 // SpinConst (kernels.h): one 64-byte record per spin, 4 x 16-byte loads
@@ -225,8 +235,8 @@ __device__ __forceinline__ void rotate(const Mat3& m, double& x, double& y, doub
 }
 
 // one interval on spin s (on the fly): precession (+ relaxation), fp64 — engine.py:288-302
-template <int S>
-__device__ __forceinline__ void interval(const KParams& kp, Spins<S>& sp, int s, int flags, int cls, double dt,
+template <int S, class SP>
+__device__ __forceinline__ void interval(const KParams& kp, SP& sp, int s, int flags, int cls, double dt,
                                          double dmx, double dmy, double dmz) {
   if (!(flags & EV_MOVE) || !sp.act(s)) return;
   const int64_t i = sp.idx(s);
@@ -241,8 +251,8 @@ __device__ __forceinline__ void interval(const KParams& kp, Spins<S>& sp, int s,
 }
 
 // the fused pulse on its own pass over the state (paths that do not load the state anyway)
-template <int S>
-__device__ __forceinline__ void apply_pre(const KParams& kp, Spins<S>& sp, int pre, int mode) {
+template <int S, class SP>
+__device__ __forceinline__ void apply_pre(const KParams& kp, SP& sp, int pre, int mode) {
   const Mat3 m = load_mat(kp, pre);
   if (mode == 1) {  // about x: (x, r4 y + r5 z, r7 y + r8 z)
 #pragma unroll
@@ -844,7 +854,7 @@ __device__ __forceinline__ void chirp_f32(const KParams& kp, const DevOp* op, Sp
 // [3][S][bd] is addressed (component, slot) x bd + thread on every access; with a
 // constant bd those offsets are immediates.
 template <typename R, int S, int NC, bool kFull, int BD, bool kWin>
-__global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads,
+__global__ void __launch_bounds__(kWin ? KernelTraits<R, S, NC>::kMaxThreads : KernelTraits<R, S, NC>::kMaxThreadsNoWin,
                                   kWin ? KernelTraits<R, S, NC>::kMinBlocks : KernelTraits<R, S, NC>::kMinBlocksNoWin)
     integrate_kernel(const KParams kp) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -853,7 +863,10 @@ __global__ void __launch_bounds__(KernelTraits<R, S, NC>::kMaxThreads,
   constexpr bool kMma1 = sizeof(R) == 4 && NC == 1;                     // single-coil tensor-core windows
   const int bd = BD ? BD : static_cast<int>(blockDim.x);
   const int nw = bd >> 5;
-  Spins<S> sp;
+  // registers hold the state of up to 4 spins per thread; 8 spill (measured: config 1 S=8 3.94 vs 3.26 ms
+  // in shared memory; S <= 4 3-10% faster in registers, profiles/r2v_register_state_ab.txt)
+  constexpr bool kRegState = !kFull && !kWin && S <= 4;
+  Spins<S, kRegState> sp;
   sp.sm = reinterpret_cast<double*>(smem_raw);
   sp.base = static_cast<int64_t>(blockIdx.x) * kp.spins_per_cta + threadIdx.x;
   sp.bd = bd;
@@ -1825,6 +1838,7 @@ size_t integrate_smem_bytes(int threads, bool win) {
   size_t stage = 0;
   if constexpr (sizeof(R) == 4 && NC == 1) stage = kStageBytes;
   if constexpr (sizeof(R) == 4 && NC >= 2) stage = McStage<NC>::kBytes;
+  if (!win && S <= 4) return 0;  // the variant without window / chirp / train code: state in registers
   if (!win) stage = 0;
   return static_cast<size_t>(3 * S * threads) * sizeof(double) + static_cast<size_t>(threads / 32) * stage;
 }
@@ -1860,7 +1874,7 @@ static cudaError_t launch_bd(const KParams& kp, int grid, int threads, cudaStrea
 template <typename R, int S, int NC, bool kFull, bool kWin>
 static cudaError_t launch_one(const KParams& kp, int grid, int threads, cudaStream_t stream) {
 #ifndef BLOCH_NO_FIXED_BD
-  constexpr int kMax = KernelTraits<R, S, NC>::kMaxThreads;
+  constexpr int kMax = kWin ? KernelTraits<R, S, NC>::kMaxThreads : KernelTraits<R, S, NC>::kMaxThreadsNoWin;
   if constexpr (sizeof(R) == 4 && NC == 1 && S == 8 && !kFull) {
     if (threads == kMax) return launch_bd<R, S, NC, kFull, kMax, kWin>(kp, grid, threads, stream);
   }

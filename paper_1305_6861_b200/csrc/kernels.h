@@ -50,6 +50,7 @@ struct KernelTraits {
   static constexpr int kMaxThreads = 512;
   static constexpr int kMinBlocks = 1;
   static constexpr int kMinBlocksNoWin = 1;  // the variant without window code (every window deferred)
+  static constexpr int kMaxThreadsNoWin = 512;
 };
 #ifndef BLOCH_NOWIN_MINB
 #define BLOCH_NOWIN_MINB 2
@@ -59,6 +60,7 @@ struct KernelTraits<float, 8, 1> {  // the fp32 single-coil workhorse: 2 CTAs x 
   static constexpr int kMaxThreads = 320;   // measured: 1 x 16 warps 17.6 ms, 2 x 10 warps 14.1 ms,
   static constexpr int kMinBlocks = 2;      // 3 x 8 warps (80 regs, spills) 15.5 ms on config 1
   static constexpr int kMinBlocksNoWin = BLOCH_NOWIN_MINB;
+  static constexpr int kMaxThreadsNoWin = 320;
 };
 
 // (real type, spins per thread, coils) instantiated in bloch_kernels.cu
@@ -83,6 +85,7 @@ struct KernelTraits<float, 4, 1> {  // long windows (>= 384 samples): 2 CTAs x 1
   static constexpr int kMaxThreads = 384;
   static constexpr int kMinBlocks = 2;
   static constexpr int kMinBlocksNoWin = BLOCH_NOWIN_MINB;
+  static constexpr int kMaxThreadsNoWin = 320;  // register state: 102 registers, no spills (384: 80, spilling)
 };
 
 template <>
@@ -90,6 +93,7 @@ struct KernelTraits<float, 1, 1> {  // small blocks (spin shards): one spin per 
   static constexpr int kMaxThreads = 320;
   static constexpr int kMinBlocks = 2;
   static constexpr int kMinBlocksNoWin = BLOCH_NOWIN_MINB;
+  static constexpr int kMaxThreadsNoWin = 320;
 };
 
 template <>
@@ -97,6 +101,7 @@ struct KernelTraits<float, 1, 8> {  // small eight-coil blocks: one spin per thr
   static constexpr int kMaxThreads = 320;
   static constexpr int kMinBlocks = 2;
   static constexpr int kMinBlocksNoWin = BLOCH_NOWIN_MINB;
+  static constexpr int kMaxThreadsNoWin = 320;
 };
 
 template <typename R, int S, int NC>

@@ -1,4 +1,5 @@
-"""Per-launch ncu counters of the integrator per config -> profiles/ncu_counters.json (read by bench.py).
+"""Per-launch ncu counters of the integrator (and, for csv names containing "contract", of the window
+contraction) per config -> profiles/ncu_counters.json (read by bench.py).
 
 usage: python tools/ncu_counters.py OUT.json LIB_SHA16 cfg0.csv cfg1.csv ...   (one csv per config, from
   ncu --metrics smsp__inst_executed.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,
@@ -13,6 +14,7 @@ import re
 import sys
 
 UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3,
+         "ns": 1e-9, "us": 1e-6, "ms": 1e-3,
          "second": 1.0, "inst": 1, "Kinst": 1e3, "Minst": 1e6, "Ginst": 1e9, "hz": 1, "Khz": 1e3, "Mhz": 1e6,
          "Ghz": 1e9, "%": 1, "cycle/second": 1, "cycle/nsecond": 1e9, "cycle/usecond": 1e6}
 
@@ -34,7 +36,8 @@ for path in sys.argv[3:]:
         kname[r[ni]] = r[ki]
     n = len(per)
     mean = lambda m: sum(d.get(m, 0.0) for d in per.values()) / max(1, n)
-    res[f"config{cfg}"] = {
+    key = f"config{cfg}_contract" if "contract" in path.split("/")[-1] else f"config{cfg}"
+    res[key] = {
         "lib_sha16": sha, "launches": n, "kernel": next(iter(kname.values()))[:80] if kname else None,
         "inst_executed": mean("smsp__inst_executed.sum"), "dram_read": mean("dram__bytes_read.sum"),
         "dram_write": mean("dram__bytes_write.sum"), "duration_s": mean("gpu__time_duration.sum"),
