@@ -15,7 +15,8 @@
 //
 // The complex product is embedded as a real GEMM D = A B^T, K-dimension =
 // (spin, re/im), both operands K-major:
-//     A[(k, re)] = [Re z^k, -Im z^k],  A[(k, im)] = [Im z^k, Re z^k]  per spin  (M: 2 rows per sample)
+//     A[(k, re)] = [Re z^k, -Im z^k],  A[(k, im)] = [Im z^k, Re z^k]  per spin  (M: 2 rows per sample;
+//                                       an M-tile is 64 real rows then the 64 imaginary rows)
 //     B[w]       = [Re U, Im U]                                        per spin  (N: windows)
 // so D[(k, re)][w] = Re S, D[(k, im)][w] = Im S.  Every operand is split into
 // bf16 parts x = hi + lo and the product runs as three kind::f16 passes

@@ -205,29 +205,32 @@ __global__ void __launch_bounds__(ct::kThreads, 1)
       }
     }
   } else {
-    // ---- generators: warp q owns samples [8 MT q, 8 MT (q+1)) of the tile, lanes 0-15 the even ones
-    // and lanes 16-31 the odd ones (of spin lane & 15), so one STS.32 of the warp covers two rows 64 B
-    // apart in bank space: conflict-free in the swizzled layout
+    // ---- generators.  An M-tile holds 64 samples: row r = the sample's real row [Re z^k, -Im z^k],
+    // row 64 + r its imaginary row [Im z^k, Re z^k].  Warp q owns samples [8 MT q, 8 MT (q+1)) of the
+    // tile, lanes 0-15 the even ones and lanes 16-31 the odd ones (of spin lane & 15): every STS.32 of
+    // the warp covers an even and an odd 64-B row, i.e. banks 0-15 and 16-31, and the SWIZZLE_64B chunk
+    // permutation ((row >> 1) & 3) is the same for both halves
     const int q = warp - 2, half = lane >> 4, sl = lane & 15;
     constexpr int kSamp = 64 * MT / ct::kGenWarps;  // samples per warp per stage
     constexpr int kVals = kSamp / 2;                // per lane
     const int m = (kSamp * q) >> 6;
-    const int rr0 = ((kSamp * q) & 63) + half;
-    const int kfirst = k0 + kSamp * q + half;  // absolute sample of value 0
-    const uint32_t off0 = m * ct::kTileBytes + 128 * rr0 + ((sl & 3) << 2);
-    const uint32_t ch_e = (((sl >> 2) ^ half) << 4), ch_o = (((sl >> 2) ^ (half ^ 2)) << 4);
-    const uint32_t sw = half ? 64u : 0u;  // offset of this half's first store (the im row for the odd half)
+    const int r0 = ((kSamp * q) & 63) + half;     // row of value 0 (value v: r0 + 2 v)
+    const int kfirst = k0 + kSamp * q + half;     // absolute sample of value 0
+    const uint32_t off0 = m * ct::kTileBytes + 64 * r0 + ((sl & 3) << 2);
+    uint32_t chk[4];                              // swizzled 16-B chunk of this lane's spin, by (row >> 1) & 3
+#pragma unroll
+    for (int x = 0; x < 4; ++x) chk[x] = ((sl >> 2) ^ ((((kSamp * q) & 63) >> 1) + x & 3)) << 4;
     // ---- drain of accumulation segment e: TMEM lanes of this warp's quarter (two warps per quarter,
     // half of the columns each) -> partial slot (chunk, e); the MMA of the next segment waits for the
     // generator warps' acc_empty arrivals
     const int quarter = warp & 3, colh = q >> 2;
-    const int row = 32 * quarter + lane;  // accumulator row: sample k0 + 64 m + row / 2, component row & 1
+    const int row = 32 * quarter + lane;  // accumulator row: sample k0 + 64 m + (row & 63), component row >> 6
     auto drain = [&](int e) {
       ct::mbar_wait(acc_full, e & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       float* slot = j.part + ((static_cast<int64_t>(kc) * p.segs + e) * j.C + coil) * j.W * j.K * 2;
       for (int mm = 0; mm < MT; ++mm) {
-        const int k = k0 + 64 * mm + (row >> 1);
+        const int k = k0 + 64 * mm + (row & 63);
         for (int c0 = 16 * colh; c0 < nw; c0 += 32) {
           uint32_t r[16];
           const uint32_t addr = tmem + (static_cast<uint32_t>(32 * quarter) << 16) + static_cast<uint32_t>(mm * nw + c0);
@@ -241,7 +244,7 @@ __global__ void __launch_bounds__(ct::kThreads, 1)
 #pragma unroll
             for (int c = 0; c < 16; ++c) {
               const int w = w0 + c0 + c;
-              if (w < j.W) slot[(static_cast<int64_t>(w) * j.K + k) * 2 + (row & 1)] = __uint_as_float(r[c]);
+              if (w < j.W) slot[(static_cast<int64_t>(w) * j.K + k) * 2 + (row >> 6)] = __uint_as_float(r[c]);
             }
           }
         }
@@ -289,9 +292,7 @@ __global__ void __launch_bounds__(ct::kThreads, 1)
         P = make_float2(cwc.x * z0.x - cwc.y * z0.y, cwc.x * z0.y + cwc.y * z0.x);  // the coil weight rides along
         Q = czq;
       }
-      unsigned char* ah = A(s, 0);
-      unsigned char* ae = ah + off0 + ch_e;
-      unsigned char* ao = ah + off0 + ch_o;
+      unsigned char* ab = A(s, 0) + off0;
 #pragma unroll
       for (int v = 0; v < kVals; ++v) {
         // bf16 hi parts rounded to nearest (Veltkamp, both components packed) and the residuals
@@ -300,15 +301,11 @@ __global__ void __launch_bounds__(ct::kThreads, 1)
         const float2 d = __fadd2_rn(c, make_float2(-P.x, -P.y));
         const float2 hi = __fadd2_rn(c, make_float2(-d.x, -d.y));
         const float2 lo = __fadd2_rn(P, make_float2(-hi.x, -hi.y));
-        unsigned char* o = ((v & 1) ? ao : ae) + 256 * v;
-        // row (k, re) = [Re z^k, -Im z^k], row (k, im) = [Im z^k, Re z^k]; the odd half-warp stores
-        // its im row first, so each STS covers banks 0-15 with one half and 16-31 with the other
-        const uint32_t hre = ct::pack2(hi.x, -hi.y), him = ct::pack2(hi.y, hi.x);
-        const uint32_t lre = ct::pack2(lo.x, -lo.y), lim = ct::pack2(lo.y, lo.x);
-        *reinterpret_cast<uint32_t*>(o + sw) = half ? him : hre;
-        *reinterpret_cast<uint32_t*>(o + (64 - sw)) = half ? hre : him;
-        *reinterpret_cast<uint32_t*>(o + a_bytes + sw) = half ? lim : lre;
-        *reinterpret_cast<uint32_t*>(o + a_bytes + (64 - sw)) = half ? lre : lim;
+        unsigned char* o = ab + 128 * v + chk[v & 3];
+        *reinterpret_cast<uint32_t*>(o) = ct::pack2(hi.x, -hi.y);                   // real row
+        *reinterpret_cast<uint32_t*>(o + 4096) = ct::pack2(hi.y, hi.x);             // imaginary row
+        *reinterpret_cast<uint32_t*>(o + a_bytes) = ct::pack2(lo.x, -lo.y);
+        *reinterpret_cast<uint32_t*>(o + a_bytes + 4096) = ct::pack2(lo.y, lo.x);
         const float nx = P.x * Q.x - P.y * Q.y;
         P.y = P.x * Q.y + P.y * Q.x;
         P.x = nx;

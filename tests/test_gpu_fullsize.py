@@ -95,3 +95,26 @@ def test_full_lattice_subset_vs_oracle(index):
     ot = O.precompute_tables(w.sequence, snapshot_times=(w.sequence.end_time,))
     o_e, o_s = O.compute_block(ot, sub.pos, sub.mx, sub.my, sub.mz, sub.t1, sub.t2, sub.m0, sub.domega, sub.weight)
     assert O.rel_l2(o_e, g_e) <= 2e-5 and O.rel_l2(o_s[0], g_s[0]) <= 1e-9
+
+
+@pytest.mark.parametrize("index", [1, 2, 3, 4])
+def test_fullsize_contraction_matches_integrator_sums(index):
+    """The tensor-core window contraction against the integrator's own per-warp window sums, every spin of
+    the config (both within the BASELINE.json k-space tolerance of each other; each path is pinned to the
+    reference's goldens separately)."""
+    from paper_1305_6861_b200.engine import get_engine
+
+    w, tables = _workload(index)
+    b = w.block
+    eng = get_engine(0, 32)
+    on_e, on_s = compute_block(tables, b)
+    assert eng.last_phases()["groups"] >= 1
+    eng.set_contraction(False)
+    try:
+        off_e, off_s = compute_block(tables, b)
+    finally:
+        eng.set_contraction(True)
+    assert O.rel_l2(off_e, on_e) <= 1e-4
+    # the spin state does not depend on how the samples are summed (same fp64 propagators; different kernel
+    # instances may contract a product into an FMA differently)
+    assert O.rel_l2(off_s[0], on_s[0]) <= 1e-12

@@ -4,7 +4,8 @@ With a tiny BLOCH_PARTIAL_BUDGET_MB the op stream runs as many launches, the fp6
 state handed over through global memory and each segment's samples folded
 before the next; echoes and snapshots must be bit-identical to one launch, for
 programs with windows, chirps, generic samples, RF trains and snapshots, in
-both precisions and with several coils."""
+both precisions and with several coils.  The window contraction is off here: it keeps no partial rows
+(its U rows must fit the budget, else the windows stay in the integrator, tested below)."""
 
 import json
 import os
@@ -35,6 +36,7 @@ name, precision, out = sys.argv[2], int(sys.argv[3]), sys.argv[4]
 rec = load_golden(name)
 t = precompute_sequence_tables(cases.small_cases()[name]["sequence"], snapshot_times=tuple(rec["snapshot_times"].tolist()))
 eng = get_engine(0, precision)
+eng.set_contraction(False)  # the integrator's own window sums: the rows the segments bound
 e, s = eng.compute(t, rec["spin_pos"], rec["spin_mx"], rec["spin_my"], rec["spin_mz"], rec["spin_t1"], rec["spin_t2"],
                    rec["spin_m0"], rec["spin_domega"], rec["spin_weight"])
 np.savez(out, echoes=e, **{f"snap{i}": x for i, x in enumerate(s) if x is not None})
@@ -51,7 +53,14 @@ def test_segmented_program_bit_identical(name, precision, tmp_path):
     b = SpinBlock(index=0, pos=rec["spin_pos"], mx=rec["spin_mx"], my=rec["spin_my"], mz=rec["spin_mz"],
                   t1=rec["spin_t1"], t2=rec["spin_t2"], m0=rec["spin_m0"], domega=rec["spin_domega"],
                   weight=rec["spin_weight"])
-    e1, s1 = compute_block(t, b, precision=precision)
+    from paper_1305_6861_b200.engine import get_engine
+
+    eng = get_engine(0, precision)
+    eng.set_contraction(False)
+    try:
+        e1, s1 = compute_block(t, b, precision=precision)
+    finally:
+        eng.set_contraction(True)
     out = str(tmp_path / "seg.npz")
     env = dict(os.environ, BLOCH_PARTIAL_BUDGET_MB="0.002")  # ~2 KB of partial rows per launch
     r = subprocess.run([sys.executable, "-c", _CHILD, ROOT, name, str(precision), out], capture_output=True,
@@ -64,3 +73,24 @@ def test_segmented_program_bit_identical(name, precision, tmp_path):
     for i, x in enumerate(s1):
         if x is not None:
             assert np.array_equal(got[f"snap{i}"], x), i
+
+
+@pytest.mark.parametrize("name", ["tse16", "mixed_coils"])
+def test_contraction_over_budget_falls_back_to_integrator_sums(name, tmp_path):
+    """A partial budget too small for the U rows: the call runs without the contraction (every window summed by
+    the integrator, in segments) and still matches the reference golden."""
+    from oracle.bloch_oracle import rel_l2
+
+    rec = load_golden(name)
+    out = str(tmp_path / "seg.npz")
+    child = _CHILD.replace("eng.set_contraction(False)  # the integrator's own window sums: the rows the segments bound\n",
+                           "")
+    child += "print(json.dumps({'groups': eng.last_phases()['groups']}))\n"
+    env = dict(os.environ, BLOCH_PARTIAL_BUDGET_MB="0.002")
+    r = subprocess.run([sys.executable, "-c", child, ROOT, name, "32", out], capture_output=True, text=True, env=env,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    info = json.loads(r.stdout.strip().splitlines()[-1])
+    assert info["groups"] == 0
+    got = np.load(out)
+    assert rel_l2(rec["echo_full"], got["echoes"]) <= 1e-4

@@ -41,7 +41,8 @@ for it in range(8):
     tm = e.last_timing()
     if it >= 3: ks.append(tm['kernel_ms']); ds.append(tm['device_ms'])
 L = e.last_launch()
-print('cfg{cfg} 1/{nsh} n=%d S=%d grid=%d thr=%d kernel_ms %.3f device_ms %.3f' % (hi - lo, L['spins_per_thread'], L['grid'], L['threads'], min(ks), min(ds)))
+ph = e.last_phases()
+print('cfg{cfg} 1/{nsh} n=%d S=%d grid=%d thr=%d kernel_ms %.3f device_ms %.3f integrate_ms %.3f contract_ms %.3f' % (hi - lo, L['spins_per_thread'], L['grid'], L['threads'], min(ks), min(ds), ph['integrate_ms'], ph['contract_ms']))
 """
         r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
         print(r.stdout.strip() or r.stderr[-800:], flush=True)
