@@ -214,6 +214,42 @@ __device__ __forceinline__ RotCoef load_rot(const KParams& kp, const DevOp* op, 
   return RotCoef{a.x, a.y, b.x, b.y, d.x, d.y, e.x, e.y};
 }
 
+// L1 prefetch of the read-only plane values the next op will load for this thread's spins (the
+// register-state kernels, whose L1 is not shared with a spin-state carve-out): the op's L2 round trip
+// overlaps the current op instead of opening the next one.  Progression running factors are
+// read-modify-written through L2 (ld.cg) and are not prefetched.
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+template <class SP>
+__device__ __forceinline__ void prefetch_next_op(const KParams& kp, const DevOp* nop, SP& sp) {
+  const int kind = __ldg(&nop->kind);
+  int a = -1, b = -1, c = -1, d = -1;  // fp64 planes a, b; fp32 sample planes c, d
+  if (kind == OP_EVENT) {
+    if (__ldg(&nop->rot) >= 0) {
+      a = __ldg(&nop->pl[0]);
+      b = __ldg(&nop->pl[1]);
+    } else if (__ldg(&nop->prg) >= 0) {
+      a = __ldg(&nop->pl[__ldg(&nop->flags) == 2 ? 2 : 1]);
+      b = __ldg(&nop->pl[3]);
+    }
+  } else if (kind == OP_UWIN) {
+    a = __ldg(&nop->pl[2]);
+    b = __ldg(&nop->pl[3]);
+    c = __ldg(&nop->pl[0]);
+    d = __ldg(&nop->pl[1]);
+  }
+#pragma unroll
+  for (int s = 0; s < SP::kS; ++s) {
+    if (!sp.act(s)) continue;
+    const int64_t i = sp.idx(s);
+    if (a >= 0) prefetch_l1(kp.planes + static_cast<int64_t>(a) * kp.n + i);
+    if (b >= 0) prefetch_l1(kp.planes + static_cast<int64_t>(b) * kp.n + i);
+    if (c >= 0 && kp.planes32) prefetch_l1(kp.planes32 + static_cast<int64_t>(c) * kp.n + i);
+    if (d >= 0 && kp.planes32) prefetch_l1(kp.planes32 + static_cast<int64_t>(d) * kp.n + i);
+  }
+}
+
 // a hard pulse fused into the following op (DevOp.pre): 9 uniform matrix entries, bloch.py:124-139
 struct Mat3 {
   double r[9];
@@ -889,6 +925,11 @@ __global__ void __launch_bounds__(kWin ? KernelTraits<R, S, NC>::kMaxThreads : K
   for (int o = kp.op_begin; o < kp.n_ops; ++o) {
     const DevOp* op = kp.ops + o;
     const int kind = __ldg(&op->kind);
+#ifndef BLOCH_NO_L1_PREFETCH
+    if constexpr (kRegState) {
+      if (o + 1 < kp.n_ops) prefetch_next_op(kp, op + 1, sp);
+    }
+#endif
 
     if (kind == OP_ROT) {  // engine.py:277-283
       double r[9];
@@ -990,19 +1031,20 @@ __global__ void __launch_bounds__(kWin ? KernelTraits<R, S, NC>::kMaxThreads : K
       constexpr int G = S < 4 ? S : 4;
 #pragma unroll
       for (int g0 = 0; g0 < S; g0 += G) {
-        double2 c[G], ab[G], cp[G], zz[G];
+        double2 c[G], ab[G];
+        float2 cp[G], zz[G];  // Cpre and z only form U (bf16 hi + lo, ~2^-16): fp32 suffices
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           const int64_t i = sp.act(g0 + g) ? sp.idx(g0 + g) : 0;
           c[g] = __ldg(pc + i);
           ab[g] = __ldg(pab + i);
           if constexpr (sizeof(R) == 4) {  // Cpre and z are PL_SAMPLE planes: float2 in the fp32 mode
-            const float2 a = __ldg(plane32_at(kp, pcp, i)), b = __ldg(plane32_at(kp, pz, i));
-            cp[g] = make_double2(a.x, a.y);
-            zz[g] = make_double2(b.x, b.y);
+            cp[g] = __ldg(plane32_at(kp, pcp, i));
+            zz[g] = __ldg(plane32_at(kp, pz, i));
           } else {
-            cp[g] = __ldg(plane_at(kp, pcp, i));
-            zz[g] = __ldg(plane_at(kp, pz, i));
+            const double2 a = __ldg(plane_at(kp, pcp, i)), b = __ldg(plane_at(kp, pz, i));
+            cp[g] = make_float2(static_cast<float>(a.x), static_cast<float>(a.y));
+            zz[g] = make_float2(static_cast<float>(b.x), static_cast<float>(b.y));
           }
         }
 #pragma unroll
@@ -1010,14 +1052,15 @@ __global__ void __launch_bounds__(kWin ? KernelTraits<R, S, NC>::kMaxThreads : K
           const int s = g0 + g;
           const double x = sp.mx(s), y = sp.my(s);
           if (sp.act(s)) {
-            double ur = cp[g].x * x - cp[g].y * y, ui = cp[g].x * y + cp[g].y * x;
+            const float fx = static_cast<float>(x), fy = static_cast<float>(y);
+            float ur = cp[g].x * fx - cp[g].y * fy, ui = cp[g].x * fy + cp[g].y * fx;
             if (!lead) {  // the first sample follows one interval
-              const double t = ur * zz[g].x - ui * zz[g].y;
+              const float t = ur * zz[g].x - ui * zz[g].y;
               ui = ur * zz[g].y + ui * zz[g].x;
               ur = t;
             }
             uint32_t hi, lo;
-            contract_split(ur, ui, hi, lo);
+            contract_split_f(ur, ui, hi, lo);
             const int64_t q = contract_u_index(kp.urows, row, sp.idx(s));
             __stcs(kp.uhi + q, hi);  // streamed: read back by the contraction
             __stcs(kp.ulo + q, lo);

@@ -94,6 +94,17 @@ __host__ __device__ inline uint32_t bf16_rn_bits(float f) {
   memcpy(&u, &f, 4);
   return (u + 0x7fffu + ((u >> 16) & 1u)) & 0xffff0000u;
 }
+// U word pair of an fp32 complex value: hi = bf16x2 (Re, Im) rounded, lo = bf16x2 of the residuals (the
+// integrator's path: no fp64 <-> fp32 conversions beyond the state's own)
+__host__ __device__ inline void contract_split_f(float re, float im, uint32_t& hi, uint32_t& lo) {
+  const uint32_t hr = bf16_rn_bits(re), hm = bf16_rn_bits(im);
+  float fr, fm;
+  memcpy(&fr, &hr, 4);
+  memcpy(&fm, &hm, 4);
+  const uint32_t lr = bf16_rn_bits(re - fr), lm = bf16_rn_bits(im - fm);  // exact residuals
+  hi = (hr >> 16) | hm;
+  lo = (lr >> 16) | lm;
+}
 // U word pair of a complex value: hi = bf16x2 (Re, Im) rounded, lo = bf16x2 of the residuals
 __host__ __device__ inline void contract_split(double re, double im, uint32_t& hi, uint32_t& lo) {
   const uint32_t hr = bf16_rn_bits(static_cast<float>(re)), hm = bf16_rn_bits(static_cast<float>(im));

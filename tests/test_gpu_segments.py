@@ -86,7 +86,7 @@ def test_contraction_over_budget_falls_back_to_integrator_sums(name, tmp_path):
     child = _CHILD.replace("eng.set_contraction(False)  # the integrator's own window sums: the rows the segments bound\n",
                            "")
     child += "print(json.dumps({'groups': eng.last_phases()['groups']}))\n"
-    env = dict(os.environ, BLOCH_PARTIAL_BUDGET_MB="0.002")
+    env = dict(os.environ, BLOCH_PARTIAL_BUDGET_MB="0.00001")  # ~10 bytes: below any U array
     r = subprocess.run([sys.executable, "-c", child, ROOT, name, "32", out], capture_output=True, text=True, env=env,
                        timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
