@@ -214,42 +214,6 @@ __device__ __forceinline__ RotCoef load_rot(const KParams& kp, const DevOp* op, 
   return RotCoef{a.x, a.y, b.x, b.y, d.x, d.y, e.x, e.y};
 }
 
-// L1 prefetch of the read-only plane values the next op will load for this thread's spins (the
-// register-state kernels, whose L1 is not shared with a spin-state carve-out): the op's L2 round trip
-// overlaps the current op instead of opening the next one.  Progression running factors are
-// read-modify-written through L2 (ld.cg) and are not prefetched.
-__device__ __forceinline__ void prefetch_l1(const void* p) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
-template <class SP>
-__device__ __forceinline__ void prefetch_next_op(const KParams& kp, const DevOp* nop, SP& sp) {
-  const int kind = __ldg(&nop->kind);
-  int a = -1, b = -1, c = -1, d = -1;  // fp64 planes a, b; fp32 sample planes c, d
-  if (kind == OP_EVENT) {
-    if (__ldg(&nop->rot) >= 0) {
-      a = __ldg(&nop->pl[0]);
-      b = __ldg(&nop->pl[1]);
-    } else if (__ldg(&nop->prg) >= 0) {
-      a = __ldg(&nop->pl[__ldg(&nop->flags) == 2 ? 2 : 1]);
-      b = __ldg(&nop->pl[3]);
-    }
-  } else if (kind == OP_UWIN) {
-    a = __ldg(&nop->pl[2]);
-    b = __ldg(&nop->pl[3]);
-    c = __ldg(&nop->pl[0]);
-    d = __ldg(&nop->pl[1]);
-  }
-#pragma unroll
-  for (int s = 0; s < SP::kS; ++s) {
-    if (!sp.act(s)) continue;
-    const int64_t i = sp.idx(s);
-    if (a >= 0) prefetch_l1(kp.planes + static_cast<int64_t>(a) * kp.n + i);
-    if (b >= 0) prefetch_l1(kp.planes + static_cast<int64_t>(b) * kp.n + i);
-    if (c >= 0 && kp.planes32) prefetch_l1(kp.planes32 + static_cast<int64_t>(c) * kp.n + i);
-    if (d >= 0 && kp.planes32) prefetch_l1(kp.planes32 + static_cast<int64_t>(d) * kp.n + i);
-  }
-}
-
 // a hard pulse fused into the following op (DevOp.pre): 9 uniform matrix entries, bloch.py:124-139
 struct Mat3 {
   double r[9];
@@ -925,11 +889,6 @@ __global__ void __launch_bounds__(kWin ? KernelTraits<R, S, NC>::kMaxThreads : K
   for (int o = kp.op_begin; o < kp.n_ops; ++o) {
     const DevOp* op = kp.ops + o;
     const int kind = __ldg(&op->kind);
-#ifndef BLOCH_NO_L1_PREFETCH
-    if constexpr (kRegState) {
-      if (o + 1 < kp.n_ops) prefetch_next_op(kp, op + 1, sp);
-    }
-#endif
 
     if (kind == OP_ROT) {  // engine.py:277-283
       double r[9];
@@ -1052,15 +1011,31 @@ __global__ void __launch_bounds__(kWin ? KernelTraits<R, S, NC>::kMaxThreads : K
           const int s = g0 + g;
           const double x = sp.mx(s), y = sp.my(s);
           if (sp.act(s)) {
-            const float fx = static_cast<float>(x), fy = static_cast<float>(y);
-            float ur = cp[g].x * fx - cp[g].y * fy, ui = cp[g].x * fy + cp[g].y * fx;
-            if (!lead) {  // the first sample follows one interval
-              const float t = ur * zz[g].x - ui * zz[g].y;
-              ui = ur * zz[g].y + ui * zz[g].x;
-              ur = t;
-            }
             uint32_t hi, lo;
-            contract_split_f(ur, ui, hi, lo);
+            // u in fp32 (two conversions of the state) or in fp64 (split with fp64 residuals): equal to
+            // ~2^-24, well inside the bf16 hi + lo split; the faster one per variant, measured same-box:
+            // S = 8 fp32 3.23 vs 3.34 ms (config 1), S = 1 1.39 vs 1.41 (config 2 / 8), S = 4 fp64 8.65 vs
+            // 8.80 (config 2) and 2.38 vs 2.63 (config 2 / 2), profiles/r2z_u_split_ab.txt
+            constexpr bool kU32 = S == 8 || S == 1;
+            if constexpr (kU32) {
+              const float fx = static_cast<float>(x), fy = static_cast<float>(y);
+              float ur = cp[g].x * fx - cp[g].y * fy, ui = cp[g].x * fy + cp[g].y * fx;
+              if (!lead) {  // the first sample follows one interval
+                const float t = ur * zz[g].x - ui * zz[g].y;
+                ui = ur * zz[g].y + ui * zz[g].x;
+                ur = t;
+              }
+              contract_split_f(ur, ui, hi, lo);
+            } else {
+              const double cr = cp[g].x, ci = cp[g].y, zr = zz[g].x, zi = zz[g].y;
+              double ur = cr * x - ci * y, ui = cr * y + ci * x;
+              if (!lead) {
+                const double t = ur * zr - ui * zi;
+                ui = ur * zi + ui * zr;
+                ur = t;
+              }
+              contract_split(ur, ui, hi, lo);
+            }
             const int64_t q = contract_u_index(kp.urows, row, sp.idx(s));
             __stcs(kp.uhi + q, hi);  // streamed: read back by the contraction
             __stcs(kp.ulo + q, lo);

@@ -60,7 +60,8 @@ constexpr int kContractMaxSamples = 4096;  // windows up to this long (the fp32 
 
 struct ContractPlan {
   int mt;          // 64-sample M-tiles per CTA (1, 2, 4)
-  int nw;          // windows per CTA (MMA N, multiple of 16, <= 256)
+  int nw;          // windows per N-subtile (MMA N, multiple of 16, <= 256)
+  int nsub;        // N-subtiles per CTA (1 or 2): the CTA covers nsub * nw windows, one generated A tile
   int tiles_k;     // CTA tiles along the samples (all coils: C x tiles per coil)
   int tpc;         // CTA sample tiles per coil
   int tiles_w;     // CTA tiles along the windows

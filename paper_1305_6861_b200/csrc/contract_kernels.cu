@@ -112,9 +112,10 @@ __global__ void __launch_bounds__(ct::kThreads, 1)
   // that the stores below stay STS
   unsigned char* smem = smem_raw + ((1024u - (ct::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nw = p.nw, depth = p.depth;
+  const int nw = p.nw, nsub = p.nsub, depth = p.depth;
+  const int ncol = nsub * nw;                        // windows (accumulator columns) per M-tile
   const int a_bytes = MT * ct::kTileBytes;           // one of A hi / A lo
-  const int b_bytes = nw * ct::kRowBytes;            // one of B hi / B lo
+  const int b_bytes = ncol * ct::kRowBytes;          // one of B hi / B lo
   const int stage_bytes = 2 * a_bytes + 2 * b_bytes;
   auto A = [&](int s, int part) { return smem + s * stage_bytes + part * a_bytes; };
   auto B = [&](int s, int part) { return smem + s * stage_bytes + 2 * a_bytes + part * b_bytes; };
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(ct::kThreads, 1)
   const int rest = blockIdx.x / p.tiles_k;
   const int tw = rest % p.tiles_w, kc = rest / p.tiles_w;
   const int coil = tk / p.tpc;
-  const int k0 = (tk - coil * p.tpc) * 64 * MT, w0 = tw * nw;
+  const int k0 = (tk - coil * p.tpc) * 64 * MT, w0 = tw * ncol;
   const int64_t total_st = (j.n + ct::kStageSpins - 1) / ct::kStageSpins;
   const int64_t st0 = static_cast<int64_t>(kc) * p.stages;
   const int nst = static_cast<int>(min(static_cast<int64_t>(p.stages), total_st - st0));
@@ -167,8 +168,10 @@ __global__ void __launch_bounds__(ct::kThreads, 1)
         if (t >= depth) ct::mbar_wait(empty + s, ((t / depth) - 1) & 1);
         ct::mbar_expect_tx(full_u + s, 2u * static_cast<uint32_t>(b_bytes));
         const int blk = static_cast<int>(st0 + t);  // 16-spin block = stage
-        ct::tma_load_3d(B(s, 0), &map_hi, full_u + s, 0, j.row0 + w0, blk);
-        ct::tma_load_3d(B(s, 1), &map_lo, full_u + s, 0, j.row0 + w0, blk);
+        for (int sub = 0; sub < nsub; ++sub) {
+          ct::tma_load_3d(B(s, 0) + sub * nw * ct::kRowBytes, &map_hi, full_u + s, 0, j.row0 + w0 + sub * nw, blk);
+          ct::tma_load_3d(B(s, 1) + sub * nw * ct::kRowBytes, &map_lo, full_u + s, 0, j.row0 + w0 + sub * nw, blk);
+        }
       }
     }
   } else if (warp == 1) {
@@ -189,14 +192,17 @@ __global__ void __launch_bounds__(ct::kThreads, 1)
 #pragma unroll
           for (int m = 0; m < MT; ++m) {
             const uint32_t ah = ct::smem_u32(A(s, 0)) + m * ct::kTileBytes, al = ct::smem_u32(A(s, 1)) + m * ct::kTileBytes;
-            const uint32_t d = tmem + static_cast<uint32_t>(m * nw);
+            for (int sub = 0; sub < nsub; ++sub) {
+              const uint32_t d = tmem + static_cast<uint32_t>((m * nsub + sub) * nw);
+              const uint32_t bo = sub * nw * ct::kRowBytes;
 #pragma unroll
-            for (int ks = 0; ks < 2; ++ks) {  // two K steps of 16 bf16 (32 B) per 64-B row
-              const uint32_t o = ks * 32;
-              const uint32_t acc = (!first || ks > 0) ? 1u : 0u;
-              ct::mma_bf16(d, ct::sw64_desc(ah + o), ct::sw64_desc(bh + o), idesc, acc);
-              ct::mma_bf16(d, ct::sw64_desc(ah + o), ct::sw64_desc(bl + o), idesc, 1u);
-              ct::mma_bf16(d, ct::sw64_desc(al + o), ct::sw64_desc(bh + o), idesc, 1u);
+              for (int ks = 0; ks < 2; ++ks) {  // two K steps of 16 bf16 (32 B) per 64-B row
+                const uint32_t o = ks * 32;
+                const uint32_t acc = (!first || ks > 0) ? 1u : 0u;
+                ct::mma_bf16(d, ct::sw64_desc(ah + o), ct::sw64_desc(bh + bo + o), idesc, acc);
+                ct::mma_bf16(d, ct::sw64_desc(ah + o), ct::sw64_desc(bl + bo + o), idesc, 1u);
+                ct::mma_bf16(d, ct::sw64_desc(al + o), ct::sw64_desc(bh + bo + o), idesc, 1u);
+              }
             }
           }
         }
@@ -231,9 +237,9 @@ __global__ void __launch_bounds__(ct::kThreads, 1)
       float* slot = j.part + ((static_cast<int64_t>(kc) * p.segs + e) * j.C + coil) * j.W * j.K * 2;
       for (int mm = 0; mm < MT; ++mm) {
         const int k = k0 + 64 * mm + (row & 63);
-        for (int c0 = 16 * colh; c0 < nw; c0 += 32) {
+        for (int c0 = 16 * colh; c0 < ncol; c0 += 32) {
           uint32_t r[16];
-          const uint32_t addr = tmem + (static_cast<uint32_t>(32 * quarter) << 16) + static_cast<uint32_t>(mm * nw + c0);
+          const uint32_t addr = tmem + (static_cast<uint32_t>(32 * quarter) << 16) + static_cast<uint32_t>(mm * ncol + c0);
           asm volatile(
               "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
@@ -253,7 +259,7 @@ __global__ void __launch_bounds__(ct::kThreads, 1)
       __syncwarp();
       if (lane == 0) ct::mbar_arrive(acc_empty);
     };
-    // per-spin phase tables of the next stage are loaded one stage ahead
+    // per-spin phase tables are loaded two stages ahead (one stage of generation does not cover an L2 miss)
     auto load_z = [&](int t, float4& zt, float2& zq, float2& wc) {
       const int64_t i = (st0 + t) * ct::kStageSpins + sl;
       if (t < nst && i < j.n) {
@@ -265,15 +271,19 @@ __global__ void __launch_bounds__(ct::kThreads, 1)
         zq = wc = make_float2(0.f, 0.f);
       }
     };
-    float4 nzt;
-    float2 nzq, nwc;
+    float4 nzt, mzt;
+    float2 nzq, nwc, mzq, mwc;
     load_z(0, nzt, nzq, nwc);
+    load_z(1, mzt, mzq, mwc);
     const float kf = static_cast<float>(kfirst);
     int e_next = 0;  // next segment to drain
     for (int t = 0; t < nst; ++t) {
       const float4 czt = nzt;
       const float2 czq = nzq, cwc = nwc;
-      load_z(t + 1, nzt, nzq, nwc);
+      nzt = mzt;
+      nzq = mzq;
+      nwc = mwc;
+      load_z(t + 2, mzt, mzq, mwc);
       const int s = t % depth;
       if (t >= depth) {
         ct::mbar_wait(empty + s, ((t / depth) - 1) & 1);
@@ -368,21 +378,30 @@ __global__ void contract_fold_kernel(const float* __restrict__ part, int chunks,
 
 ContractPlan contract_plan(int K, int W, int64_t n, int n_sm, int C) {
   ContractPlan p{};
-  // windows per CTA: the fewest tiles of at most 256, split evenly (W = 384: two tiles of 192, not 256 + 128)
-  const int tw = (W + 255) / 256;
-  p.nw = (((W + tw - 1) / tw + 15) / 16) * 16;
+  // windows per CTA: up to two N-subtiles of <= 256 sharing one generated A tile (generation per MMA
+  // halves; the U tile is then re-read by twice as many sample tiles), split evenly (W = 384: 2 x 192)
+  static const int nsub_env = [] {
+    const char* e = getenv("BLOCH_CONTRACT_NSUB");
+    return e ? atoi(e) : 0;
+  }();
+  const int Wr = ((W + 15) / 16) * 16;
+  // two N-subtiles only while the pipeline stays 3 deep (W <= 384): config 4 (W = 384) contraction
+  // 5.54 -> 5.36 ms; config 2 (W = 512, depth 2) 3.65 -> 3.81 ms, kept at one (profiles/r2aa_nsub.txt)
+  p.nsub = nsub_env == 1 ? 1 : (nsub_env == 2 ? 2 : (Wr > 256 && Wr <= 384 ? 2 : 1));
+  const int tw = (W + 256 * p.nsub - 1) / (256 * p.nsub);
+  p.nw = (((W + tw * p.nsub - 1) / (tw * p.nsub) + 15) / 16) * 16;
   if (p.nw < 16) p.nw = 16;
   const int ktiles64 = (K + 63) / 64;
   p.mt = 1;
   for (int m : {4, 2}) {
-    if (m * p.nw <= 512 && m <= ktiles64) {
+    if (m * p.nsub * p.nw <= 512 && m <= ktiles64) {
       p.mt = m;
       break;
     }
   }
   p.tmem_cols = 32;
-  while (p.tmem_cols < p.mt * p.nw) p.tmem_cols <<= 1;
-  const int stage = 2 * p.mt * ct::kTileBytes + 2 * p.nw * ct::kRowBytes;
+  while (p.tmem_cols < p.mt * p.nsub * p.nw) p.tmem_cols <<= 1;
+  const int stage = 2 * p.mt * ct::kTileBytes + 2 * p.nsub * p.nw * ct::kRowBytes;
   const int budget = 227 * 1024 - 1024 - 256;  // alignment slack, barriers
   p.depth = budget / stage;
   if (p.depth > 4) p.depth = 4;
@@ -391,7 +410,7 @@ ContractPlan contract_plan(int K, int W, int64_t n, int n_sm, int C) {
   p.dbg = 0;
   p.tpc = (K + 64 * p.mt - 1) / (64 * p.mt);
   p.tiles_k = C * p.tpc;
-  p.tiles_w = (W + p.nw - 1) / p.nw;
+  p.tiles_w = (W + p.nsub * p.nw - 1) / (p.nsub * p.nw);
   const int64_t total_st = (n + ct::kStageSpins - 1) / ct::kStageSpins;
   int64_t chunks = n_sm / (p.tiles_k * p.tiles_w);
   if (chunks < 1) chunks = 1;

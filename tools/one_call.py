@@ -1,4 +1,4 @@
-"""One device-resident call of a config (for ncu captures): python tools/one_call.py CFG [repeats]"""
+"""One device-resident call of a config (for ncu captures): python tools/one_call.py CFG [repeats] [shard N]"""
 import sys
 
 import numpy as np
@@ -10,8 +10,13 @@ from paper_1305_6861_b200.engine import _unit_weight, get_engine, precompute_seq
 
 c = int(sys.argv[1])
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+nsh = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 w = configs.make(c)
 b, n, C = w.block, w.n_spins, w.n_coils
+if nsh > 1:  # rank 0's np.linspace shard
+    from paper_1305_6861_b200.parallel import shard_block
+    b = shard_block(b, nsh, 0)
+    n = b.n
 t = precompute_sequence_tables(w.sequence)
 dev = torch.device("cuda", 0)
 f = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
