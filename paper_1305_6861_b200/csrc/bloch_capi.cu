@@ -931,6 +931,25 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       kp.spins_per_cta = static_cast<int32_t>(spc);
       kp.gev = c->d_gev.as<bloch::GEv>();
       kp.mats = c->d_mats.as<double>();
+      {
+        static const bool no_smem_mats = getenv("BLOCH_NO_SMEM_MATS") != nullptr;  // A/B hook
+        const int64_t nm = static_cast<int64_t>(P.mats.size() / 9);
+        kp.n_mats_smem = (!no_smem_mats && !v.full && !v.win && v.S <= 2 && nm <= bloch::kMatsSmemMax)
+                             ? static_cast<int32_t>(nm) : 0;
+        // progression running factors in shared memory (register-state kernels, up to 64 KB per CTA)
+        static const bool no_smem_prog = getenv("BLOCH_NO_SMEM_PROG") != nullptr;  // A/B hook
+        kp.n_prog_smem = 0;
+        const int np = static_cast<int>(P.prog_classes.size());
+        if (!no_smem_prog && !v.full && !v.win && v.S <= 4 && np > 0 && np <= 32 &&
+            static_cast<int64_t>(np) * v.S * threads * 16 <= 64 * 1024) {
+          for (int pc = 0; pc < np; ++pc) kp.prog_plane[pc] = -1;
+          for (const bloch::DevOp& op : OPS)
+            if (op.kind == bloch::OP_EVENT && op.prg >= 0 && op.prg < np) kp.prog_plane[op.prg] = op.pl[0];
+          bool ok = true;
+          for (int pc = 0; pc < np; ++pc) ok = ok && kp.prog_plane[pc] >= 0;
+          if (ok) kp.n_prog_smem = np;
+        }
+      }
       kp.n = n;
       kp.sc = c->sc.as<bloch::SpinConst>();
       kp.mx0 = d_mx;

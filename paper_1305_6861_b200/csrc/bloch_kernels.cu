@@ -218,11 +218,11 @@ __device__ __forceinline__ RotCoef load_rot(const KParams& kp, const DevOp* op, 
 struct Mat3 {
   double r[9];
 };
-__device__ __forceinline__ Mat3 load_mat(const KParams& kp, int pre) {
+__device__ __forceinline__ Mat3 load_mat(const double* mats, int pre) {
   Mat3 m;
-  const double* q = kp.mats + static_cast<int64_t>(pre) * 9;
+  const double* q = mats + static_cast<int64_t>(pre) * 9;
 #pragma unroll
-  for (int k = 0; k < 9; ++k) m.r[k] = __ldg(q + k);
+  for (int k = 0; k < 9; ++k) m.r[k] = q[k];  // shared memory (staged) or global through L1
   return m;
 }
 __device__ __forceinline__ void rotate(const Mat3& m, double& x, double& y, double& z) {
@@ -252,8 +252,8 @@ __device__ __forceinline__ void interval(const KParams& kp, SP& sp, int s, int f
 
 // the fused pulse on its own pass over the state (paths that do not load the state anyway)
 template <int S, class SP>
-__device__ __forceinline__ void apply_pre(const KParams& kp, SP& sp, int pre, int mode) {
-  const Mat3 m = load_mat(kp, pre);
+__device__ __forceinline__ void apply_pre(const double* mats, SP& sp, int pre, int mode) {
+  const Mat3 m = load_mat(mats, pre);
   if (mode == 1) {  // about x: (x, r4 y + r5 z, r7 y + r8 z)
 #pragma unroll
     for (int s = 0; s < S; ++s) {
@@ -872,6 +872,29 @@ __global__ void __launch_bounds__(kWin ? KernelTraits<R, S, NC>::kMaxThreads : K
   sp.bd = bd;
   sp.n = kp.n;
   sp.init_active();
+  // the fused pulse matrices: staged in shared memory by the register-state kernels (their shared memory
+  // is otherwise unused; each matrix is read once per op by every warp, an L2 round trip from global)
+  const double* mats = kp.mats;
+  // ... and the progression running factors of this thread's spins, [class][S][bd] after the matrices: an
+  // L2 read-modify-write per member otherwise (config 2: the kernel's top stall)
+  double2* progs = nullptr;
+  if constexpr (kRegState) {
+    if (kp.n_mats_smem > 0) {
+      double* sm = reinterpret_cast<double*>(smem_raw);
+      for (int k = threadIdx.x; k < 9 * kp.n_mats_smem; k += blockDim.x) sm[k] = __ldg(kp.mats + k);
+      __syncthreads();
+      mats = sm;
+    }
+    if (kp.n_prog_smem > 0) {
+      progs = reinterpret_cast<double2*>(smem_raw + ((static_cast<size_t>(kp.n_mats_smem) * 72 + 15) & ~size_t(15)));
+      for (int pc = 0; pc < kp.n_prog_smem; ++pc) {
+        const double2* src = kp.planes + static_cast<int64_t>(kp.prog_plane[pc]) * kp.n;
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+          progs[(pc * S + s) * bd + threadIdx.x] = sp.act(s) ? src[sp.idx(s)] : make_double2(1.0, 0.0);
+      }
+    }
+  }
   Strip<R> strip;  // one partial row per warp of the grid
   strip.lane = threadIdx.x & 31;
   strip.row = reinterpret_cast<R*>(kp.partial) +
@@ -908,7 +931,7 @@ __global__ void __launch_bounds__(kWin ? KernelTraits<R, S, NC>::kMaxThreads : K
       const int flags = __ldg(&op->count), snap = __ldg(&op->aux), cls = __ldg(&op->cls), rc = __ldg(&op->rot),
                 pg = __ldg(&op->prg), pre = __ldg(&op->pre);
       if constexpr (!kFull) {  // a fused pulse (basic programs only): its own pass over the state
-        if (pre >= 0) apply_pre<S>(kp, sp, pre, __ldg(&op->tmode));
+        if (pre >= 0) apply_pre<S>(mats, sp, pre, __ldg(&op->tmode));
       }
       // Two-phase per group of G spins: issue every table load of the group
       // before any store, so the L2 round trips overlap instead of serialising
@@ -933,6 +956,27 @@ __global__ void __launch_bounds__(kWin ? KernelTraits<R, S, NC>::kMaxThreads : K
             sp.my(s) = c[g].x * y + c[g].y * x;
             sp.mz(s) = fma(sp.mz(s), ab[g].x, ab[g].y);
           }
+        }
+      } else if (kRegState && pg >= 0 && progs != nullptr) {  // progression member, running factor in smem
+        const int adv = __ldg(&op->flags);  // 0 (last member), 1 or 2
+        const double2 *pq = plane(kp, op, adv == 2 ? 2 : 1), *pab = plane(kp, op, 3);  // q or q^2
+        double2 c[S], ab[S], q[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          const int64_t i = sp.act(s) ? sp.idx(s) : 0;
+          c[s] = progs[(pg * S + s) * bd + threadIdx.x];
+          ab[s] = __ldg(pab + i);
+          q[s] = adv ? __ldg(pq + i) : make_double2(1.0, 0.0);
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          const double x = sp.mx(s), y = sp.my(s);
+          sp.mx(s) = c[s].x * x - c[s].y * y;
+          sp.my(s) = c[s].x * y + c[s].y * x;
+          sp.mz(s) = fma(sp.mz(s), ab[s].x, ab[s].y);
+          if (adv)
+            progs[(pg * S + s) * bd + threadIdx.x] = make_double2(c[s].x * q[s].x - c[s].y * q[s].y,
+                                                                  c[s].x * q[s].y + c[s].y * q[s].x);
         }
       } else if (pg >= 0) {  // one member of an interval progression: C, then C *= q^adv
         const int adv = __ldg(&op->flags);  // 0 (last member), 1 or 2
@@ -982,7 +1026,7 @@ __global__ void __launch_bounds__(kWin ? KernelTraits<R, S, NC>::kMaxThreads : K
     if (kind == OP_UWIN) {  // deferred window (contract.h): store u for the contraction, apply the exit
       const int lead = __ldg(&op->aux), pre = __ldg(&op->pre);
       if constexpr (!kFull) {
-        if (pre >= 0) apply_pre<S>(kp, sp, pre, __ldg(&op->tmode));
+        if (pre >= 0) apply_pre<S>(mats, sp, pre, __ldg(&op->tmode));
       }
       const int64_t row = __ldg(&op->s0);
       const double2 *pc = plane(kp, op, 2), *pab = plane(kp, op, 3);
@@ -1284,7 +1328,7 @@ __global__ void __launch_bounds__(kWin ? KernelTraits<R, S, NC>::kMaxThreads : K
       const int cnt = __ldg(&op->count), lead = __ldg(&op->aux), s0 = __ldg(&op->s0) - kp.sample_base, rc = __ldg(&op->rot),
                 pre = __ldg(&op->pre);
       if constexpr (!kFull) {
-        if (pre >= 0) apply_pre<S>(kp, sp, pre, __ldg(&op->tmode));
+        if (pre >= 0) apply_pre<S>(mats, sp, pre, __ldg(&op->tmode));
       }
       if constexpr (sizeof(R) == 4 && NC >= 2) {
         if (cnt >= kMmaMinWindow && kp.w32 != nullptr) {  // tensor-core multi-coil window
@@ -1670,6 +1714,16 @@ __global__ void __launch_bounds__(kWin ? KernelTraits<R, S, NC>::kMaxThreads : K
       }
     }
   }
+  if constexpr (kRegState) {  // a segmented program: the running factors travel to the next segment's launch
+    if (progs != nullptr && kp.mx1 != nullptr) {
+      for (int pc = 0; pc < kp.n_prog_smem; ++pc) {
+        double2* dst = kp.planes + static_cast<int64_t>(kp.prog_plane[pc]) * kp.n;
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+          if (sp.act(s)) dst[sp.idx(s)] = progs[(pc * S + s) * bd + threadIdx.x];
+      }
+    }
+  }
   if (kp.mx1 != nullptr) {  // a segmented program: the state travels to the next segment's launch
 #pragma unroll
     for (int s = 0; s < S; ++s) {
@@ -1867,7 +1921,10 @@ static std::mutex g_smem_mu;
 
 template <typename R, int S, int NC, bool kFull, int BD, bool kWin>
 static cudaError_t launch_bd(const KParams& kp, int grid, int threads, cudaStream_t stream) {
-  const size_t smem = integrate_smem_bytes<R, S, NC>(threads, kWin || kFull);
+  size_t smem = integrate_smem_bytes<R, S, NC>(threads, kWin || kFull);
+  if (!kWin && !kFull && S <= 4)  // staged pulse matrices and progression running factors (host-sized)
+    smem += ((static_cast<size_t>(kp.n_mats_smem) * 72 + 15) & ~size_t(15)) +
+            static_cast<size_t>(kp.n_prog_smem) * S * threads * sizeof(double2);
   static size_t smem_set[kMaxDevices] = {};  // raise the limit only when needed (not inside a graph capture)
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);

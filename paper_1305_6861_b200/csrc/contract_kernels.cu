@@ -24,8 +24,7 @@
 namespace bloch {
 namespace ct {
 
-constexpr int kGenWarps = 8;               // A generators (and accumulator drains)
-constexpr int kThreads = 64 + 32 * kGenWarps;
+constexpr int kThreads(int gen_warps) { return 64 + 32 * gen_warps; }  // + A generators (and drains)
 constexpr int kStageSpins = 16;            // K = 32 bf16 = 64 B per operand row (one SWIZZLE_64B row)
 constexpr int kRowBytes = 64;
 constexpr int kTileBytes = 128 * kRowBytes;  // one 128-row operand tile: 8 KB
@@ -103,8 +102,8 @@ __device__ __forceinline__ uint32_t pack2(float lo_elem, float hi_elem) {  // bf
 
 }  // namespace ct
 
-template <int MT>
-__global__ void __launch_bounds__(ct::kThreads, 1)
+template <int MT, int GW>
+__global__ void __launch_bounds__(ct::kThreads(GW), 1)
     contract_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo,
                     const ContractJob j, const ContractPlan p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -141,11 +140,11 @@ __global__ void __launch_bounds__(ct::kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < depth; ++s) {
       ct::mbar_init(full_u + s, 1);
-      ct::mbar_init(full_z + s, ct::kGenWarps);
+      ct::mbar_init(full_z + s, GW);
       ct::mbar_init(empty + s, 1);
     }
     ct::mbar_init(acc_full, 1);
-    ct::mbar_init(acc_empty, ct::kGenWarps);
+    ct::mbar_init(acc_empty, GW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -217,7 +216,7 @@ __global__ void __launch_bounds__(ct::kThreads, 1)
     // the warp covers an even and an odd 64-B row, i.e. banks 0-15 and 16-31, and the SWIZZLE_64B chunk
     // permutation ((row >> 1) & 3) is the same for both halves
     const int q = warp - 2, half = lane >> 4, sl = lane & 15;
-    constexpr int kSamp = 64 * MT / ct::kGenWarps;  // samples per warp per stage
+    constexpr int kSamp = 64 * MT / GW;  // samples per warp per stage
     constexpr int kVals = kSamp / 2;                // per lane
     const int m = (kSamp * q) >> 6;
     const int r0 = ((kSamp * q) & 63) + half;     // row of value 0 (value v: r0 + 2 v)
@@ -229,7 +228,7 @@ __global__ void __launch_bounds__(ct::kThreads, 1)
     // ---- drain of accumulation segment e: TMEM lanes of this warp's quarter (two warps per quarter,
     // half of the columns each) -> partial slot (chunk, e); the MMA of the next segment waits for the
     // generator warps' acc_empty arrivals
-    const int quarter = warp & 3, colh = q >> 2;
+    const int quarter = warp & 3, colh = q >> 2;  // GW / 4 warps per TMEM lane quarter share the columns
     const int row = 32 * quarter + lane;  // accumulator row: sample k0 + 64 m + (row & 63), component row >> 6
     auto drain = [&](int e) {
       ct::mbar_wait(acc_full, e & 1);
@@ -237,7 +236,7 @@ __global__ void __launch_bounds__(ct::kThreads, 1)
       float* slot = j.part + ((static_cast<int64_t>(kc) * p.segs + e) * j.C + coil) * j.W * j.K * 2;
       for (int mm = 0; mm < MT; ++mm) {
         const int k = k0 + 64 * mm + (row & 63);
-        for (int c0 = 16 * colh; c0 < ncol; c0 += 32) {
+        for (int c0 = 16 * colh; c0 < ncol; c0 += 16 * (GW / 4)) {
           uint32_t r[16];
           const uint32_t addr = tmem + (static_cast<uint32_t>(32 * quarter) << 16) + static_cast<uint32_t>(mm * ncol + c0);
           asm volatile(
@@ -469,7 +468,7 @@ cudaError_t make_map(CUtensorMap* m, const uint32_t* base, const ContractJob& j,
 
 std::mutex g_contract_mu;
 
-template <int MT>
+template <int MT, int GW>
 cudaError_t launch_mt(const CUtensorMap& mh, const CUtensorMap& ml, const ContractJob& j, const ContractPlan& p,
                       cudaStream_t st) {
   static int smem_set[kMaxDevices] = {};
@@ -480,13 +479,13 @@ cudaError_t launch_mt(const CUtensorMap& mh, const CUtensorMap& ml, const Contra
   {
     std::lock_guard<std::mutex> lk(g_contract_mu);
     if (p.smem > smem_set[dev]) {
-      e = cudaFuncSetAttribute(contract_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem);
+      e = cudaFuncSetAttribute(contract_kernel<MT, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem);
       if (e != cudaSuccess) return e;
       smem_set[dev] = p.smem;
     }
   }
   const int grid = p.tiles_k * p.tiles_w * p.chunks;
-  contract_kernel<MT><<<grid, ct::kThreads, p.smem, st>>>(mh, ml, j, p);
+  contract_kernel<MT, GW><<<grid, ct::kThreads(GW), p.smem, st>>>(mh, ml, j, p);
   return cudaGetLastError();
 }
 
@@ -504,10 +503,16 @@ cudaError_t launch_contract(const ContractJob& j, const ContractPlan& p, cudaStr
   cudaError_t e = make_map(&mh, j.uhi, j, p.nw);
   if (e == cudaSuccess) e = make_map(&ml, j.ulo, j, p.nw);
   if (e != cudaSuccess) return e;
+  // one-M-tile CTAs (64 samples) generate 4 values per lane and stage with 8 warps: 4 warps halve the
+  // per-stage overhead (start powers, fences, barrier traffic) per value
+  static const int gw_env = [] {
+    const char* e = getenv("BLOCH_CONTRACT_GW");
+    return e ? atoi(e) : 0;
+  }();
   switch (p.mt) {
-    case 4: e = launch_mt<4>(mh, ml, j, p, st); break;
-    case 2: e = launch_mt<2>(mh, ml, j, p, st); break;
-    default: e = launch_mt<1>(mh, ml, j, p, st); break;
+    case 4: e = launch_mt<4, 8>(mh, ml, j, p, st); break;
+    case 2: e = launch_mt<2, 8>(mh, ml, j, p, st); break;
+    default: e = gw_env == 8 ? launch_mt<1, 8>(mh, ml, j, p, st) : launch_mt<1, 4>(mh, ml, j, p, st); break;
   }
   if (e != cudaSuccess) return e;
   const int64_t per = static_cast<int64_t>(j.C) * j.W * j.K * 2;

@@ -41,7 +41,13 @@ struct KParams {
   uint32_t* uhi;                 // OP_UWIN: U of bf16x2 (Re, Im) words, hi part (contract.h, contract_u_index)
   uint32_t* ulo;                 //          lo part
   int64_t urows;                 //          U rows
+  int32_t n_mats_smem;           // pulse matrices staged in shared memory by the register-state kernels (0: read
+                                 // from global); the fused pulses of a program, when they fit kMatsSmemMax
+  int32_t n_prog_smem;           // progression classes whose running factors the register-state kernels keep in
+                                 // shared memory for the whole launch (0: read-modify-write through L2)
+  int32_t prog_plane[32];        // running-factor plane of each progression class
 };
+constexpr int kMatsSmemMax = 640;  // 45 KB of fp64 3x3 matrices
 
 // Launch shape per variant: max threads per CTA and min resident CTAs per SM
 // (registers per thread <= 64K / (kMaxThreads * kMinBlocks)).
