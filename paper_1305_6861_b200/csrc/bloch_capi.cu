@@ -854,8 +854,9 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
                          2 * uwords * 4 <= partial_budget_bytes();
       const std::vector<bloch::DevOp>& OPS = defer ? P.dops : P.ops;
       bool full = false, win = c->precision != BLOCH_PREC_F32;
-      for (const bloch::DevOp& op : OPS) {
-        if (op.kind == bloch::OP_RFTRAIN || op.kind == bloch::OP_CHIRP || op.kind == bloch::OP_GSAMP) full = true;
+      for (const bloch::DevOp& op : OPS) {  // tabulated RF trains (train classes) run in every variant
+        if ((op.kind == bloch::OP_RFTRAIN && op.rot < 0) || op.kind == bloch::OP_CHIRP || op.kind == bloch::OP_GSAMP)
+          full = true;
         if (op.kind == bloch::OP_WINDOW) win = true;
       }
       win = win || full;
@@ -1024,6 +1025,14 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
           j.part = c->cpart.as<float>();
           j.out0 = c->d_urow_out0.as<int64_t>() + g.row0;
           j.echo = d_echo;
+          j.chirp = g.chirp;
+          j.qconj = g.qconj;
+          if (g.chirp) {
+            const bloch::PlaneDesc& qdsc = P.planes[g.qplane];
+            j.qd[0] = qdsc.d[0];
+            j.qd[1] = qdsc.d[1];
+            j.qd[2] = qdsc.d[2];
+          }
           j.C = n_coils;
           j.ncp = ncp;
           j.w32 = n_coils > 1 ? c->w32.as<float2>() : nullptr;

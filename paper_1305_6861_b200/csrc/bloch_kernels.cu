@@ -1023,8 +1023,11 @@ __global__ void __launch_bounds__(kWin ? KernelTraits<R, S, NC>::kMaxThreads : K
       continue;
     }
 
-    if (kind == OP_UWIN) {  // deferred window (contract.h): store u for the contraction, apply the exit
-      const int lead = __ldg(&op->aux), pre = __ldg(&op->pre);
+    if (kind == OP_UWIN || kind == OP_UCHIRP) {  // deferred window / chirp (contract.h): store u, apply the exit
+      // window: u = Cpre m (times z without a leading no-op sample); chirp: u = w m (one coil), the samples
+      // u r0^(k+1) q^(k(k+1)/2) are the contraction's
+      const bool chirp = kind == OP_UCHIRP;
+      const int lead = chirp ? 1 : __ldg(&op->aux), pre = __ldg(&op->pre);
       if constexpr (!kFull) {
         if (pre >= 0) apply_pre<S>(mats, sp, pre, __ldg(&op->tmode));
       }
@@ -1041,7 +1044,12 @@ __global__ void __launch_bounds__(kWin ? KernelTraits<R, S, NC>::kMaxThreads : K
           const int64_t i = sp.act(g0 + g) ? sp.idx(g0 + g) : 0;
           c[g] = __ldg(pc + i);
           ab[g] = __ldg(pab + i);
-          if constexpr (sizeof(R) == 4) {  // Cpre and z are PL_SAMPLE planes: float2 in the fp32 mode
+          if (chirp) {  // the single-coil receive weight (several coils: applied by the contraction)
+            const double2 w = (NC == 1 && kp.w != nullptr) ? __ldg(reinterpret_cast<const double2*>(kp.w) + i)
+                                                           : make_double2(1.0, 0.0);
+            cp[g] = make_float2(static_cast<float>(w.x), static_cast<float>(w.y));
+            zz[g] = make_float2(1.f, 0.f);
+          } else if constexpr (sizeof(R) == 4) {  // Cpre and z are PL_SAMPLE planes: float2 in the fp32 mode
             cp[g] = __ldg(plane32_at(kp, pcp, i));
             zz[g] = __ldg(plane32_at(kp, pz, i));
           } else {
@@ -1092,35 +1100,39 @@ __global__ void __launch_bounds__(kWin ? KernelTraits<R, S, NC>::kMaxThreads : K
       continue;
     }
 
+    if (kind == OP_RFTRAIN && __ldg(&op->rot) >= 0) {
+      // a reused RF train (train class): its tabulated affine propagator m -> A m + b (train_table_kernel);
+      // every variant has it (a program whose trains are all classes needs no on-the-fly train code)
+      const int tcl = __ldg(&op->rot);
+      constexpr int G = S < 4 ? S : 4;
+      const double2* tb = reinterpret_cast<const double2*>(kp.train) + static_cast<int64_t>(tcl) * kp.n * 6;
+#pragma unroll
+      for (int g0 = 0; g0 < S; g0 += G) {
+        double2 a[G][6];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const int64_t i = sp.act(g0 + g) ? sp.idx(g0 + g) : 0;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) a[g][k] = __ldg(tb + i * 6 + k);
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const int s = g0 + g;
+          const double x = sp.mx(s), y = sp.my(s), z = sp.mz(s);
+          sp.mx(s) = fma(a[g][0].x, x, fma(a[g][0].y, y, fma(a[g][1].x, z, a[g][4].y)));
+          sp.my(s) = fma(a[g][1].y, x, fma(a[g][2].x, y, fma(a[g][2].y, z, a[g][5].x)));
+          sp.mz(s) = fma(a[g][3].x, x, fma(a[g][3].y, y, fma(a[g][4].x, z, a[g][5].y)));
+        }
+      }
+      continue;
+    }
+
     if constexpr (kFull) {
-    if (kind == OP_RFTRAIN) {  // discretised shaped pulse: (pulse_j, identical interval) x count
+    if (kind == OP_RFTRAIN) {  // discretised shaped pulse: (pulse_j, identical interval) x count, on the fly
       const int cnt = __ldg(&op->count), m0i = __ldg(&op->aux), flags = __ldg(&op->flags), cls = __ldg(&op->cls);
       const double dt = __ldg(&op->p[0]), dmx = __ldg(&op->p[1]), dmy = __ldg(&op->p[2]), dmz = __ldg(&op->p[3]);
       const double* mats = kp.mats + static_cast<int64_t>(m0i) * 9;
       constexpr int G = S < 4 ? S : 4;  // spins per register group
-      const int tcl = __ldg(&op->rot);
-      if (tcl >= 0) {  // reused train: its tabulated affine propagator m -> A m + b (train_table_kernel)
-        const double2* tb = reinterpret_cast<const double2*>(kp.train) + static_cast<int64_t>(tcl) * kp.n * 6;
-#pragma unroll
-        for (int g0 = 0; g0 < S; g0 += G) {
-          double2 a[G][6];
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            const int64_t i = sp.act(g0 + g) ? sp.idx(g0 + g) : 0;
-#pragma unroll
-            for (int k = 0; k < 6; ++k) a[g][k] = __ldg(tb + i * 6 + k);
-          }
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            const int s = g0 + g;
-            const double x = sp.mx(s), y = sp.my(s), z = sp.mz(s);
-            sp.mx(s) = fma(a[g][0].x, x, fma(a[g][0].y, y, fma(a[g][1].x, z, a[g][4].y)));
-            sp.my(s) = fma(a[g][1].y, x, fma(a[g][2].x, y, fma(a[g][2].y, z, a[g][5].x)));
-            sp.mz(s) = fma(a[g][3].x, x, fma(a[g][3].y, y, fma(a[g][4].x, z, a[g][5].y)));
-          }
-        }
-        continue;
-      }
 #pragma unroll 1
       for (int g0 = 0; g0 < S; g0 += G) {
         double x[G], y[G], z[G], zr[G], zi[G], e1[G], rg[G];

@@ -53,7 +53,10 @@ struct ContractJob {
   const float2* w32;    // [n][ncp] fp32 coil weights (C > 1; one coil carries its weight in U)
   int64_t G;            // complex samples per coil in the echo array
   float4* zt;           // [n] scratch: per-spin (theta_hi, theta_lo, a, 0), theta = phase per sample mod 2 pi
-  float2* zq;           // [n] scratch: per-spin z^2
+  float2* zq;           // [n] scratch: per-spin z^2 (chirp: (theta_q lo, 0), theta_q hi in zt.w)
+  int32_t chirp;        // 1: a chirp group, sample k = u r0^(k+1) q^(k(k+1)/2); (T, d, tw) describe r0 and
+  double qd[3];         //    q = exp(-i pos . qd), conjugated when qconj
+  int32_t qconj;
 };
 
 constexpr int kContractMaxSamples = 4096;  // windows up to this long (the fp32 phase k theta_hi is exact)

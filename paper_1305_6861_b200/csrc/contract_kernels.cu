@@ -90,6 +90,20 @@ __device__ __forceinline__ float2 zpow32(float4 t, float k) {
   const float amp = __expf(-k * t.z);
   return make_float2(amp * cs, -amp * sn);
 }
+// a phase m * head (exact: m and the 12-bit head are short) reduced to [-pi, pi] up to 2pi_lo
+__device__ __forceinline__ float red2pi(float p) {
+  const float nn = __fadd_rn(__fmaf_rn(p, 0.15915494309189535f, 12582912.0f), -12582912.0f);
+  return __fmaf_rn(-nn, 0.0019353071795864769f, __fmaf_rn(-nn, 6.28125f, p));
+}
+// chirp sample factor r0^m1 q^m2 = exp(-m1 a) exp(-i (m1 theta0 + m2 theta_q)), m1 = k + 1, m2 = k (k + 1) / 2
+__device__ __forceinline__ float2 zchirp32(float4 t, float ql, float m1, float m2) {
+  float r = red2pi(m1 * t.x) + red2pi(m2 * t.w);
+  r = __fmaf_rn(m1, t.y, __fmaf_rn(m2, ql, r));
+  float sn, cs;
+  __sincosf(r, &sn, &cs);
+  const float amp = __expf(-m1 * t.z);
+  return make_float2(amp * cs, -amp * sn);
+}
 // bf16 hi part (round to nearest: Veltkamp split keeping 8 significant bits) and the residual
 __device__ __forceinline__ void split_bf16(float x, float& hi, float& lo) {
   const float c = __fmul_rn(x, 65537.0f);
@@ -102,7 +116,7 @@ __device__ __forceinline__ uint32_t pack2(float lo_elem, float hi_elem) {  // bf
 
 }  // namespace ct
 
-template <int MT, int GW>
+template <int MT, int GW, bool CH>
 __global__ void __launch_bounds__(ct::kThreads(GW), 1)
     contract_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo,
                     const ContractJob j, const ContractPlan p) {
@@ -296,7 +310,8 @@ __global__ void __launch_bounds__(ct::kThreads(GW), 1)
         continue;
       }
       float2 P = make_float2(0.f, 0.f), Q = make_float2(0.f, 0.f);
-      if ((st0 + t) * ct::kStageSpins + sl < j.n) {
+      const bool live = (st0 + t) * ct::kStageSpins + sl < j.n;
+      if (!CH && live) {
         const float2 z0 = ct::zpow32(czt, kf);
         P = make_float2(cwc.x * z0.x - cwc.y * z0.y, cwc.x * z0.y + cwc.y * z0.x);  // the coil weight rides along
         Q = czq;
@@ -304,6 +319,11 @@ __global__ void __launch_bounds__(ct::kThreads(GW), 1)
       unsigned char* ab = A(s, 0) + off0;
 #pragma unroll
       for (int v = 0; v < kVals; ++v) {
+        if constexpr (CH) {  // chirp: each sample's factor directly (short runs, no recurrence)
+          const float k = kf + 2.f * v;
+          const float2 z0 = live ? ct::zchirp32(czt, czq.x, k + 1.f, 0.5f * k * (k + 1.f)) : make_float2(0.f, 0.f);
+          P = make_float2(cwc.x * z0.x - cwc.y * z0.y, cwc.x * z0.y + cwc.y * z0.x);
+        }
         // bf16 hi parts rounded to nearest (Veltkamp, both components packed) and the residuals
         // (scalar __fmul_rn: never contracted into the following subtraction, which would void the split)
         const float2 c = make_float2(__fmul_rn(P.x, 65537.0f), __fmul_rn(P.y, 65537.0f));
@@ -315,9 +335,11 @@ __global__ void __launch_bounds__(ct::kThreads(GW), 1)
         *reinterpret_cast<uint32_t*>(o + 4096) = ct::pack2(hi.y, hi.x);             // imaginary row
         *reinterpret_cast<uint32_t*>(o + a_bytes) = ct::pack2(lo.x, -lo.y);
         *reinterpret_cast<uint32_t*>(o + a_bytes + 4096) = ct::pack2(lo.y, lo.x);
-        const float nx = P.x * Q.x - P.y * Q.y;
-        P.y = P.x * Q.y + P.y * Q.x;
-        P.x = nx;
+        if constexpr (!CH) {
+          const float nx = P.x * Q.x - P.y * Q.y;
+          P.y = P.x * Q.y + P.y * Q.x;
+          P.x = nx;
+        }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
@@ -335,10 +357,22 @@ __global__ void __launch_bounds__(ct::kThreads(GW), 1)
 // expression) reduced mod 2 pi and split into a 12-significant-bit head and the rest; a = T r2;
 // z^2 = exp(-2 a) exp(-2 i theta)
 __global__ void contract_prep_kernel(const SpinConst* __restrict__ sc, int64_t n, double T, double d0, double d1,
-                                     double d2, double tw, float4* __restrict__ zt, float2* __restrict__ zq) {
+                                     double d2, double tw, float4* __restrict__ zt, float2* __restrict__ zq,
+                                     int chirp, double q0, double q1, double q2, int qconj) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const SpinConst c = sc[i];
+    if (chirp) {  // r0 = exp(-T r2) exp(-i theta0), q = exp(-i theta_q): both phases split head / tail
+      const double th = ct::reduce_2pi(fma(c.z, d2, fma(c.y, d1, c.x * d0)) + c.dw * tw);
+      double thq = ct::reduce_2pi(fma(c.z, q2, fma(c.y, q1, c.x * q0)));
+      if (qconj) thq = -thq;
+      const float hi = __uint_as_float(__float_as_uint(static_cast<float>(th)) & 0xfffff000u);
+      const float hq = __uint_as_float(__float_as_uint(static_cast<float>(thq)) & 0xfffff000u);
+      const double a = T != 0.0 ? T * c.r2 : 0.0;
+      zt[i] = make_float4(hi, static_cast<float>(th - static_cast<double>(hi)), static_cast<float>(a), hq);
+      zq[i] = make_float2(static_cast<float>(thq - static_cast<double>(hq)), 0.f);
+      continue;
+    }
     const double th = ct::reduce_2pi(fma(c.z, d2, fma(c.y, d1, c.x * d0)) + c.dw * tw);
     const float hi = __uint_as_float(__float_as_uint(static_cast<float>(th)) & 0xfffff000u);
     const float lo = static_cast<float>(th - static_cast<double>(hi));
@@ -468,7 +502,7 @@ cudaError_t make_map(CUtensorMap* m, const uint32_t* base, const ContractJob& j,
 
 std::mutex g_contract_mu;
 
-template <int MT, int GW>
+template <int MT, int GW, bool CH = false>
 cudaError_t launch_mt(const CUtensorMap& mh, const CUtensorMap& ml, const ContractJob& j, const ContractPlan& p,
                       cudaStream_t st) {
   static int smem_set[kMaxDevices] = {};
@@ -479,13 +513,13 @@ cudaError_t launch_mt(const CUtensorMap& mh, const CUtensorMap& ml, const Contra
   {
     std::lock_guard<std::mutex> lk(g_contract_mu);
     if (p.smem > smem_set[dev]) {
-      e = cudaFuncSetAttribute(contract_kernel<MT, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem);
+      e = cudaFuncSetAttribute(contract_kernel<MT, GW, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem);
       if (e != cudaSuccess) return e;
       smem_set[dev] = p.smem;
     }
   }
   const int grid = p.tiles_k * p.tiles_w * p.chunks;
-  contract_kernel<MT, GW><<<grid, ct::kThreads(GW), p.smem, st>>>(mh, ml, j, p);
+  contract_kernel<MT, GW, CH><<<grid, ct::kThreads(GW), p.smem, st>>>(mh, ml, j, p);
   return cudaGetLastError();
 }
 
@@ -493,26 +527,30 @@ cudaError_t launch_mt(const CUtensorMap& mh, const CUtensorMap& ml, const Contra
 
 cudaError_t launch_contract(const ContractJob& j, const ContractPlan& p, cudaStream_t st) {
   if (j.n <= 0 || j.W <= 0 || j.K <= 0) return cudaSuccess;
-  if (j.K > kContractMaxSamples || j.C < 1 || (j.C > 1 && !j.w32)) return cudaErrorInvalidValue;
+  if (j.K > kContractMaxSamples || j.C < 1 || (j.C > 1 && !j.w32) || (j.chirp && j.K > 64))
+    return cudaErrorInvalidValue;
   {
     const int64_t blocks = (j.n + 255) / 256;
     contract_prep_kernel<<<static_cast<int>(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(
-        j.sc, j.n, j.T, j.d[0], j.d[1], j.d[2], j.tw, j.zt, j.zq);
+        j.sc, j.n, j.T, j.d[0], j.d[1], j.d[2], j.tw, j.zt, j.zq, j.chirp, j.qd[0], j.qd[1], j.qd[2], j.qconj);
   }
   CUtensorMap mh, ml;
   cudaError_t e = make_map(&mh, j.uhi, j, p.nw);
   if (e == cudaSuccess) e = make_map(&ml, j.ulo, j, p.nw);
   if (e != cudaSuccess) return e;
-  // one-M-tile CTAs (64 samples) generate 4 values per lane and stage with 8 warps: 4 warps halve the
-  // per-stage overhead (start powers, fences, barrier traffic) per value
+  // generator warps: 8 (4 for one-M-tile CTAs halve the per-stage overhead per value but hide less latency:
+  // config 4 contraction 6.27 vs 5.93 ms, profiles/r2ff_generator_warps.txt; BLOCH_CONTRACT_GW=4 to compare)
   static const int gw_env = [] {
     const char* e = getenv("BLOCH_CONTRACT_GW");
     return e ? atoi(e) : 0;
   }();
-  switch (p.mt) {
+  if (j.chirp) {  // chirps: at most kMaxDeferChirp samples, one M-tile
+    if (p.mt != 1) return cudaErrorInvalidValue;
+    e = launch_mt<1, 8, true>(mh, ml, j, p, st);
+  } else switch (p.mt) {
     case 4: e = launch_mt<4, 8>(mh, ml, j, p, st); break;
     case 2: e = launch_mt<2, 8>(mh, ml, j, p, st); break;
-    default: e = gw_env == 8 ? launch_mt<1, 8>(mh, ml, j, p, st) : launch_mt<1, 4>(mh, ml, j, p, st); break;
+    default: e = gw_env == 4 ? launch_mt<1, 4>(mh, ml, j, p, st) : launch_mt<1, 8>(mh, ml, j, p, st); break;
   }
   if (e != cudaSuccess) return e;
   const int64_t per = static_cast<int64_t>(j.C) * j.W * j.K * 2;

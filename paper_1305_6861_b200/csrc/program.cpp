@@ -14,6 +14,7 @@
 #include <map>
 #include <set>
 #include <cmath>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -502,39 +503,107 @@ void defer_windows(Program& prog) {
   prog.groups.clear();
   prog.urow_out0.clear();
   prog.n_deferred_samples = 0;
-  std::map<std::pair<int32_t, int32_t>, int32_t> gid;
-  std::vector<std::vector<size_t>> members;
+  // plane dedup over the existing planes (assign_planes' keys), for the planes of single-sample events
+  using PKey = std::array<double, 6>;
+  std::map<PKey, int32_t> pids;
+  auto pkey = [](const PlaneDesc& pd) {
+    return PKey{static_cast<double>(pd.kind * 16 + pd.flags), pd.T, pd.d[0], pd.d[1], pd.d[2], pd.tw};
+  };
+  for (size_t k = 0; k < prog.planes.size(); ++k)
+    if (!(prog.planes[k].flags & PL_MUTABLE)) pids.emplace(pkey(prog.planes[k]), static_cast<int32_t>(k));
+  auto plane = [&](int32_t kind, int32_t flags, double T, const double* d, double tw) -> int32_t {
+    PlaneDesc pd{};
+    pd.kind = kind;
+    pd.flags = flags;
+    pd.T = T;
+    for (int a = 0; a < 3; ++a) pd.d[a] = kind == PL_PHASE ? d[a] : 0.0;
+    pd.tw = kind == PL_PHASE ? tw : 0.0;
+    auto f = pids.find(pkey(pd));
+    if (f != pids.end()) return f->second;
+    const int32_t id = static_cast<int32_t>(prog.planes.size());
+    prog.planes.push_back(pd);
+    pids.emplace(pkey(pd), id);
+    return id;
+  };
+  // a single-sample generic event as a one-sample window: u = w m z, exit C = z (fp64), (A, B) of its dt
+  const double zero3[3] = {0.0, 0.0, 0.0};
+  auto single = [&](const DevOp& op, DevOp& w) {
+    const GEv& g = prog.gev[op.aux];
+    const double dt = g.dt, dm[3] = {g.dmx, g.dmy, g.dmz};
+    const bool mv = (g.flags & EV_MOVE) != 0, rx = (g.flags & EV_RELAX) != 0;
+    const double T = rx ? dt : 0.0;
+    w = op;
+    w.kind = OP_WINDOW;
+    w.count = 1;
+    w.aux = 0;  // no leading no-op sample: the sample follows the interval
+    w.pre = -1;
+    w.pl[0] = plane(PL_PHASE, PL_WEIGHT | PL_SAMPLE, 0.0, zero3, 0.0);
+    w.pl[1] = plane(PL_PHASE, PL_SAMPLE, T, mv ? dm : zero3, mv ? dt : 0.0);
+    w.pl[2] = plane(PL_PHASE, 0, T, mv ? dm : zero3, mv ? dt : 0.0);
+    w.pl[3] = plane(PL_AB, 0, T, zero3, 0.0);
+  };
+  // candidates: tabulated windows, tabulated chirps, single-sample generic events (grouped below)
+  struct Cand {
+    size_t k;
+    DevOp op;  // as deferred (single samples rewritten as one-sample windows)
+  };
+  using GKey = std::array<int32_t, 5>;  // (chirp, z / r0 plane, q plane, conj, count)
+  std::map<GKey, std::vector<Cand>> by_key;
+  std::vector<GKey> key_order;
+  // Short runs (chirps, single samples) are deferred only on request (BLOCH_DEFER_SHORT=1): each group costs a
+  // 64-sample M-tile pass over every spin whatever its length, so config 3's four 10-sample ramp classes and
+  // its single samples cost 2.4 ms in the contraction against 1.5 ms in the integrator (7.22 vs 5.70 ms,
+  // profiles/r2gg_short_runs.txt).  Whole EPI lines as one group (a piecewise generator) would fix that.
+  static const bool short_runs = [] {
+    const char* e = getenv("BLOCH_DEFER_SHORT");
+    return e && atoi(e) != 0;
+  }();
   for (size_t k = 0; k < prog.ops.size(); ++k) {
     const DevOp& op = prog.ops[k];
-    if (op.kind != OP_WINDOW || op.rot < 0 || op.count < kMinDeferWindow || op.count > kMaxDeferWindow) continue;
-    const auto key = std::make_pair(op.pl[1], op.count);
-    auto f = gid.find(key);
-    if (f == gid.end()) {
-      f = gid.emplace(key, static_cast<int32_t>(prog.groups.size())).first;
-      prog.groups.push_back(WinGroup{op.pl[1], op.count, 0, 0});
-      members.emplace_back();
+    GKey key;
+    DevOp d = op;
+    if (op.kind == OP_WINDOW && op.rot >= 0 && op.count >= kMinDeferWindow && op.count <= kMaxDeferWindow) {
+      key = {0, op.pl[1], -1, 0, op.count};
+    } else if (short_runs && op.kind == OP_CHIRP && op.rot >= 0 && op.count <= kMaxDeferChirp) {
+      key = {1, op.pl[0], op.pl[1], op.tmode & 1, op.count};
+    } else if (short_runs && op.kind == OP_GSAMP && op.count == 1) {
+      single(op, d);
+      key = {0, d.pl[1], -1, 0, 1};
+    } else {
+      continue;
     }
-    members[f->second].push_back(k);
+    auto f = by_key.find(key);
+    if (f == by_key.end()) {
+      key_order.push_back(key);
+      f = by_key.emplace(key, std::vector<Cand>()).first;
+    }
+    f->second.push_back(Cand{k, d});
   }
   std::vector<int32_t> row_of(prog.ops.size(), -1);
+  std::vector<DevOp> as_deferred(prog.ops.size());
   int32_t row = 0;
-  for (size_t g = 0; g < prog.groups.size(); ++g) {
-    prog.groups[g].row0 = row;
-    prog.groups[g].n_windows = static_cast<int32_t>(members[g].size());
-    for (size_t k : members[g]) {
-      const DevOp& op = prog.ops[k];
+  for (const GKey& key : key_order) {
+    const std::vector<Cand>& mem = by_key[key];
+    const bool long_window = key[0] == 0 && key[4] >= kMinDeferWindow;
+    if (!long_window && static_cast<int32_t>(mem.size()) < kMinDeferGroup) continue;  // short runs: groups only
+    WinGroup g{key[1], key[4], row, static_cast<int32_t>(mem.size()), key[0], key[2], key[3]};
+    prog.groups.push_back(g);
+    for (const Cand& c : mem) {
+      const DevOp& op = prog.ops[c.k];
       const int64_t first = prog.sample_g[op.s0];
       for (int32_t q = 1; q < op.count; ++q)
         if (prog.sample_g[op.s0 + q] != first + q) throw std::logic_error("window samples not contiguous");
       prog.urow_out0.push_back(first);
       prog.n_deferred_samples += op.count;
-      row_of[k] = row++;
+      as_deferred[c.k] = c.op;
+      row_of[c.k] = row++;
     }
   }
   for (size_t k = 0; k < prog.ops.size(); ++k) {
     DevOp op = prog.ops[k];
     if (row_of[k] >= 0) {
-      op.kind = OP_UWIN;
+      op = as_deferred[k];
+      op.kind = op.kind == OP_CHIRP ? OP_UCHIRP : OP_UWIN;
       op.s0 = row_of[k];
     } else if (op.kind == OP_WINDOW || op.kind == OP_CHIRP || op.kind == OP_GSAMP) {
       const int32_t s0 = static_cast<int32_t>(prog.dsample_g.size());

@@ -37,7 +37,12 @@
 
 namespace bloch {
 
-enum OpKind : int32_t { OP_ROT = 1, OP_EVENT = 2, OP_GSAMP = 3, OP_WINDOW = 4, OP_CHIRP = 5, OP_RFTRAIN = 6, OP_UWIN = 7 };
+enum OpKind : int32_t {
+  OP_ROT = 1, OP_EVENT = 2, OP_GSAMP = 3, OP_WINDOW = 4, OP_CHIRP = 5, OP_RFTRAIN = 6, OP_UWIN = 7, OP_UCHIRP = 8
+};
+// OP_UCHIRP (deferred-window program): a tabulated OP_CHIRP whose samples u r0^(k+1) q^(k(k+1)/2) are formed
+// by the contraction; the integrator stores u = w m in U row `s0` and applies the run's closed form (pl[2],
+// pl[3]).  A generic sampled interval of one sample (OP_GSAMP, count 1) becomes a one-sample OP_UWIN.
 // OP_UWIN (the deferred-window program, Program::dops): a tabulated OP_WINDOW whose samples are formed
 // afterwards by the tensor-core contraction (contract.h).  The integrator stores the window's entry
 // magnetisation u = Cpre m (times z without a leading no-op sample) as bf16 hi/lo words in U row `s0`
@@ -157,10 +162,15 @@ constexpr int kMaxDeferWindow = 4096;  // ... up to this long (contract.h kContr
 // The windows of one rotation class (same z plane, same sample count) contracted as one product
 // (contract.h): U rows [row0, row0 + n_windows) in op order.
 struct WinGroup {
-  int32_t zplane;     // plane id of the per-sample factor z
+  int32_t zplane;     // plane id of the per-sample factor z (a chirp's r0)
   int32_t count;      // samples per window
   int32_t row0;       // first U row
   int32_t n_windows;  // windows (U rows)
+  int32_t chirp;      // 1: chirp group, sample k = u r0^(k+1) q^(k(k+1)/2)
+  int32_t qplane;     // chirp: plane of q (pure gradient phase, canonical sign)
+  int32_t qconj;      // chirp: q is the conjugate of the plane
 };
+constexpr int kMaxDeferChirp = 64;  // chirps this long at most (k(k+1)/2 times a 12-bit phase head stays exact)
+constexpr int kMinDeferGroup = 16;  // short runs (chirps, single samples) are deferred in groups this large
 
 }  // namespace bloch

@@ -329,3 +329,40 @@ def test_gpu_contraction_runs_and_matches(name):
     ph = eng.last_phases()
     assert ph["groups"] >= 1 and ph["contracted_samples"] > 0, ph
     assert echo_error(rec, echoes) <= KSPACE_TOL[32]
+
+
+_SHORT_CHILD = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests"); sys.path.insert(0, sys.argv[1] + "/tests/golden")
+from test_gpu_parity import _tables, _block, echo_error, snapshot_errors
+from conftest import load_golden
+from paper_1305_6861_b200 import compute_block
+from paper_1305_6861_b200.engine import get_engine
+name = sys.argv[2]
+rec = load_golden(name)
+e, s = compute_block(_tables(name, rec), _block(rec), precision=32)
+eng = get_engine(0, 32)
+print(json.dumps({"err": echo_error(rec, e), "snap": max(snapshot_errors(rec, s) or [0.0]),
+                  "groups": eng.program_stats()["window_groups"], "rest": eng.program_stats()["integrator_samples"]}))
+"""
+
+
+@pytest.mark.parametrize("name", ["epi16", "mixed", "mixed_coils", "cfg3"])
+def test_gpu_short_run_contraction(name):
+    """BLOCH_DEFER_SHORT=1: tabulated chirps (trapezoid ramps, u r0^(k+1) q^(k(k+1)/2)) and single-sample
+    events contracted as well, against the reference goldens."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, BLOCH_DEFER_SHORT="1")
+    r = subprocess.run([sys.executable, "-c", _SHORT_CHILD, root, name], capture_output=True, text=True, env=env,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["err"] <= KSPACE_TOL[32] and d["snap"] <= STATE_TOL[32], d
+    if name in ("epi16", "cfg3"):
+        assert d["rest"] == 0, d  # every sample contracted

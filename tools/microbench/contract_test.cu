@@ -84,6 +84,7 @@ int main(int argc, char** argv) {
   j.out0 = d_out0;
   j.echo = d_echo;
   j.C = 1;
+  j.chirp = 0;
   j.ncp = 1;
   j.w32 = nullptr;
   j.G = static_cast<int64_t>(W) * K;
