@@ -364,5 +364,7 @@ def test_gpu_short_run_contraction(name):
     assert r.returncode == 0, r.stderr[-2000:]
     d = json.loads(r.stdout.strip().splitlines()[-1])
     assert d["err"] <= KSPACE_TOL[32] and d["snap"] <= STATE_TOL[32], d
-    if name in ("epi16", "cfg3"):
+    if name == "epi16":
         assert d["rest"] == 0, d  # every sample contracted
+    if name == "cfg3":  # runs in groups smaller than kMinDeferGroup (program.h) stay in the integrator
+        assert d["rest"] < 16, d
