@@ -260,6 +260,18 @@ int bloch_last_segments(const bloch_ctx* ctx, int32_t* segments);
  * `enable` = 0 keeps every window in the integrator (per-warp sums).  Default: enabled. */
 int bloch_set_contraction(bloch_ctx* ctx, int32_t enable);
 
+/* Resident-table integrator (fp32 mode, every window contracted, RF trains tabulated): the per-spin
+ * class tables of a CTA's spins stay in shared memory for the whole launch, one spin per thread, so
+ * each table value crosses L2 once per call instead of once per op (the reference's relax cache,
+ * engine.py:292-299, generalised and held on chip).  `enable` = 0 keeps integrate_kernel, which reads
+ * the tables through L2 at every op.  Default: enabled; programs it does not cover (on-the-fly
+ * chirps, generic sampled events, in-kernel windows, tables beyond 227 KB per 128 spins) fall back. */
+int bloch_set_resident(bloch_ctx* ctx, int32_t enable);
+
+/* Whether the last bloch_compute_block ran the resident-table integrator, and the bytes of class
+ * tables per spin of the current program's resident plan (0: the program is not covered). */
+int bloch_last_resident(const bloch_ctx* ctx, int32_t* resident, int32_t* bytes_per_spin);
+
 /* The compiled program's window groups (one contraction each), the samples they produce and the
  * samples the integrator still sums itself when the contraction runs (host-only contexts too). */
 int bloch_program_groups(const bloch_ctx* ctx, int32_t* n_groups, int64_t* contracted_samples,

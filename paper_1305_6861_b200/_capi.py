@@ -87,6 +87,8 @@ SIGNATURES = {
     "bloch_last_launch": (c_int, [c_void_p] + [POINTER(c_int32)] * 5),
     "bloch_last_segments": (c_int, [c_void_p, POINTER(c_int32)]),
     "bloch_set_contraction": (c_int, [c_void_p, c_int32]),
+    "bloch_set_resident": (c_int, [c_void_p, c_int32]),
+    "bloch_last_resident": (c_int, [c_void_p, POINTER(c_int32), POINTER(c_int32)]),
     "bloch_program_groups": (c_int, [c_void_p, POINTER(c_int32), POINTER(c_int64), POINTER(c_int64)]),
     "bloch_program_ops": (c_int, [c_void_p, c_int32, c_int32] + [POINTER(c_int32)] * 7),
     "bloch_last_phases": (c_int, [c_void_p, POINTER(c_float), POINTER(c_float), POINTER(c_int32), POINTER(c_int64)]),

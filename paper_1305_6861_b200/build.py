@@ -18,8 +18,8 @@ CSRC = os.path.join(HERE, "csrc")
 LIB_NAME = "libbloch_b200.so"
 LIB_PATH = os.path.join(HERE, LIB_NAME)
 
-SOURCES = ["bloch_kernels.cu", "bloch_capi.cu", "program.cpp", "raster_kernels.cu", "contract_kernels.cu"]
-HEADERS = ["kernels.h", "program.h", "program_host.h", "raster.h", "contract.h"]
+SOURCES = ["bloch_kernels.cu", "bloch_capi.cu", "program.cpp", "raster_kernels.cu", "contract_kernels.cu", "resident_kernels.cu"]
+HEADERS = ["kernels.h", "program.h", "program_host.h", "raster.h", "contract.h", "resident.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -47,29 +47,34 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
     ]
     if not force and not defines and not _stale(target, deps):
         return target
-    cmd = [
-        nvcc_path(),
-        *ARCH,
-        "-O3",
-        "-lineinfo",
-        "-std=c++17",
-        "-shared",
-        "-Xcompiler",
-        "-fPIC",
-        "-Xptxas",
-        "-v" if verbose else "-O3",
-        "-I",
-        os.path.join(ROOT, "include"),
-        *[f"-D{d}" for d in defines],
-        "-o",
-        target + ".tmp",
-        *srcs,
-    ]
+    # one object per source, compiled in parallel and only when stale (A/B builds with defines: their own objects)
+    import hashlib
+    from concurrent.futures import ThreadPoolExecutor
+
+    tag = hashlib.sha1(" ".join(defines).encode()).hexdigest()[:8] if defines else "base"
+    objdir = os.path.join(CSRC, "_obj", tag)
+    os.makedirs(objdir, exist_ok=True)
+    hdrs = [d for d in deps if d not in srcs]
+    common = [nvcc_path(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas",
+              "-v" if verbose else "-O3", "-I", os.path.join(ROOT, "include"), *[f"-D{d}" for d in defines]]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        if force or _stale(obj, [src] + hdrs):
+            cmd = [*common, "-c", src, "-o", obj]
+            res = subprocess.run(cmd, capture_output=True, text=True)
+            if res.returncode != 0:
+                raise RuntimeError(f"nvcc failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+            if verbose:
+                sys.stderr.write(res.stdout + res.stderr)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(srcs)) as pool:
+        objs = list(pool.map(compile_one, srcs))
+    cmd = [nvcc_path(), *ARCH, "-shared", "-o", target + ".tmp", *objs]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
-    if verbose:
-        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError(f"nvcc link failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
     os.replace(target + ".tmp", target)
     return target
 

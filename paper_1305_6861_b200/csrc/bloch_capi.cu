@@ -14,6 +14,7 @@
 #include <string>
 
 #include "../../include/bloch_b200.h"
+#include "resident.h"
 #include "contract.h"
 #include "kernels.h"
 #include "program_host.h"
@@ -95,6 +96,11 @@ struct bloch_ctx {
   // window contraction (contract.h): deferred-window program, U rows, split-K partials
   DevBuf d_dops, d_dsample_g, d_urow_out0, uhi, ulo, cpart, ztab, zqtab;
   bool contraction = true;
+  // resident-table integrator (resident.h): the deferred program with the class tables in shared memory
+  bloch::ResidentPlan rplan;
+  DevBuf d_rops, d_rloads, d_rmats, d_rmats4;
+  bool resident = true;
+  int32_t last_resident = 0;  // the last call ran resident_integrate_kernel
   float integrate_ms = 0.f, contract_ms = 0.f;
   int32_t last_groups = 0;
   int64_t last_csamples = 0;
@@ -397,7 +403,7 @@ int bloch_destroy(bloch_ctx* c) {
   for (DevBuf* b : {&c->d_ops, &c->d_gev, &c->d_mats, &c->d_sample_g, &c->d_relax_t, &c->relax, &c->d_planes, &c->planetab, &c->planetab32, &c->in_pos, &c->in_mx, &c->in_my, &c->in_mz,
                     &c->in_t1, &c->in_t2, &c->in_m0, &c->in_dw, &c->in_w, &c->sc, &c->wpad, &c->w32, &c->partial,
                     &c->echo, &c->snaps, &c->d_train_cls, &c->traintab, &c->state, &c->d_dops, &c->d_dsample_g,
-                    &c->d_urow_out0, &c->uhi, &c->ulo, &c->cpart, &c->ztab, &c->zqtab,
+                    &c->d_urow_out0, &c->uhi, &c->ulo, &c->cpart, &c->ztab, &c->zqtab, &c->d_rops, &c->d_rloads, &c->d_rmats, &c->d_rmats4,
                     &c->raster_scratch})
     b->release();
   for (auto& ev : c->ev)
@@ -465,6 +471,15 @@ int bloch_set_tables(bloch_ctx* c, int32_t n_es, const int64_t* es_ev_offset,
       upload(c->d_dops, prog.dops.data(), prog.dops.size() * sizeof(bloch::DevOp), c->stream);
       upload(c->d_dsample_g, prog.dsample_g.data(), prog.dsample_g.size() * sizeof(int64_t), c->stream);
       upload(c->d_urow_out0, prog.urow_out0.data(), prog.urow_out0.size() * sizeof(int64_t), c->stream);
+    }
+    bloch::resident_compile(prog, c->rplan);
+    if (c->device != BLOCH_HOST_ONLY) {
+      if (c->rplan.ok) {
+        upload(c->d_rops, c->rplan.rops.data(), c->rplan.rops.size() * sizeof(bloch::ROp), c->stream);
+        upload(c->d_rloads, c->rplan.loads.data(), c->rplan.loads.size() * sizeof(bloch::RLoad), c->stream);
+        upload(c->d_rmats, c->rplan.mats.data(), c->rplan.mats.size() * sizeof(double), c->stream);
+        upload(c->d_rmats4, c->rplan.mats4.data(), c->rplan.mats4.size() * sizeof(double), c->stream);
+      }
       ck(cudaStreamSynchronize(c->stream), "set_tables sync");
     }
     c->snap_present.assign(static_cast<size_t>(n_snap), 0);
@@ -871,6 +886,12 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       Variant v = pick_variant(c->precision, n, ncp, c->n_sm, win, hot * 16);
       v.full = full;
       v.win = win;
+      // the resident-table integrator: fully deferred fp32 programs whose tables fit a CTA's shared memory
+      static const bool no_resident = getenv("BLOCH_NO_RESIDENT") != nullptr;  // A/B hook
+      const int res_threads = (defer && !full && !win && c->resident && !no_resident && c->rplan.ok)
+                                  ? bloch::resident_threads(c->rplan, n, c->n_sm) : 0;
+      c->last_resident = res_threads > 0;
+      if (res_threads > 0) v.S = 1;
       int max_t = 512, min_b = 1;
       variant_shape(v, &max_t, &min_b);
       const int64_t slots = int64_t(c->n_sm) * min_b;  // resident CTAs per wave
@@ -879,6 +900,7 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       int64_t threads = (n + slots * waves * v.S - 1) / (slots * waves * v.S);
       threads = ((threads + 31) / 32) * 32;
       threads = std::max<int64_t>(32, std::min<int64_t>(max_t, threads));
+      if (res_threads > 0) threads = res_threads;
       const int64_t spc = threads * v.S;
       const int64_t grid = (n + spc - 1) / spc;
       c->last_launch[0] = v.prec;
@@ -981,7 +1003,36 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
         kp.mx1 = hand_over ? state + (k & 1) * 3 * n : nullptr;
         kp.my1 = hand_over ? state + (k & 1) * 3 * n + n : nullptr;
         kp.mz1 = hand_over ? state + (k & 1) * 3 * n + 2 * n : nullptr;
-        ck(dispatch(v, kp, static_cast<int>(grid), static_cast<int>(threads), st), "integrate kernel");
+        if (res_threads > 0) {
+          bloch::RParams rp{};
+          rp.rops = c->d_rops.as<bloch::ROp>();
+          rp.n_rops = static_cast<int32_t>(c->rplan.rops.size());
+          rp.loads = c->d_rloads.as<bloch::RLoad>();
+          rp.n_loads = static_cast<int32_t>(c->rplan.loads.size());
+          rp.mats = c->d_rmats.as<double>();
+          rp.n_mats = static_cast<int32_t>(c->rplan.mats.size() / 9);
+          rp.mats4 = c->d_rmats4.as<double>();
+          rp.n_mats4 = static_cast<int32_t>(c->rplan.mats4.size() / 4);
+          rp.ops = kp.ops;
+          rp.n = n;
+          rp.mx0 = kp.mx0;
+          rp.my0 = kp.my0;
+          rp.mz0 = kp.mz0;
+          rp.planes = kp.planes;
+          rp.planes32 = kp.planes32;
+          rp.train = kp.train;
+          rp.sc = kp.sc;
+          rp.relax = kp.relax;
+          rp.w1 = n_coils == 1 ? reinterpret_cast<const double2*>(d_w) : nullptr;
+          rp.snaps = kp.snaps;
+          rp.uhi = kp.uhi;
+          rp.ulo = kp.ulo;
+          rp.urows = kp.urows;
+          ck(bloch::launch_resident(rp, c->rplan, static_cast<int>(grid), static_cast<int>(threads), st),
+             "resident integrate kernel");
+        } else {
+          ck(dispatch(v, kp, static_cast<int>(grid), static_cast<int>(threads), st), "integrate kernel");
+        }
         c->launches++;
         if (!hand_over && !defer) {  // after the last integrator launch (the fold of its samples follows)
           if (c->gate_signal) ck(cudaEventRecord(c->gate_signal, st), "gate signal");
@@ -1092,6 +1143,22 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
     if (capturing) abandon_capture(c);
     return fail(BLOCH_E_CUDA, ex.what());
   }
+  return BLOCH_OK;
+}
+
+int bloch_set_resident(bloch_ctx* c, int32_t enable) {
+  if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
+  c->resident = enable != 0;
+  for (bloch_ctx* sub : c->subs) sub->resident = enable != 0;
+  c->drop_graph();
+  return BLOCH_OK;
+}
+
+int bloch_last_resident(const bloch_ctx* c, int32_t* resident, int32_t* bytes_per_spin) {
+  if (!c) return fail(BLOCH_E_INVALID, "ctx is NULL");
+  const bloch_ctx* q = c->subs.empty() ? c : c->subs[0];
+  if (resident) *resident = q->last_resident;
+  if (bytes_per_spin) *bytes_per_spin = q->rplan.ok ? q->rplan.bytes_per_spin : 0;
   return BLOCH_OK;
 }
 

@@ -424,6 +424,19 @@ class BlochEngine:
         (replaces engine.py:303-305 for those windows).  On by default."""
         _capi.check(self._lib.bloch_set_contraction(self._h, 1 if enable else 0), "bloch_set_contraction")
 
+    def set_resident(self, enable: bool) -> None:
+        """Resident-table integrator (bloch_set_resident): the class tables of a CTA's spins held in shared
+        memory for the whole launch (the relax cache of engine.py:292-299, generalised, on chip).  On by
+        default; off keeps the integrator that reads the tables through L2 at every op."""
+        _capi.check(self._lib.bloch_set_resident(self._h, 1 if enable else 0), "bloch_set_resident")
+
+    def last_resident(self) -> Dict[str, int]:
+        """Whether the last call ran the resident-table integrator and the table bytes per spin of the
+        program's resident plan (bloch_last_resident)."""
+        a, b = ctypes.c_int32(), ctypes.c_int32()
+        _capi.check(self._lib.bloch_last_resident(self._h, ctypes.byref(a), ctypes.byref(b)), "bloch_last_resident")
+        return {"resident": a.value, "bytes_per_spin": b.value}
+
     def last_phases(self) -> Dict[str, float]:
         """Integrator vs window-contraction device time (ms) of the last call, the window groups
         contracted and the samples they produced (bloch_last_phases)."""

@@ -318,6 +318,43 @@ def test_gpu_window_sums_without_contraction(name):
         assert e <= STATE_TOL[32], f"{name} snapshot {i} rel L2 {e:.3e}"
 
 
+# --- the resident-table integrator (resident.h) and the integrator that reads the tables through L2 ---
+
+RESIDENT = ["cfg0", "cfg1", "cfg2", "cfg4"]  # must run resident; the small cases: whatever their plan says
+
+
+@pytest.mark.parametrize("name", SMALL + CONFIGS)
+def test_gpu_resident_on_and_off_match_goldens(name):
+    """Fully deferred fp32 programs run resident_integrate_kernel (class tables in shared memory); with it
+    switched off the same programs run integrate_kernel's deferred variant.  Both against the goldens, and
+    against each other much tighter (same fp64 state arithmetic, same U words up to the fp32 u)."""
+    from paper_1305_6861_b200.engine import get_engine
+
+    rec = load_golden(name)
+    eng = get_engine(0, 32)
+    out = {}
+    for on in (True, False):
+        eng.set_resident(on)
+        try:
+            echoes, snaps = compute_block(_tables(name, rec), _block(rec), precision=32)
+            used = eng.last_resident()["resident"]
+        finally:
+            eng.set_resident(True)
+        if not on:
+            assert used == 0
+        elif name in RESIDENT:
+            assert used == 1, (name, eng.last_resident())
+        err = echo_error(rec, echoes)
+        assert err <= KSPACE_TOL[32], f"{name} resident={on} k-space rel L2 {err:.3e}"
+        for i, e in enumerate(snapshot_errors(rec, snaps)):
+            assert e <= STATE_TOL[32], f"{name} resident={on} snapshot {i} rel L2 {e:.3e}"
+        out[on] = (np.asarray(echoes), snaps)
+    assert rel_l2(out[False][0], out[True][0]) <= 2e-6
+    for a, b in zip(out[False][1], out[True][1]):
+        if a is not None:
+            assert rel_l2(a, b) <= 1e-12
+
+
 @pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "se16_box", "tse16", "epi16", "tse_2coil"])
 def test_gpu_contraction_runs_and_matches(name):
     """The long tabulated windows of these programs go through the tensor-core contraction."""
