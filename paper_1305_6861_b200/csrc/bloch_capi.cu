@@ -888,10 +888,11 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       v.win = win;
       // the resident-table integrator: fully deferred fp32 programs whose tables fit a CTA's shared memory
       static const bool no_resident = getenv("BLOCH_NO_RESIDENT") != nullptr;  // A/B hook
+      int res_s = 1;
       const int res_threads = (defer && !full && !win && c->resident && !no_resident && c->rplan.ok)
-                                  ? bloch::resident_threads(c->rplan, n, c->n_sm) : 0;
+                                  ? bloch::resident_threads(c->rplan, n, c->n_sm, &res_s) : 0;
       c->last_resident = res_threads > 0;
-      if (res_threads > 0) v.S = 1;
+      if (res_threads > 0) v.S = res_s;
       int max_t = 512, min_b = 1;
       variant_shape(v, &max_t, &min_b);
       const int64_t slots = int64_t(c->n_sm) * min_b;  // resident CTAs per wave
@@ -1028,7 +1029,7 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
           rp.uhi = kp.uhi;
           rp.ulo = kp.ulo;
           rp.urows = kp.urows;
-          ck(bloch::launch_resident(rp, c->rplan, static_cast<int>(grid), static_cast<int>(threads), st),
+          ck(bloch::launch_resident(rp, c->rplan, v.S, static_cast<int>(grid), static_cast<int>(threads), st),
              "resident integrate kernel");
         } else {
           ck(dispatch(v, kp, static_cast<int>(grid), static_cast<int>(threads), st), "integrate kernel");

@@ -7,6 +7,7 @@
 // pulse, then its events in order; every compiled op covers a contiguous run
 // of that walk, so the device replays the same operator sequence.
 #include "program_host.h"
+#include "resident.h"
 
 #include <algorithm>
 #include <array>
@@ -57,7 +58,7 @@ void find_chirp_classes(Program& prog);
 void fuse_pulses(Program& prog);
 void find_train_classes(Program& prog);
 void assign_planes(Program& prog);
-void defer_windows(Program& prog);
+void defer_windows(Program& prog, int short_runs);
 
 void compile_program(const TablesView& t, Program& prog) {
   prog = Program();
@@ -489,7 +490,35 @@ void fuse_intervals(Program& prog, const std::function<int32_t(double)>& relax_c
   find_train_classes(prog);
   fuse_pulses(prog);
   assign_planes(prog);
-  defer_windows(prog);
+  // Short runs (tabulated chirps, single-sample events) join the contraction when that makes the program
+  // fully deferred and covered by the resident-table integrator (resident.h): config 3 4.64 vs 5.82 ms
+  // (profiles/r3e_shards.txt).  Otherwise they cost more in the contraction than in the integrator (each
+  // group is a 64-sample M-tile pass over every spin whatever its length: 7.22 vs 5.70 ms on config 3 with
+  // integrate_kernel, profiles/r2gg_short_runs.txt).  BLOCH_DEFER_SHORT=1 / 0 forces either.
+  static const int short_env = [] {
+    const char* e = getenv("BLOCH_DEFER_SHORT");
+    return e ? (atoi(e) != 0 ? 1 : 0) : -1;
+  }();
+  if (short_env == 1) {
+    defer_windows(prog, 1);
+    return;
+  }
+  if (short_env != 0) {
+    for (int mode = 1; mode <= 2; ++mode) {  // a few stragglers (a ramp cut by a snapshot) as groups of their own
+      Program alt = prog;
+      defer_windows(alt, mode);
+      ResidentPlan plan;
+      resident_compile(alt, plan);
+      size_t small = 0;
+      for (const WinGroup& g : alt.groups)
+        small += !(g.chirp == 0 && g.count >= kMinDeferWindow) && g.n_windows < kMinDeferGroup;
+      if (plan.ok && small <= 4) {
+        prog = std::move(alt);
+        return;
+      }
+    }
+  }
+  defer_windows(prog, 0);
 }
 
 // The deferred-window view (program.h OP_UWIN, contract.h): every tabulated window of at least
@@ -497,7 +526,9 @@ void fuse_intervals(Program& prog, const std::function<int32_t(double)>& relax_c
 // tensor-core product per group instead of per-warp sums in the integrator.  U rows are numbered group
 // by group, in op order inside a group.  The remaining sampled ops keep their samples under new
 // compact ids (dsample_g), so the integrator's partial rows only hold those.
-void defer_windows(Program& prog) {
+// short_runs: 0 = long windows only; 1 = also tabulated chirps and single-sample events in groups of at
+// least kMinDeferGroup; 2 = also their smaller groups (one contraction launch each)
+void defer_windows(Program& prog, int short_runs) {
   prog.dops.clear();
   prog.dsample_g.clear();
   prog.groups.clear();
@@ -550,14 +581,6 @@ void defer_windows(Program& prog) {
   using GKey = std::array<int32_t, 5>;  // (chirp, z / r0 plane, q plane, conj, count)
   std::map<GKey, std::vector<Cand>> by_key;
   std::vector<GKey> key_order;
-  // Short runs (chirps, single samples) are deferred only on request (BLOCH_DEFER_SHORT=1): each group costs a
-  // 64-sample M-tile pass over every spin whatever its length, so config 3's four 10-sample ramp classes and
-  // its single samples cost 2.4 ms in the contraction against 1.5 ms in the integrator (7.22 vs 5.70 ms,
-  // profiles/r2gg_short_runs.txt).  Whole EPI lines as one group (a piecewise generator) would fix that.
-  static const bool short_runs = [] {
-    const char* e = getenv("BLOCH_DEFER_SHORT");
-    return e && atoi(e) != 0;
-  }();
   for (size_t k = 0; k < prog.ops.size(); ++k) {
     const DevOp& op = prog.ops[k];
     GKey key;
@@ -585,7 +608,7 @@ void defer_windows(Program& prog) {
   for (const GKey& key : key_order) {
     const std::vector<Cand>& mem = by_key[key];
     const bool long_window = key[0] == 0 && key[4] >= kMinDeferWindow;
-    if (!long_window && static_cast<int32_t>(mem.size()) < kMinDeferGroup) continue;  // short runs: groups only
+    if (!long_window && short_runs < 2 && static_cast<int32_t>(mem.size()) < kMinDeferGroup) continue;
     WinGroup g{key[1], key[4], row, static_cast<int32_t>(mem.size()), key[0], key[2], key[3]};
     prog.groups.push_back(g);
     for (const Cand& c : mem) {
@@ -668,7 +691,8 @@ void find_chirp_classes(Program& prog) {
     if (op.kind != OP_CHIRP) continue;
     const Key k = key_of(op);
     op.rot = -1;
-    if (uses[k] < 2) continue;
+    // a ramp that occurs once (e.g. cut short by a snapshot) is a class too: tabulating it costs what its
+    // on-the-fly evaluation would, and a program whose chirps are all classes can be fully deferred
     auto f = ids.find(k);
     if (f == ids.end()) {
       if (prog.chirp_classes.size() >= kMaxChirp) continue;

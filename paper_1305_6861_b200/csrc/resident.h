@@ -67,7 +67,8 @@ struct ResidentPlan {
 constexpr int kResidentMaxMats = 128;
 constexpr int kResidentMaxMats4 = 1024;
 constexpr int kResidentMaxThreads = 1024;
-constexpr int kResidentMinThreads = 128;       // below this many spins per SM-resident CTA the planes do not pay
+constexpr int kResidentMinThreads = 128;   // below this many spins per CTA the resident tables do not pay
+constexpr int kResidentTwoSpinMin = 768;   // CTAs of at least this many spins run two spins per thread
 constexpr int kResidentSmemBytes = 227 * 1024;
 
 // Compile the deferred program into resident form; plan.ok = false when an op is not covered.
@@ -96,8 +97,10 @@ struct RParams {
   int64_t urows;
 };
 
-// threads per CTA for n spins on n_sm SMs (0: the tables of kResidentMinThreads spins do not fit)
-int resident_threads(const ResidentPlan& plan, int64_t n, int n_sm);
-cudaError_t launch_resident(const RParams& rp, const ResidentPlan& plan, int grid, int threads, cudaStream_t stream);
+// threads per CTA and spins per thread (1 or 2) for n spins on n_sm SMs (0: the tables of
+// kResidentMinThreads spins do not fit)
+int resident_threads(const ResidentPlan& plan, int64_t n, int n_sm, int* spins_per_thread);
+cudaError_t launch_resident(const RParams& rp, const ResidentPlan& plan, int spins_per_thread, int grid, int threads,
+                            cudaStream_t stream);
 
 }  // namespace bloch

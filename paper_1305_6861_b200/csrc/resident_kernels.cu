@@ -192,23 +192,33 @@ void resident_compile(const Program& P, ResidentPlan& plan) {
 
 constexpr int kResidentFixedBytes = 2 * 64 * 32;  // the two staged record chunks (kRecChunk x 32 B)
 
-// shared memory ahead of the tables: the axis pulses (32 B each), then the general ones (72 B each)
-static size_t resident_mats_bytes(const ResidentPlan& plan) {
-  return plan.mats4.size() * 8 + ((plan.mats.size() * 8 + 15) & ~size_t(15));
-}
+// shared memory ahead of the tables: the axis pulses (32 B each), then the general ones (80 B each: 9
+// entries padded so that every matrix starts on a 16-byte boundary)
+static size_t resident_mats_bytes(const ResidentPlan& plan) { return plan.mats4.size() * 8 + plan.mats.size() / 9 * 80; }
 
-int resident_threads(const ResidentPlan& plan, int64_t n, int n_sm) {
+int resident_threads(const ResidentPlan& plan, int64_t n, int n_sm, int* spins_per_thread) {
   if (!plan.ok || n <= 0) return 0;
   const int64_t room = kResidentSmemBytes - 1024 - kResidentFixedBytes - static_cast<int64_t>(resident_mats_bytes(plan));
-  int64_t cap = plan.bytes_per_spin > 0 ? room / plan.bytes_per_spin : kResidentMaxThreads;
-  cap = std::min<int64_t>(kResidentMaxThreads, (cap / 32) * 32);
+  int64_t cap = plan.bytes_per_spin > 0 ? room / plan.bytes_per_spin : kResidentMaxThreads;  // spins per CTA
+  cap = std::min<int64_t>(kResidentMaxThreads, (cap / 64) * 64);
   if (cap < kResidentMinThreads) return 0;
   // equal waves of one CTA per SM
   const int64_t per_wave = static_cast<int64_t>(n_sm) * cap;
   const int64_t waves = (n + per_wave - 1) / per_wave;
-  int64_t t = (n + n_sm * waves - 1) / (n_sm * waves);
-  t = ((t + 31) / 32) * 32;
-  return static_cast<int>(std::max<int64_t>(32, std::min<int64_t>(cap, t)));
+  int64_t spins = (n + n_sm * waves - 1) / (n_sm * waves);  // per CTA
+  static const int force_s = [] {  // experiment hook: BLOCH_RESIDENT_SPINS=1|2
+    const char* e = getenv("BLOCH_RESIDENT_SPINS");
+    return e ? atoi(e) : 0;
+  }();
+  // two spins per thread amortise the record decode, the pulse loads and the branches; one spin per thread
+  // keeps enough warps when a CTA has few spins (shards)
+  int S = spins >= kResidentTwoSpinMin ? 2 : 1;
+  if (force_s == 1 || force_s == 2) S = force_s;
+  const int64_t q = 32 * S;
+  spins = ((spins + q - 1) / q) * q;
+  spins = std::max<int64_t>(q, std::min<int64_t>(cap, spins));
+  if (spins_per_thread) *spins_per_thread = S;
+  return static_cast<int>(spins / S);
 }
 
 // ---------------------------------------------------------------------------
@@ -262,43 +272,82 @@ __device__ __forceinline__ void split_bf16x2(float re, float im, uint32_t& hi, u
 
 constexpr int kRecChunk = 64;  // staged records per chunk (two chunks of 32-byte records: 4 KB)
 
+// staged op kinds: bit 2 = the common exit (m+ *= C, mz = A mz + B)
+enum : int { SK_NOP = 0, SK_FLY = 1, SK_TRAIN = 2, SK_TAB = 4, SK_PROG = 5, SK_UWIN = 6, SK_UCHIRP = 7 };
+constexpr int kSnapBit = 16;  // w0.z: the event takes a snapshot (index in w0.w)
+
+// one interval evaluated per spin: precession (+ relaxation), engine.py:288-302 (rare: out of line)
+// (state by value: a reference would pin the caller's state registers to local memory)
+__device__ __noinline__ double3 fly_interval(const ROp* rop, const DevOp* ops, const void* sc, const double* relax,
+                                             int64_t n, int64_t i, double x, double y, double z) {
+  const int flags = __ldg(&rop->flags), cls = __ldg(&rop->cls);
+  if (!(flags & EV_MOVE)) return make_double3(x, y, z);
+  const DevOp* op = ops + __ldg(&rop->src);
+  const double dt = __ldg(&op->p[0]), dmx = __ldg(&op->p[1]), dmy = __ldg(&op->p[2]), dmz = __ldg(&op->p[3]);
+  const double2* s = reinterpret_cast<const double2*>(static_cast<const SpinConst*>(sc) + i);
+  const double2 s0 = __ldg(s), s1 = __ldg(s + 1), s2 = __ldg(s + 2);  // (x, y), (z, dw), (m0, r1)
+  const double2 e = cls >= 0 ? __ldg(reinterpret_cast<const double2*>(relax) + (static_cast<int64_t>(cls) * n + i))
+                             : make_double2(1.0, 1.0);
+  const double th = fma(s1.x, dmz, fma(s0.y, dmy, s0.x * dmx)) + s1.y * dt;  // engine.py:289
+  double sn, cs;
+  sincos(r_reduce_2pi(th), &sn, &cs);
+  const double ms = -sn;
+  const double nx = e.y * (cs * x - ms * y);  // clockwise: (c - i s)(x + i y), bloch.py:10-17
+  y = e.y * (cs * y + ms * x);
+  x = nx;
+  if (cls >= 0) z = fma(z, e.x, s2.x * (1.0 - e.x));
+  return make_double3(x, y, z);
+}
+
 }  // namespace
 
 // Staged record (shared memory, 32 bytes), decoded once per chunk per CTA from the 48-byte ROp:
-//   w0 = (kind, shared address of the fused pulse or 0, tmode | arg << 2, U byte offset / snapshot index)
-//   w1 = shared addresses of the op's four tables (thread 0's word; a thread adds tid * 16 or tid * 8)
-// arg: R_UWIN lead flag, R_PROG advance.
-__global__ void __launch_bounds__(kResidentMaxThreads, 1) resident_integrate_kernel(const RParams rp) {
+//   w0 = (staged kind, shared address of the fused pulse or 0, tmode | arg << 2 | snapshot bit,
+//         U byte offset (windows) / snapshot index (events))
+//   w1 = shared addresses (slot 0's word) of C, (A, B), and two more: PROG q; UWIN Cpre, z; TRAIN the row
+// arg: UWIN lead flag, PROG advance.  A thread's word of slot s: + (s blockDim + tid) * 16 (or * 8).
+template <int S>
+__global__ void __launch_bounds__(kResidentMaxThreads / S, 1) resident_integrate_kernel(const RParams rp) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, bd = blockDim.x;
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * bd + tid;
-  const bool act = i < rp.n;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * (S * bd) + tid;  // spin of slot 0; slot s: + s bd
   const uint32_t s_base = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
   const uint32_t s_rec = s_base;                                    // [2][kRecChunk] staged records
   const uint32_t s_m4 = s_rec + 2 * kRecChunk * 32;                 // axis pulses, 32 B each
-  const uint32_t s_m9 = s_m4 + 32u * rp.n_mats4;                    // general pulses, 72 B each
-  const uint32_t s_area = s_m9 + ((72u * rp.n_mats + 15u) & ~15u);  // the tables, [table][thread]
+  const uint32_t s_m9 = s_m4 + 32u * rp.n_mats4;                    // general pulses, 80 B each
+  const uint32_t s_area = s_m9 + 80u * rp.n_mats;                   // the tables, [table][slot][thread]
   {
     double* m4 = reinterpret_cast<double*>(smem_raw + 2 * kRecChunk * 32);
     double* m9 = m4 + 4 * rp.n_mats4;
     for (int k = tid; k < 4 * rp.n_mats4; k += bd) m4[k] = __ldg(rp.mats4 + k);
-    for (int k = tid; k < 9 * rp.n_mats; k += bd) m9[k] = __ldg(rp.mats + k);
+    for (int k = tid; k < 9 * rp.n_mats; k += bd) m9[(k / 9) * 10 + k % 9] = __ldg(rp.mats + k);
   }
-  const uint32_t t16 = s_area + tid * 16, t8 = s_area + tid * 8;
+  bool act[S];
+  uint32_t t16[S], t8[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    act[s] = base + s * bd < rp.n;
+    t16[s] = (s * bd + tid) * 16;
+    t8[s] = (s * bd + tid) * 8;
+  }
   // the CTA's tables: each value crosses L2 once per launch
   for (int j = 0; j < rp.n_loads; ++j) {
     const RLoad* L = rp.loads + j;
     const int kind = __ldg(&L->kind), id = __ldg(&L->id);
-    const uint32_t off = static_cast<uint32_t>(__ldg(&L->off)) * bd;
-    if (kind == 1) {
-      sts_f2(t8 + off, act ? __ldg(rp.planes32 + (static_cast<int64_t>(id) * rp.n + i)) : make_float2(1.f, 0.f));
-    } else if (kind == 0) {
-      sts_d2(t16 + off, act ? __ldg(rp.planes + (static_cast<int64_t>(id) * rp.n + i)) : make_double2(1.0, 0.0));
-    } else {
-      const int word = __ldg(&L->word);
-      sts_d2(t16 + off, act ? __ldg(reinterpret_cast<const double2*>(rp.train) +
-                                    ((static_cast<int64_t>(id) * rp.n + i) * 6 + word))
-                            : make_double2(0.0, 0.0));
+    const uint32_t off = s_area + static_cast<uint32_t>(__ldg(&L->off)) * (S * bd);
+    const int word = __ldg(&L->word);
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int64_t i = base + s * bd;
+      if (kind == 1) {
+        sts_f2(off + t8[s], act[s] ? __ldg(rp.planes32 + (static_cast<int64_t>(id) * rp.n + i)) : make_float2(1.f, 0.f));
+      } else if (kind == 0) {
+        sts_d2(off + t16[s], act[s] ? __ldg(rp.planes + (static_cast<int64_t>(id) * rp.n + i)) : make_double2(1.0, 0.0));
+      } else {
+        sts_d2(off + t16[s], act[s] ? __ldg(reinterpret_cast<const double2*>(rp.train) +
+                                           ((static_cast<int64_t>(id) * rp.n + i) * 6 + word))
+                                    : make_double2(0.0, 0.0));
+      }
     }
   }
   // stage chunk `ch` of the op records into buffer ch & 1
@@ -309,16 +358,25 @@ __global__ void __launch_bounds__(kResidentMaxThreads, 1) resident_integrate_ker
       const int4* g = reinterpret_cast<const int4*>(rp.rops + o);
       const int4 a = __ldg(g), b = __ldg(g + 1), c = __ldg(g + 2);
       const int kind = a.x, pre = a.y, tmode = a.z;
-      int4 w0, w1;
-      w0.x = kind;
-      w0.y = pre < 0 ? 0 : static_cast<int>((tmode == 1 || tmode == 2) ? s_m4 + 32u * pre : s_m9 + 72u * pre);
-      const int arg = kind == R_UWIN ? (a.w != 0) : kind == R_PROG ? c.y : 0;
-      w0.z = tmode | (arg << 2);
-      w0.w = (kind == R_UWIN || kind == R_UCHIRP) ? c.x * 64 : a.w;
-      w1.x = static_cast<int>(s_area + static_cast<uint32_t>(b.x) * bd);
-      w1.y = static_cast<int>(s_area + static_cast<uint32_t>(b.y) * bd);
-      w1.z = static_cast<int>(s_area + static_cast<uint32_t>(b.z) * bd);
-      w1.w = static_cast<int>(s_area + static_cast<uint32_t>(b.w) * bd);
+      const uint32_t sb = S * bd;
+      auto at = [&](int off) { return static_cast<int>(s_area + static_cast<uint32_t>(off) * sb); };
+      int4 w0, w1 = make_int4(0, 0, 0, 0);
+      int sk = SK_NOP, arg = 0;
+      w0.w = a.w;  // events: snapshot index
+      switch (kind) {
+        case R_TAB: sk = SK_TAB; w1.x = at(b.x); w1.y = at(b.y); break;
+        case R_PROG: sk = SK_PROG; arg = c.y; w1.x = at(b.x); w1.y = at(b.w); w1.z = at(b.y); break;
+        case R_UWIN: sk = SK_UWIN; arg = a.w != 0; w0.w = c.x * 64; w1.x = at(b.z); w1.y = at(b.w); w1.z = at(b.x);
+                     w1.w = at(b.y); break;
+        case R_UCHIRP: sk = SK_UCHIRP; w0.w = c.x * 64; w1.x = at(b.z); w1.y = at(b.w); break;
+        case R_TRAIN: sk = SK_TRAIN; w1.z = at(b.x); break;
+        case R_FLY: sk = SK_FLY; break;
+        default: break;
+      }
+      const bool snap = (kind == R_TAB || kind == R_PROG || kind == R_FLY) && a.w >= 0 && rp.snaps != nullptr;
+      w0.x = sk;
+      w0.y = pre < 0 ? 0 : static_cast<int>((tmode == 1 || tmode == 2) ? s_m4 + 32u * pre : s_m9 + 80u * pre);
+      w0.z = tmode | (arg << 2) | (snap ? kSnapBit : 0);
       const uint32_t dst = s_rec + ((ch & 1) * kRecChunk + r) * 32;
       sts_i4(dst, w0);
       sts_i4(dst + 16, w1);
@@ -327,148 +385,155 @@ __global__ void __launch_bounds__(kResidentMaxThreads, 1) resident_integrate_ker
   stage(0);
   __syncthreads();  // the matrices and chunk 0 (the tables are read only by the thread that wrote them)
 
-  double x = act ? rp.mx0[i] : 0.0, y = act ? rp.my0[i] : 0.0, z = act ? rp.mz0[i] : 0.0;
-  // contract_u_index(rows, r, i) = ((i >> 4) rows + r) 16 + (i & 15): this spin's word of row 0
-  const int64_t ubase = act ? (i >> 4) * rp.urows * 16 + (i & 15) : 0;
-  const char* uhi0 = reinterpret_cast<const char*>(rp.uhi + ubase);
-  const char* ulo0 = reinterpret_cast<const char*>(rp.ulo + ubase);
-  const uint32_t tid16 = tid * 16, tid8 = tid * 8;
+  double x[S], y[S], z[S];
+  const char *uhi0[S], *ulo0[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int64_t i = base + s * bd;
+    x[s] = act[s] ? rp.mx0[i] : 0.0;
+    y[s] = act[s] ? rp.my0[i] : 0.0;
+    z[s] = act[s] ? rp.mz0[i] : 0.0;
+    // contract_u_index(rows, r, i) = ((i >> 4) rows + r) 16 + (i & 15): this spin's word of row 0
+    const int64_t ub = act[s] ? (i >> 4) * rp.urows * 16 + (i & 15) : 0;
+    uhi0[s] = reinterpret_cast<const char*>(rp.uhi + ub);
+    ulo0[s] = reinterpret_cast<const char*>(rp.ulo + ub);
+  }
 
   const int n_chunks = (rp.n_rops + kRecChunk - 1) / kRecChunk;
   for (int ch = 0; ch < n_chunks; ++ch) {
     if (ch + 1 < n_chunks) stage(ch + 1);  // lands during this chunk; the barrier below publishes it
     const int cnt = min(kRecChunk, rp.n_rops - ch * kRecChunk);
     uint32_t ra = s_rec + (ch & 1) * kRecChunk * 32;
-    int4 n0 = lds_i4(ra), n1 = lds_i4(ra + 16);
-    for (int r = 0; r < cnt; ++r) {
-      const int4 w0 = n0, w1 = n1;
-      ra += 32;  // the next record while this one runs (the slot after the buffer's last is never used)
-      if (r + 1 < cnt) {
-        n0 = lds_i4(ra);
-        n1 = lds_i4(ra + 16);
-      }
+    for (int r = 0; r < cnt; ++r, ra += 32) {
+      const int4 w0 = lds_i4(ra), w1 = lds_i4(ra + 16);
       const int kind = w0.x;
       if (w0.y) {  // a fused hard pulse first (bloch.py:124-139)
         const uint32_t ma = static_cast<uint32_t>(w0.y);
         const int tmode = w0.z & 3;
         if (tmode == 1) {  // about x: (x, r4 y + r5 z, r7 y + r8 z)
           const double2 m0 = lds_d2(ma), m1 = lds_d2(ma + 16);
-          const double ny = m0.x * y + m0.y * z;
-          z = m1.x * y + m1.y * z;
-          y = ny;
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            const double ny = m0.x * y[s] + m0.y * z[s];
+            z[s] = m1.x * y[s] + m1.y * z[s];
+            y[s] = ny;
+          }
         } else if (tmode == 2) {  // about y: (r0 x + r2 z, y, r6 x + r8 z)
           const double2 m0 = lds_d2(ma), m1 = lds_d2(ma + 16);
-          const double nx = m0.x * x + m0.y * z;
-          z = m1.x * x + m1.y * z;
-          x = nx;
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            const double nx = m0.x * x[s] + m0.y * z[s];
+            z[s] = m1.x * x[s] + m1.y * z[s];
+            x[s] = nx;
+          }
         } else {
           const double2 m0 = lds_d2(ma), m1 = lds_d2(ma + 16), m2 = lds_d2(ma + 32), m3 = lds_d2(ma + 48);
           double m8;
           asm volatile("ld.shared.f64 %0, [%1];" : "=d"(m8) : "r"(ma + 64));
-          const double nx = m0.x * x + m0.y * y + m1.x * z;
-          const double ny = m1.y * x + m2.x * y + m2.y * z;
-          z = m3.x * x + m3.y * y + m8 * z;
-          x = nx;
-          y = ny;
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            const double nx = m0.x * x[s] + m0.y * y[s] + m1.x * z[s];
+            const double ny = m1.y * x[s] + m2.x * y[s] + m2.y * z[s];
+            z[s] = m3.x * x[s] + m3.y * y[s] + m8 * z[s];
+            x[s] = nx;
+            y[s] = ny;
+          }
         }
       }
-      if (kind == R_PROG) {
-        const uint32_t pa = static_cast<uint32_t>(w1.x) + tid16;
-        const double2 cc = lds_d2(pa);
-        const double2 ab = lds_d2(static_cast<uint32_t>(w1.w) + tid16);
-        if (w0.z >> 2) {  // advance the running factor by q or q^2
-          const double2 q = lds_d2(static_cast<uint32_t>(w1.y) + tid16);
-          sts_d2(pa, make_double2(cc.x * q.x - cc.y * q.y, cc.x * q.y + cc.y * q.x));
+      if (kind & 4) {  // m+ *= C, mz = A mz + B, after the kind's own work on the entry state
+        double2 cc[S], ab[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          cc[s] = lds_d2(static_cast<uint32_t>(w1.x) + t16[s]);
+          ab[s] = lds_d2(static_cast<uint32_t>(w1.y) + t16[s]);
         }
-        const double nx = cc.x * x - cc.y * y;
-        y = cc.x * y + cc.y * x;
-        x = nx;
-        z = fma(z, ab.x, ab.y);
-      } else if (kind == R_UWIN) {
-        const float2 cp = lds_f2(static_cast<uint32_t>(w1.x) + tid8);
-        const double2 cc = lds_d2(static_cast<uint32_t>(w1.z) + tid16);
-        const double2 ab = lds_d2(static_cast<uint32_t>(w1.w) + tid16);
-        // u = Cpre m in fp32 (two conversions of the state): equal to ~2^-24, inside the bf16 hi + lo split
-        const float fx = static_cast<float>(x), fy = static_cast<float>(y);
-        float ur = cp.x * fx - cp.y * fy, ui = cp.x * fy + cp.y * fx;
-        if (!(w0.z >> 2)) {  // no leading no-op sample: the first sample follows one interval
-          const float2 zz = lds_f2(static_cast<uint32_t>(w1.y) + tid8);
-          const float t = ur * zz.x - ui * zz.y;
-          ui = ur * zz.y + ui * zz.x;
-          ur = t;
+        if (kind == SK_PROG) {
+          if (w0.z & 12) {  // advance the running factor by q or q^2
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+              const double2 q = lds_d2(static_cast<uint32_t>(w1.z) + t16[s]);
+              sts_d2(static_cast<uint32_t>(w1.x) + t16[s],
+                     make_double2(cc[s].x * q.x - cc[s].y * q.y, cc[s].x * q.y + cc[s].y * q.x));
+            }
+          }
+        } else if (kind == SK_UWIN) {
+          float2 cp[S], zz[S];
+          const bool lead = (w0.z & 4) != 0;
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            cp[s] = lds_f2(static_cast<uint32_t>(w1.z) + t8[s]);
+            if (!lead) zz[s] = lds_f2(static_cast<uint32_t>(w1.w) + t8[s]);
+          }
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            // u = Cpre m in fp32 (two conversions of the state): equal to ~2^-24, inside the bf16 hi + lo split
+            const float fx = static_cast<float>(x[s]), fy = static_cast<float>(y[s]);
+            float ur = cp[s].x * fx - cp[s].y * fy, ui = cp[s].x * fy + cp[s].y * fx;
+            if (!lead) {  // no leading no-op sample: the first sample follows one interval
+              const float t = ur * zz[s].x - ui * zz[s].y;
+              ui = ur * zz[s].y + ui * zz[s].x;
+              ur = t;
+            }
+            if (act[s]) {
+              uint32_t hi, lo;
+              split_bf16x2(ur, ui, hi, lo);
+              __stcs(reinterpret_cast<uint32_t*>(const_cast<char*>(uhi0[s] + w0.w)), hi);  // streamed: read by the
+              __stcs(reinterpret_cast<uint32_t*>(const_cast<char*>(ulo0[s] + w0.w)), lo);  // contraction
+            }
+          }
+        } else if (kind == SK_UCHIRP) {
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            if (!act[s]) continue;
+            const double2 w = rp.w1 != nullptr ? __ldg(rp.w1 + (base + s * bd)) : make_double2(1.0, 0.0);
+            const float wx = static_cast<float>(w.x), wy = static_cast<float>(w.y);
+            const float fx = static_cast<float>(x[s]), fy = static_cast<float>(y[s]);
+            uint32_t hi, lo;
+            split_bf16x2(wx * fx - wy * fy, wx * fy + wy * fx, hi, lo);
+            __stcs(reinterpret_cast<uint32_t*>(const_cast<char*>(uhi0[s] + w0.w)), hi);
+            __stcs(reinterpret_cast<uint32_t*>(const_cast<char*>(ulo0[s] + w0.w)), lo);
+          }
         }
-        if (act) {
-          uint32_t hi, lo;
-          split_bf16x2(ur, ui, hi, lo);
-          __stcs(reinterpret_cast<uint32_t*>(const_cast<char*>(uhi0 + w0.w)), hi);  // streamed: read by the contraction
-          __stcs(reinterpret_cast<uint32_t*>(const_cast<char*>(ulo0 + w0.w)), lo);
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          const double nx = cc[s].x * x[s] - cc[s].y * y[s];
+          y[s] = cc[s].x * y[s] + cc[s].y * x[s];
+          x[s] = nx;
+          z[s] = fma(z[s], ab[s].x, ab[s].y);
         }
-        const double nx = cc.x * x - cc.y * y;
-        y = cc.x * y + cc.y * x;
-        x = nx;
-        z = fma(z, ab.x, ab.y);
-        continue;
-      } else if (kind == R_TAB) {
-        const double2 cc = lds_d2(static_cast<uint32_t>(w1.x) + tid16);
-        const double2 ab = lds_d2(static_cast<uint32_t>(w1.y) + tid16);
-        const double nx = cc.x * x - cc.y * y;
-        y = cc.x * y + cc.y * x;
-        x = nx;
-        z = fma(z, ab.x, ab.y);
-      } else if (kind == R_TRAIN) {
-        const uint32_t ta = static_cast<uint32_t>(w1.x) + tid16, st = 16u * bd;
-        const double2 t0 = lds_d2(ta), t1 = lds_d2(ta + st), t2 = lds_d2(ta + 2 * st), t3 = lds_d2(ta + 3 * st),
-                      t4 = lds_d2(ta + 4 * st), t5 = lds_d2(ta + 5 * st);
-        const double nx = fma(t0.x, x, fma(t0.y, y, fma(t1.x, z, t4.y)));
-        const double ny = fma(t1.y, x, fma(t2.x, y, fma(t2.y, z, t5.x)));
-        z = fma(t3.x, x, fma(t3.y, y, fma(t4.x, z, t5.y)));
-        x = nx;
-        y = ny;
-        continue;
-      } else if (kind == R_UCHIRP) {
-        const double2 cc = lds_d2(static_cast<uint32_t>(w1.z) + tid16);
-        const double2 ab = lds_d2(static_cast<uint32_t>(w1.w) + tid16);
-        if (act) {
-          const double2 w = rp.w1 != nullptr ? __ldg(rp.w1 + i) : make_double2(1.0, 0.0);
-          const float wx = static_cast<float>(w.x), wy = static_cast<float>(w.y);
-          const float fx = static_cast<float>(x), fy = static_cast<float>(y);
-          uint32_t hi, lo;
-          split_bf16x2(wx * fx - wy * fy, wx * fy + wy * fx, hi, lo);
-          __stcs(reinterpret_cast<uint32_t*>(const_cast<char*>(uhi0 + w0.w)), hi);
-          __stcs(reinterpret_cast<uint32_t*>(const_cast<char*>(ulo0 + w0.w)), lo);
+      } else if (kind == SK_TRAIN) {
+        const uint32_t st = 16u * S * bd;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          const uint32_t ta = static_cast<uint32_t>(w1.z) + t16[s];
+          const double2 t0 = lds_d2(ta), t1 = lds_d2(ta + st), t2 = lds_d2(ta + 2 * st), t3 = lds_d2(ta + 3 * st),
+                        t4 = lds_d2(ta + 4 * st), t5 = lds_d2(ta + 5 * st);
+          const double nx = fma(t0.x, x[s], fma(t0.y, y[s], fma(t1.x, z[s], t4.y)));
+          const double ny = fma(t1.y, x[s], fma(t2.x, y[s], fma(t2.y, z[s], t5.x)));
+          z[s] = fma(t3.x, x[s], fma(t3.y, y[s], fma(t4.x, z[s], t5.y)));
+          x[s] = nx;
+          y[s] = ny;
         }
-        const double nx = cc.x * x - cc.y * y;
-        y = cc.x * y + cc.y * x;
-        x = nx;
-        z = fma(z, ab.x, ab.y);
-        continue;
-      } else if (kind == R_FLY) {  // one interval per spin: precession (+ relaxation), engine.py:288-302
-        const ROp* rop = rp.rops + (ch * kRecChunk + r);
-        const int flags = __ldg(&rop->flags), cls = __ldg(&rop->cls);
-        if ((flags & EV_MOVE) && act) {
-          const DevOp* op = rp.ops + __ldg(&rop->src);
-          const double dt = __ldg(&op->p[0]), dmx = __ldg(&op->p[1]), dmy = __ldg(&op->p[2]), dmz = __ldg(&op->p[3]);
-          const double2* s = reinterpret_cast<const double2*>(static_cast<const SpinConst*>(rp.sc) + i);
-          const double2 s0 = __ldg(s), s1 = __ldg(s + 1), s2 = __ldg(s + 2);  // (x, y), (z, dw), (m0, r1)
-          const double2 e = cls >= 0 ? __ldg(reinterpret_cast<const double2*>(rp.relax) +
-                                             (static_cast<int64_t>(cls) * rp.n + i))
-                                     : make_double2(1.0, 1.0);
-          const double th = fma(s1.x, dmz, fma(s0.y, dmy, s0.x * dmx)) + s1.y * dt;  // engine.py:289
-          double sn, cs;
-          sincos(r_reduce_2pi(th), &sn, &cs);
-          const double ms = -sn;
-          const double nx = e.y * (cs * x - ms * y);  // clockwise: (c - i s)(x + i y), bloch.py:10-17
-          y = e.y * (cs * y + ms * x);
-          x = nx;
-          if (cls >= 0) z = fma(z, e.x, s2.x * (1.0 - e.x));
-        }
+      } else if (kind == SK_FLY) {
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+          if (act[s]) {
+            const double3 m = fly_interval(rp.rops + (ch * kRecChunk + r), rp.ops, rp.sc, rp.relax, rp.n, base + s * bd,
+                                           x[s], y[s], z[s]);
+            x[s] = m.x;
+            y[s] = m.y;
+            z[s] = m.z;
+          }
       }
-      // events: the optional snapshot (engine.py:306-308)
-      if (kind != R_NOP && w0.w >= 0 && rp.snaps != nullptr && act) {
-        double* q = rp.snaps + (static_cast<int64_t>(w0.w) * rp.n + i) * 3;
-        q[0] = x;
-        q[1] = y;
-        q[2] = z;
+      if (w0.z & kSnapBit) {  // events: the optional snapshot (engine.py:306-308)
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          if (!act[s]) continue;
+          double* q = rp.snaps + (static_cast<int64_t>(w0.w) * rp.n + (base + s * bd)) * 3;
+          q[0] = x[s];
+          q[1] = y[s];
+          q[2] = z[s];
+        }
       }
     }
     __syncthreads();  // chunk ch + 1 staged; every warp is done with chunk ch's buffer before it is restaged
@@ -477,8 +542,8 @@ __global__ void __launch_bounds__(kResidentMaxThreads, 1) resident_integrate_ker
 
 static std::mutex g_res_mu;
 
-cudaError_t launch_resident(const RParams& rp, const ResidentPlan& plan, int grid, int threads, cudaStream_t stream) {
-  const size_t smem = kResidentFixedBytes + resident_mats_bytes(plan) + static_cast<size_t>(plan.bytes_per_spin) * threads;
+template <int S>
+static cudaError_t launch_resident_s(const RParams& rp, size_t smem, int grid, int threads, cudaStream_t stream) {
   static size_t smem_set[kMaxDevices] = {};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -486,14 +551,22 @@ cudaError_t launch_resident(const RParams& rp, const ResidentPlan& plan, int gri
   {
     std::lock_guard<std::mutex> lk(g_res_mu);
     if (dev >= 0 && dev < kMaxDevices && smem > 48 * 1024 && smem > smem_set[dev]) {
-      e = cudaFuncSetAttribute(resident_integrate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      e = cudaFuncSetAttribute(resident_integrate_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                kResidentSmemBytes);
       if (e != cudaSuccess) return e;
       smem_set[dev] = kResidentSmemBytes;
     }
   }
-  resident_integrate_kernel<<<grid, threads, smem, stream>>>(rp);
+  resident_integrate_kernel<S><<<grid, threads, smem, stream>>>(rp);
   return cudaGetLastError();
+}
+
+cudaError_t launch_resident(const RParams& rp, const ResidentPlan& plan, int spins_per_thread, int grid, int threads,
+                            cudaStream_t stream) {
+  const size_t smem = kResidentFixedBytes + resident_mats_bytes(plan) +
+                      static_cast<size_t>(plan.bytes_per_spin) * threads * spins_per_thread;
+  if (spins_per_thread == 2) return launch_resident_s<2>(rp, smem, grid, threads, stream);
+  return launch_resident_s<1>(rp, smem, grid, threads, stream);
 }
 
 }  // namespace bloch

@@ -2,7 +2,8 @@
 
 Every spin of configs 1 and 3 (697,708 and 732,303 spins; config 2 when its golden is present) was
 evolved by the reference's own compute_block (engine.py:259-310) through its process pool
-(engine.py:540-595).  Here the production launch — the benchmarked integrator instance, e.g.
+(engine.py:540-595).  Here the production launch — the benchmarked integrator instance:
+resident_integrate_kernel (class tables in shared memory), and with it switched off
 integrate_kernel<float, 8, 1, basic, 320> for config 1 — runs the same spins through the C-ABI and
 must meet BASELINE.json's tolerances on the WHOLE k-space (rel L2 <= 1e-4) and on the final
 magnetisation (rel L2 <= 1e-5 on every 64th spin, plus the whole array through its component sums,
@@ -22,7 +23,7 @@ pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 GOLDEN = os.path.join(HERE, "golden")
-# the launch shape the benchmark runs for each config on one B200 (spins per thread)
+# integrate_kernel's launch shape for each config on one B200 (spins per thread)
 PRODUCTION_S = {1: 8, 2: 4, 3: 4}  # configs 2 and 3: two waves of 4 spins per thread (planes exceed L2)
 
 
@@ -33,17 +34,25 @@ def _golden(index):
     return dict(np.load(path))
 
 
+@pytest.mark.parametrize("resident", [True, False])
 @pytest.mark.parametrize("index", [1, 3, 2])
-def test_fullsize_against_reference(index):
+def test_fullsize_against_reference(index, resident):
     g = _golden(index)
     w = configs.make(index)
     b = w.block
     assert b.n == int(g["n_spins"])
     t = precompute_sequence_tables(w.sequence, snapshot_times=(float(g["snapshot_time"]),))
     eng = get_engine(0, 32)
-    e, s = eng.compute(t, b.pos, b.mx, b.my, b.mz, b.t1, b.t2, b.m0, b.domega, b.weight)
-    launch = eng.last_launch()
-    assert launch["precision"] == 32 and launch["spins_per_thread"] == PRODUCTION_S[index], launch
+    eng.set_resident(resident)
+    try:
+        e, s = eng.compute(t, b.pos, b.mx, b.my, b.mz, b.t1, b.t2, b.m0, b.domega, b.weight)
+        launch = eng.last_launch()
+        launch["resident"] = eng.last_resident()["resident"]
+    finally:
+        eng.set_resident(True)
+    assert launch["precision"] == 32 and launch["resident"] == int(resident), launch
+    if not resident and index != 3:  # (config 3's short runs are deferred for the resident integrator)
+        assert launch["spins_per_thread"] == PRODUCTION_S[index], launch
     err_k = rel_l2(g["echoes"], e)
     m = s[0]
     stride = int(g["m_stride"])

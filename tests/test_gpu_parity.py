@@ -320,7 +320,7 @@ def test_gpu_window_sums_without_contraction(name):
 
 # --- the resident-table integrator (resident.h) and the integrator that reads the tables through L2 ---
 
-RESIDENT = ["cfg0", "cfg1", "cfg2", "cfg4"]  # must run resident; the small cases: whatever their plan says
+RESIDENT = ["cfg0", "cfg1", "cfg2", "cfg3", "cfg4", "epi16"]  # must run resident; the small cases: whatever their plan says
 
 
 @pytest.mark.parametrize("name", SMALL + CONFIGS)
@@ -381,8 +381,42 @@ rec = load_golden(name)
 e, s = compute_block(_tables(name, rec), _block(rec), precision=32)
 eng = get_engine(0, 32)
 print(json.dumps({"err": echo_error(rec, e), "snap": max(snapshot_errors(rec, s) or [0.0]),
-                  "groups": eng.program_stats()["window_groups"], "rest": eng.program_stats()["integrator_samples"]}))
+                  "groups": eng.program_stats()["window_groups"], "rest": eng.program_stats()["integrator_samples"],
+                  "resident": eng.last_resident()["resident"], "spins_per_thread": eng.last_launch()["spins_per_thread"]}))
 """
+
+
+def _run_child(name, **env_extra):
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _SHORT_CHILD, root, name], capture_output=True, text=True,
+                       env=dict(os.environ, **env_extra), timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+@pytest.mark.parametrize("name", ["cfg0", "cfg1", "cfg2", "cfg4", "tse16", "tse_2coil"])
+def test_gpu_resident_two_spins_per_thread(name):
+    """The two-spins-per-thread instance of resident_integrate_kernel (full-size blocks pick it; forced here on
+    the golden subsets with BLOCH_RESIDENT_SPINS=2), against the reference goldens."""
+    d = _run_child(name, BLOCH_RESIDENT_SPINS="2")
+    assert d["err"] <= KSPACE_TOL[32] and d["snap"] <= STATE_TOL[32], d
+    if name.startswith("cfg"):
+        assert d["resident"] == 1 and d["spins_per_thread"] == 2, d
+
+
+@pytest.mark.parametrize("name", ["epi16", "mixed", "cfg3"])
+def test_gpu_resident_short_runs(name):
+    """BLOCH_DEFER_SHORT=1 makes the EPI programs fully deferred (OP_UCHIRP, one-sample OP_UWIN): they then
+    run the resident-table integrator."""
+    d = _run_child(name, BLOCH_DEFER_SHORT="1")
+    assert d["err"] <= KSPACE_TOL[32] and d["snap"] <= STATE_TOL[32], d
+    if name == "epi16":
+        assert d["resident"] == 1, d
 
 
 @pytest.mark.parametrize("name", ["epi16", "mixed", "mixed_coils", "cfg3"])
