@@ -27,10 +27,14 @@ with the reference's np.linspace bounds (partition_blocks, engine.py:229-251).
   (fp32 mode) a step is two kernels: the integrator (the spin state through
   the event stream; the long ADC windows only store their entry magnetisation
   U) and the contraction (every window group's samples as one bf16x3 product
-  on tcgen05).  ``roofline`` is the integrator against HBM (algorithmic bytes:
-  staged spins, each plane once, U, final state; ``traffic`` = ncu DRAM bytes
-  of this build, profiles/ncu_counters.json) with its issue-slot fraction;
-  ``roofline_contraction`` is the contraction against the measured bf16
+  on tcgen05).  ``roofline`` is whichever of the two takes the larger share
+  of the step (``roofline.kernel`` names it); both are always present as
+  ``roofline_integrator`` and ``roofline_contraction``.  The integrator is
+  charged against HBM (algorithmic bytes: staged spins, each class table once,
+  U, final state; ``traffic`` = ncu DRAM bytes of this build,
+  profiles/ncu_counters.json) with its issue-slot fraction — with the class
+  tables resident in shared memory (resident_integrate_kernel) it is bound by
+  instruction issue, not by memory; the contraction against the measured bf16
   tensor peak (MEASURED_PEAKS.json): 3 passes x 4 real MAC per complex term.
   Without the contraction (fp64 mode, or windows it does not take) the
   integrator's own tensor-core windows are charged against the measured
@@ -389,7 +393,7 @@ def _ncu_counters(config_index, lib_sha, kernel=""):
 
 
 def roofline(counts, pstats, n_local, C, t_kernel_s, n_sm, f_max_mhz, config_index, lib_sha, precision, hbm_peak,
-             t_integ_s=None, t_contract_s=None, bf16_peak=None):
+             t_integ_s=None, t_contract_s=None, bf16_peak=None, resident=False):
     """Floors of the step's kernels: the integrator against HBM (algorithmic bytes) and its issue slots (ncu
     counters of this build), the window contraction against the measured bf16 tensor peak, the §8d model."""
     f = f_max_mhz * 1e6
@@ -409,7 +413,7 @@ def roofline(counts, pstats, n_local, C, t_kernel_s, n_sm, f_max_mhz, config_ind
     w_mma = n_local * pstats["window_samples"] * C * 8 if (precision == 32 and not contracted) else 0
     t_tensor = w_mma / (n_sm * MMA_MAC_PER_CLK_SM * f)
     out = {
-        "kernel": "integrate_kernel",
+        "kernel": "resident_integrate_kernel" if resident else "integrate_kernel",
         "bound": "hbm",
         "achieved": alg / t_integ / 1e9,
         "peak": hbm_peak,
@@ -609,6 +613,7 @@ def main(argv=None):
     t_integ, t_contract = (x / args.steps for x in run.last_phase_s)
     value = n_total * E * args.steps / t_total_s
     launch_shape = run.eng.last_launch()
+    launch_shape.update(run.eng.last_resident())
     t_kernel = t_kernel_s / args.steps
 
     # ---- end to end through the public host API (pinned host buffers) ------------------
@@ -679,7 +684,9 @@ def main(argv=None):
     d2h = out_e.nbytes + out_s.nbytes
 
     roof, roof_c = roofline(counts, pstats, n_local, C, t_kernel, n_sm, f_max, w.index, lib_sha, args.precision,
-                            hbm_peak, t_integ, t_contract, bf16_peak)
+                            hbm_peak, t_integ, t_contract, bf16_peak, resident=bool(launch_shape.get("resident")))
+    # the dominant kernel of the step carries the headline roofline
+    dominant = roof_c if (roof_c and t_contract > t_integ) else roof
     line = {
         "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_total_s * 1e3 / args.steps, "higher_is_better": True,
@@ -690,7 +697,8 @@ def main(argv=None):
         "config": config_dict(w, world, E, counts, args.scaling, args.full_lattice),
         "spins_per_rank": n_local,
         "program": pstats,
-        "roofline": roof,
+        "roofline": dict(dominant, share_of_step=(max(t_contract, t_integ) / t_kernel) if t_kernel else None),
+        "roofline_integrator": roof,
         "roofline_contraction": roof_c,
         "phases_ms": {"integrate": t_integ * 1e3, "contract": t_contract * 1e3},
         "integrator_launch": launch_shape,
@@ -718,13 +726,14 @@ def main(argv=None):
             tt, tk, _ = run.timed(pc, st, 2)
             ti, tc = (x / st for x in run.last_phase_s)
             rc, rcc = roofline(cc, ps, pc["n"], pc["C"], tk / st, n_sm, f_max, c, lib_sha, args.precision, hbm_peak,
-                               ti, tc, bf16_peak)
+                               ti, tc, bf16_peak, resident=bool(run.eng.last_resident()["resident"]))
             per[f"config{c}"] = {"workload": wc.name, "spins_total": nt, "events_per_spin": cc["events"],
                                  "value": nt * cc["events"] * st / tt, "ms_per_step": tt * 1e3 / st,
                                  "kernel_ms": tk * 1e3 / st, "integrate_ms": ti * 1e3, "contract_ms": tc * 1e3,
                                  "frac": rc["frac"], "issue_frac": rc["issue_frac"],
                                  "contraction_frac": rcc["frac"] if rcc else None, "model_frac": rc["model_frac"],
-                                 "spins_per_thread": run.eng.last_launch()["spins_per_thread"]}
+                                 "spins_per_thread": run.eng.last_launch()["spins_per_thread"],
+                                 "resident": run.eng.last_resident()["resident"]}
             del pc
         line["per_config"] = per
 
@@ -741,7 +750,8 @@ def main(argv=None):
             tt, tk, _ = run.timed(pc, st, 2)
             proj[str(nr)] = {"shard_spins": sh.n, "ms_per_step": tt * 1e3 / st, "kernel_ms": tk * 1e3 / st,
                              "efficiency_est": t1 / (nr * tt / st), "spins_per_thread":
-                             run.eng.last_launch()["spins_per_thread"]}
+                             run.eng.last_launch()["spins_per_thread"],
+                             "integrate_ms": run.last_phase_s[0] * 1e3 / st, "contract_ms": run.last_phase_s[1] * 1e3 / st}
             del pc
         line["strong_scaling_projection"] = {
             "note": "one B200: device time of rank 0's np.linspace shard (the largest) per step vs this line's "

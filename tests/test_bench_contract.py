@@ -67,7 +67,10 @@ def test_gpu_arm_contract():
     assert d["value"] > 0 and d["gpu_launches"] >= 3 * 3
     r = d["roofline"]
     assert r["peak"] > 0 and r["achieved"] > 0 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
-    assert r["bound"] == "hbm" and r["algorithmic_bytes"] > 0 and r["model_frac"] > 0
+    assert r["bound"] in ("hbm", "tensor") and 0 < r["share_of_step"] <= 1  # the step's dominant kernel
+    ri = d["roofline_integrator"]
+    assert ri["bound"] == "hbm" and ri["algorithmic_bytes"] > 0 and ri["model_frac"] > 0
+    assert ri["kernel"] == "resident_integrate_kernel" and d["integrator_launch"]["resident"] == 1
     rc = d["roofline_contraction"]  # config 0's readouts go through the tensor-core contraction
     assert rc["bound"] == "tensor" and rc["achieved"] > 0 and abs(rc["frac"] - rc["achieved"] / rc["peak"]) < 1e-9
     assert d["phases_ms"]["contract"] > 0 and d["phases_ms"]["integrate"] > 0
