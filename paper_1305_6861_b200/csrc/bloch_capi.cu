@@ -473,6 +473,9 @@ int bloch_set_tables(bloch_ctx* c, int32_t n_es, const int64_t* es_ev_offset,
       upload(c->d_urow_out0, prog.urow_out0.data(), prog.urow_out0.size() * sizeof(int64_t), c->stream);
     }
     bloch::resident_compile(prog, c->rplan);
+    if (getenv("BLOCH_RESIDENT_DEBUG"))
+      for (const bloch::WinGroup& g : prog.groups)
+        fprintf(stderr, "group: chirp %d samples %d windows %d row0 %d\n", g.chirp, g.count, g.n_windows, g.row0);
     if (c->device != BLOCH_HOST_ONLY) {
       if (c->rplan.ok) {
         upload(c->d_rops, c->rplan.rops.data(), c->rplan.rops.size() * sizeof(bloch::ROp), c->stream);

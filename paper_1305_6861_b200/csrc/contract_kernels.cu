@@ -247,7 +247,10 @@ __global__ void __launch_bounds__(ct::kThreads(GW), 1)
     auto drain = [&](int e) {
       ct::mbar_wait(acc_full, e & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      float* slot = j.part + ((static_cast<int64_t>(kc) * p.segs + e) * j.C + coil) * j.W * j.K * 2;
+      // one slot per (chunk, coil): the first segment stores, the later ones add in fp32 with a reduction
+      // (RED.ADD.F32 at L2; the same thread owns an element in every segment, so the order is fixed; the slots
+      // of a call fit L2, so they never reach DRAM — one slot per segment wrote and re-read 0.75 GB on config 2)
+      float* slot = j.part + (static_cast<int64_t>(kc) * j.C + coil) * j.W * j.K * 2;
       for (int mm = 0; mm < MT; ++mm) {
         const int k = k0 + 64 * mm + (row & 63);
         for (int c0 = 16 * colh; c0 < ncol; c0 += 16 * (GW / 4)) {
@@ -263,7 +266,11 @@ __global__ void __launch_bounds__(ct::kThreads(GW), 1)
 #pragma unroll
             for (int c = 0; c < 16; ++c) {
               const int w = w0 + c0 + c;
-              if (w < j.W) slot[(static_cast<int64_t>(w) * j.K + k) * 2 + (row >> 6)] = __uint_as_float(r[c]);
+              if (w < j.W) {
+                float* q = slot + (static_cast<int64_t>(w) * j.K + k) * 2 + (row >> 6);
+                if (e == 0) *q = __uint_as_float(r[c]);
+                else atomicAdd(q, __uint_as_float(r[c]));  // RED: no load on the drain's path; one thread per element
+              }
             }
           }
         }
@@ -385,8 +392,7 @@ __global__ void contract_prep_kernel(const SpinConst* __restrict__ sc, int64_t n
   }
 }
 
-// fixed-order fp64 fold of the partial slots (spin chunk major, segment minor) into the echo array
-// (stored, not added); chunk c holds ceil(stages_c / seg) segments
+// fixed-order fp64 fold of the chunks' partial slots into the echo array (stored, not added)
 __global__ void contract_fold_kernel(const float* __restrict__ part, int chunks, int segs, int seg, int stages,
                                      int64_t total_st, int C, int W, int K, int64_t G, const int64_t* __restrict__ out0,
                                      double* __restrict__ echo) {
@@ -396,11 +402,8 @@ __global__ void contract_fold_kernel(const float* __restrict__ part, int chunks,
     const int64_t cw = t / (2 * K), r = t - cw * 2 * K;
     const int64_t c = cw / W, w = cw - c * W;
     double acc = 0.0;
-    for (int c = 0; c < chunks; ++c) {
-      const int64_t nst = min(static_cast<int64_t>(stages), total_st - static_cast<int64_t>(c) * stages);
-      const int ns = static_cast<int>((nst + seg - 1) / seg);
-      for (int e = 0; e < ns; ++e) acc += static_cast<double>(part[(static_cast<int64_t>(c) * segs + e) * per + t]);
-    }
+    for (int c = 0; c < chunks; ++c)
+      if (total_st - static_cast<int64_t>(c) * stages > 0) acc += static_cast<double>(part[static_cast<int64_t>(c) * per + t]);
     echo[(c * G + out0[w] + (r >> 1)) * 2 + (r & 1)] = acc;
   }
 }
@@ -465,7 +468,7 @@ ContractPlan contract_plan(int K, int W, int64_t n, int n_sm, int C) {
 }
 
 size_t contract_part_bytes(const ContractPlan& p, const ContractJob& j) {
-  return static_cast<size_t>(p.chunks) * p.segs * j.C * j.W * j.K * 2 * sizeof(float);
+  return static_cast<size_t>(p.chunks) * j.C * j.W * j.K * 2 * sizeof(float);
 }
 
 namespace {
