@@ -45,7 +45,7 @@ struct ContractJob {
   const uint32_t* uhi;  // U, spin-block major (contract_u_index): bf16x2 (Re, Im) words, hi part
   const uint32_t* ulo;  // lo part
   int64_t rows;         // rows (windows of every group) of the U arrays
-  float* part;          // [chunks][C][W][K][2] partial sums per spin chunk (its accumulation segments added in fp32)
+  float* part;          // [chunks][C][K][2][Wr] partial sums per spin chunk (its accumulation segments added in fp32)
   const int64_t* out0;  // [W] complex index (coil 0) of each window's first sample in the echo array
   double* echo;         // echo array (complex128) [C][G], samples stored
   int32_t C;            // receive coils: coil c's samples are sum_s w_cs U[w][s] z_s^k (w folded into A)

@@ -250,7 +250,11 @@ __global__ void __launch_bounds__(ct::kThreads(GW), 1)
       // one slot per (chunk, coil): the first segment stores, the later ones add in fp32 with a reduction
       // (RED.ADD.F32 at L2; the same thread owns an element in every segment, so the order is fixed; the slots
       // of a call fit L2, so they never reach DRAM — one slot per segment wrote and re-read 0.75 GB on config 2)
-      float* slot = j.part + (static_cast<int64_t>(kc) * j.C + coil) * j.W * j.K * 2;
+      // Slot layout [K][2][Wr] (Wr = W rounded up to 16): a thread's 16 accumulator columns are 16 consecutive
+      // windows of one (sample, component) row, i.e. 64 contiguous bytes: four 16-byte stores / reductions
+      // instead of 16 scattered 4-byte ones.
+      const int Wr = (j.W + 15) & ~15;
+      float* slot = j.part + (static_cast<int64_t>(kc) * j.C + coil) * j.K * 2 * Wr;
       for (int mm = 0; mm < MT; ++mm) {
         const int k = k0 + 64 * mm + (row & 63);
         for (int c0 = 16 * colh; c0 < ncol; c0 += 16 * (GW / 4)) {
@@ -263,13 +267,25 @@ __global__ void __launch_bounds__(ct::kThreads(GW), 1)
               : "r"(addr));
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
           if (k < j.K) {
+            float* q = slot + (static_cast<int64_t>(k) * 2 + (row >> 6)) * Wr + (w0 + c0);
+            if (((w0 + c0) & 3) == 0 && w0 + c0 + 16 <= Wr) {
 #pragma unroll
-            for (int c = 0; c < 16; ++c) {
-              const int w = w0 + c0 + c;
-              if (w < j.W) {
-                float* q = slot + (static_cast<int64_t>(w) * j.K + k) * 2 + (row >> 6);
-                if (e == 0) *q = __uint_as_float(r[c]);
-                else atomicAdd(q, __uint_as_float(r[c]));  // RED: no load on the drain's path; one thread per element
+              for (int c = 0; c < 16; c += 4) {
+                if (e == 0)
+                  *reinterpret_cast<uint4*>(q + c) = make_uint4(r[c], r[c + 1], r[c + 2], r[c + 3]);
+                else  // RED: no load on the drain's path; one thread per element
+                  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(q + c), "f"(__uint_as_float(r[c])),
+                               "f"(__uint_as_float(r[c + 1])), "f"(__uint_as_float(r[c + 2])),
+                               "f"(__uint_as_float(r[c + 3]))
+                               : "memory");
+              }
+            } else {
+#pragma unroll
+              for (int c = 0; c < 16; ++c) {
+                if (w0 + c0 + c < Wr) {
+                  if (e == 0) q[c] = __uint_as_float(r[c]);
+                  else atomicAdd(q + c, __uint_as_float(r[c]));
+                }
               }
             }
           }
@@ -396,15 +412,17 @@ __global__ void contract_prep_kernel(const SpinConst* __restrict__ sc, int64_t n
 __global__ void contract_fold_kernel(const float* __restrict__ part, int chunks, int segs, int seg, int stages,
                                      int64_t total_st, int C, int W, int K, int64_t G, const int64_t* __restrict__ out0,
                                      double* __restrict__ echo) {
-  const int64_t per = static_cast<int64_t>(C) * W * K * 2;
+  const int Wr = (W + 15) & ~15;
+  const int64_t per = static_cast<int64_t>(C) * K * 2 * Wr;  // slot layout [C][K][2][Wr]
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < per;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t cw = t / (2 * K), r = t - cw * 2 * K;
-    const int64_t c = cw / W, w = cw - c * W;
+    const int64_t w = t % Wr, kr = t / Wr;  // kr = (c K + k) 2 + component
+    if (w >= W) continue;
+    const int64_t comp = kr & 1, ck = kr >> 1, c = ck / K, k = ck - c * K;
     double acc = 0.0;
-    for (int c = 0; c < chunks; ++c)
-      if (total_st - static_cast<int64_t>(c) * stages > 0) acc += static_cast<double>(part[static_cast<int64_t>(c) * per + t]);
-    echo[(c * G + out0[w] + (r >> 1)) * 2 + (r & 1)] = acc;
+    for (int ch = 0; ch < chunks; ++ch)
+      if (total_st - static_cast<int64_t>(ch) * stages > 0) acc += static_cast<double>(part[static_cast<int64_t>(ch) * per + t]);
+    echo[(c * G + out0[w] + k) * 2 + comp] = acc;
   }
 }
 
@@ -468,7 +486,7 @@ ContractPlan contract_plan(int K, int W, int64_t n, int n_sm, int C) {
 }
 
 size_t contract_part_bytes(const ContractPlan& p, const ContractJob& j) {
-  return static_cast<size_t>(p.chunks) * j.C * j.W * j.K * 2 * sizeof(float);
+  return static_cast<size_t>(p.chunks) * j.C * ((j.W + 15) & ~15) * j.K * 2 * sizeof(float);
 }
 
 namespace {
@@ -556,7 +574,7 @@ cudaError_t launch_contract(const ContractJob& j, const ContractPlan& p, cudaStr
     default: e = gw_env == 4 ? launch_mt<1, 4>(mh, ml, j, p, st) : launch_mt<1, 8>(mh, ml, j, p, st); break;
   }
   if (e != cudaSuccess) return e;
-  const int64_t per = static_cast<int64_t>(j.C) * j.W * j.K * 2;
+  const int64_t per = static_cast<int64_t>(j.C) * ((j.W + 15) & ~15) * j.K * 2;
   const int64_t blocks = (per + 255) / 256;
   const int64_t total_st = (j.n + ct::kStageSpins - 1) / ct::kStageSpins;
   contract_fold_kernel<<<static_cast<int>(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(
