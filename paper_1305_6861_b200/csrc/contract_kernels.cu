@@ -342,10 +342,17 @@ __global__ void __launch_bounds__(ct::kThreads(GW), 1)
       unsigned char* ab = A(s, 0) + off0;
 #pragma unroll
       for (int v = 0; v < kVals; ++v) {
+        unsigned char* o = ab + 128 * v + chk[v & 3];
         if constexpr (CH) {  // chirp: each sample's factor directly (short runs, no recurrence)
-          const float k = kf + 2.f * v;
+          // Rows interleaved over the warps (value v of warp q: row 2 q + half + 2 GW v), so the K <= 64 samples of
+          // a short run are shared by all generator warps, and rows beyond the run are skipped: their
+          // accumulator rows are never read (a 10-sample ramp costs 1 value per lane in 5 warps, not 4 in 2)
+          const int kr = 2 * q + half + 2 * GW * v;
+          if (k0 + kr >= j.K) continue;
+          const float k = static_cast<float>(k0 + kr);
           const float2 z0 = live ? ct::zchirp32(czt, czq.x, k + 1.f, 0.5f * k * (k + 1.f)) : make_float2(0.f, 0.f);
           P = make_float2(cwc.x * z0.x - cwc.y * z0.y, cwc.x * z0.y + cwc.y * z0.x);
+          o = A(s, 0) + 64 * kr + ((sl & 3) << 2) + (((sl >> 2) ^ ((kr >> 1) & 3)) << 4);
         }
         // bf16 hi parts rounded to nearest (Veltkamp, both components packed) and the residuals
         // (scalar __fmul_rn: never contracted into the following subtraction, which would void the split)
@@ -353,7 +360,6 @@ __global__ void __launch_bounds__(ct::kThreads(GW), 1)
         const float2 d = __fadd2_rn(c, make_float2(-P.x, -P.y));
         const float2 hi = __fadd2_rn(c, make_float2(-d.x, -d.y));
         const float2 lo = __fadd2_rn(P, make_float2(-hi.x, -hi.y));
-        unsigned char* o = ab + 128 * v + chk[v & 3];
         *reinterpret_cast<uint32_t*>(o) = ct::pack2(hi.x, -hi.y);                   // real row
         *reinterpret_cast<uint32_t*>(o + 4096) = ct::pack2(hi.y, hi.x);             // imaginary row
         *reinterpret_cast<uint32_t*>(o + a_bytes) = ct::pack2(lo.x, -lo.y);
