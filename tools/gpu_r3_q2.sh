@@ -1,0 +1,22 @@
+# final evidence of round 2 (resident integrator + in-L2 contraction slots): full GPU suite, ncu counters per config, launch list, bench line,
+# ncu --set full of the resident integrator (config 2), reference arm
+timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/r3q_pytest.txt 2>&1; echo "rc=$?" >> gpurun_out/r3q_pytest.txt
+SHA=$(python -c "import hashlib;print(hashlib.sha256(open('paper_1305_6861_b200/libbloch_b200.so','rb').read()).hexdigest()[:16])")
+M=smsp__inst_executed.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,sm__cycles_elapsed.avg.per_second,sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_issued.avg.pct_of_peak_sustained_active
+for c in 0 1 2 3 4; do
+  CMD="python bench.py --config $c --steps 1 --warmup 1 --no-cpu-baseline --no-per-config --no-projection --e2e-steps 1 --quiet"
+  BLOCH_NO_GRAPH=1 timeout 300 $CMD > gpurun_out/r3q_plain_cfg$c.json 2>&1 && \
+  BLOCH_NO_GRAPH=1 timeout 600 ncu --metrics $M --clock-control none -k regex:integrate -s 1 -c 1 --csv --log-file gpurun_out/r3q_cfg$c.csv $CMD > /dev/null 2>&1
+  BLOCH_NO_GRAPH=1 timeout 600 ncu --metrics $M --clock-control none -k regex:contract_kernel -s 1 -c 1 --csv --log-file gpurun_out/r3q_contract_cfg$c.csv $CMD > /dev/null 2>&1
+done
+rm -f gpurun_out/ncu_counters.json
+python tools/ncu_counters.py gpurun_out/ncu_counters.json $SHA gpurun_out/r3q_cfg*.csv gpurun_out/r3q_contract_cfg*.csv > gpurun_out/r3q_counters.log 2>&1
+cp gpurun_out/ncu_counters.json profiles/ncu_counters.json
+CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-per-config --no-projection --e2e-steps 1 --quiet"
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r3q_launches_cfg2.csv $CMD > /dev/null 2>&1
+timeout 900 python bench.py > gpurun_out/r3q_bench.json 2> gpurun_out/r3q_bench.err; echo "rc=$?" >> gpurun_out/r3q_bench.err
+BLOCH_NO_GRAPH=1 timeout 600 ncu --set full --import-source on --clock-control none -k regex:resident -c 1 -o gpurun_out/r3q_res_cfg2 python tools/one_call.py 2 > gpurun_out/r3q_ncu2.log 2>&1
+BLOCH_NO_GRAPH=1 timeout 600 ncu --set full --import-source on --clock-control none -k regex:contract_kernel -c 1 -o gpurun_out/r3q_con_cfg2 python tools/one_call.py 2 > gpurun_out/r3q_ncu3.log 2>&1
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/r3q_reference.json 2> gpurun_out/r3q_reference.err
+for c in 1 2 3 4; do timeout 300 python tools/shard_probe.py $c 1 2 4 8; done > gpurun_out/r3q_shards.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r3q_smoke.txt 2>&1
