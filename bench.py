@@ -366,14 +366,18 @@ def _peaks():
 
 
 def _lib_sha():
+    """Identity of the kernel build the counters in profiles/ncu_counters.json must match: the hash of the
+    kernel sources (nvcc output is not bit-reproducible), or of the file for an explicit BLOCH_LIB."""
     import hashlib
 
-    from paper_1305_6861_b200 import _capi
-
-    path = os.environ.get("BLOCH_LIB") or _capi.LIB_PATH
+    path = os.environ.get("BLOCH_LIB")
     try:
-        with open(path, "rb") as fh:
-            return hashlib.sha256(fh.read()).hexdigest()[:16]
+        if path:
+            with open(path, "rb") as fh:
+                return hashlib.sha256(fh.read()).hexdigest()[:16]
+        from paper_1305_6861_b200.build import source_hash
+
+        return source_hash()
     except OSError:
         return None
 

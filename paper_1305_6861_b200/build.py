@@ -30,6 +30,22 @@ def nvcc_path() -> str:
     raise RuntimeError("nvcc not found; the Bloch engine must be built with CUDA 12.9 nvcc")
 
 
+def source_hash() -> str:
+    """16 hex digits identifying the kernel sources (csrc/ + the C-ABI header).  nvcc's output is not
+    bit-reproducible from one build to the next, so measurements that must be matched to a build (the ncu
+    counters bench.py reads, profiles/ncu_counters.json) are keyed on this, not on the .so file."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for name in sorted(SOURCES + HEADERS):
+        h.update(name.encode())
+        with open(os.path.join(CSRC, name), "rb") as fh:
+            h.update(fh.read())
+    with open(os.path.join(ROOT, "include", "bloch_b200.h"), "rb") as fh:
+        h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 def _stale(target: str, deps) -> bool:
     if not os.path.exists(target):
         return True

@@ -1,7 +1,7 @@
 # evidence of the resident build: full GPU suite, ncu counters (integrator + contraction) per config, launch list, bench line,
 # ncu --set full of the resident integrator (config 2), reference arm
 timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/r3g_pytest.txt 2>&1; echo "rc=$?" >> gpurun_out/r3g_pytest.txt
-SHA=$(python -c "import hashlib;print(hashlib.sha256(open('paper_1305_6861_b200/libbloch_b200.so','rb').read()).hexdigest()[:16])")
+SHA=$(python -c "from paper_1305_6861_b200.build import source_hash; print(source_hash())")
 M=smsp__inst_executed.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,sm__cycles_elapsed.avg.per_second,sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_issued.avg.pct_of_peak_sustained_active
 for c in 0 1 2 3 4; do
   CMD="python bench.py --config $c --steps 1 --warmup 1 --no-cpu-baseline --no-per-config --no-projection --e2e-steps 1 --quiet"
