@@ -235,8 +235,12 @@ int bloch_synchronize(bloch_ctx* ctx);
 int bloch_set_kernel_gate(bloch_ctx* ctx, void* wait_event, void* signal_event);
 
 /* Device time (ms, CUDA events on the context stream) of the last
- * bloch_compute_block: the integrator kernel alone, and all device work of the
- * call (staging kernels + integrator + reduction). */
+ * bloch_compute_block: kernel_ms = from the first integrator launch to the end of the
+ * last main kernel (the integrator; with the window contraction, through the last
+ * contraction fold; with a segmented program it also spans the folds and state
+ * hand-overs between the segments' launches), and device_ms = all device work of the
+ * call (staging kernels + integrator + contraction + reduction).  bloch_last_phases
+ * splits kernel_ms into the integrator and the contraction. */
 int bloch_last_timing(const bloch_ctx* ctx, float* kernel_ms, float* device_ms,
                       int32_t* kernel_launches);
 
