@@ -906,7 +906,13 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       threads = std::max<int64_t>(32, std::min<int64_t>(max_t, threads));
       if (res_threads > 0) threads = res_threads;
       const int64_t spc = threads * v.S;
-      const int64_t grid = (n + spc - 1) / spc;
+      int64_t grid = (n + spc - 1) / spc;
+      int res_big = 0;
+      if (res_threads > 0) {  // whole warps dealt evenly over full waves of CTAs
+        int g = 0;
+        bloch::resident_grid(n, c->n_sm, res_threads, v.S, &g, &res_big);
+        grid = g;
+      }
       c->last_launch[0] = v.prec;
       c->last_launch[1] = v.S;
       c->last_launch[2] = v.NC;
@@ -1032,6 +1038,7 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
           rp.uhi = kp.uhi;
           rp.ulo = kp.ulo;
           rp.urows = kp.urows;
+          rp.n_big = res_big;
           ck(bloch::launch_resident(rp, c->rplan, v.S, static_cast<int>(grid), static_cast<int>(threads), st),
              "resident integrate kernel");
         } else {

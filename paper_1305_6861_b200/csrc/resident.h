@@ -95,7 +95,13 @@ struct RParams {
   double* snaps;
   uint32_t *uhi, *ulo;
   int64_t urows;
+  int32_t n_big;                 // CTAs [0, n_big) run blockDim threads, the rest blockDim - 32 (one warp exits)
 };
+
+// the launch of n spins at `threads` (a multiple of 32, from resident_threads) threads per CTA: the grid, and
+// how many of its CTAs keep every warp.  The spins are dealt in whole warps over n_sm x waves CTAs, so CTA
+// sizes differ by at most one warp and the last wave is as full as the others.
+void resident_grid(int64_t n, int n_sm, int threads, int spins_per_thread, int* grid, int* n_big);
 
 // threads per CTA and spins per thread (1 or 2) for n spins on n_sm SMs (0: the tables of
 // kResidentMinThreads spins do not fit)

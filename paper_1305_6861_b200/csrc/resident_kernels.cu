@@ -221,6 +221,31 @@ int resident_threads(const ResidentPlan& plan, int64_t n, int n_sm, int* spins_p
   return static_cast<int>(spins / S);
 }
 
+void resident_grid(int64_t n, int n_sm, int threads, int spins_per_thread, int* grid, int* n_big) {
+  // Measured (profiles/r4b_even_waves_ab.txt): integrator -1.9% on config 2, -0.4% on config 1 (two spins per
+  // thread); with one spin per thread a CTA's time hardly depends on its warp count (config 4 -1.6%, config 3
+  // +1.1%), so those launches keep equal CTAs.  BLOCH_RESIDENT_UNEVEN=1 / =0 forces equal / dealt CTAs.
+  static const int mode = [] {
+    const char* e = getenv("BLOCH_RESIDENT_UNEVEN");
+    return e ? (atoi(e) ? 1 : 0) : -1;
+  }();
+  const bool uneven = mode >= 0 ? mode == 1 : spins_per_thread != 2;
+  const int64_t spw = 32 * spins_per_thread;                  // spins per warp
+  const int64_t warps = (n + spw - 1) / spw, tw = threads / 32;
+  const int64_t uniform = (warps + tw - 1) / tw;              // CTAs of `threads` threads each
+  const int64_t waves = (uniform + n_sm - 1) / n_sm;
+  const int64_t ctas = waves * n_sm;
+  // ctas CTAs of tw - 1 warps, `extra` of them with one more
+  const int64_t extra = warps - ctas * (tw - 1);
+  if (uneven || tw < 2 || extra < 1 || extra > ctas) {
+    *grid = static_cast<int>(uniform);
+    *n_big = static_cast<int>(uniform);
+    return;
+  }
+  *grid = static_cast<int>(ctas);
+  *n_big = static_cast<int>(extra);
+}
+
 // ---------------------------------------------------------------------------
 // device
 // ---------------------------------------------------------------------------
@@ -309,8 +334,15 @@ __device__ __noinline__ double3 fly_interval(const ROp* rop, const DevOp* ops, c
 template <int S>
 __global__ void __launch_bounds__(kResidentMaxThreads / S, 1) resident_integrate_kernel(const RParams rp) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int tid = threadIdx.x, bd = blockDim.x;
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * (S * bd) + tid;  // spin of slot 0; slot s: + s bd
+  // CTAs from n_big on run one warp fewer (resident_grid): that warp leaves before the first barrier
+  const int tid = threadIdx.x, cta = blockIdx.x;
+  const int bd = cta < rp.n_big ? static_cast<int>(blockDim.x) : static_cast<int>(blockDim.x) - 32;
+  if (tid >= bd) return;
+  const int64_t cta0 = cta < rp.n_big
+                           ? static_cast<int64_t>(cta) * (S * static_cast<int>(blockDim.x))
+                           : static_cast<int64_t>(rp.n_big) * (S * static_cast<int>(blockDim.x)) +
+                                 static_cast<int64_t>(cta - rp.n_big) * (S * bd);
+  const int64_t base = cta0 + tid;  // spin of slot 0; slot s: + s bd
   const uint32_t s_base = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
   const uint32_t s_rec = s_base;                                    // [2][kRecChunk] staged records
   const uint32_t s_m4 = s_rec + 2 * kRecChunk * 32;                 // axis pulses, 32 B each

@@ -1,0 +1,21 @@
+# final evidence of round 2 on the build with evenly dealt warps (resident integrator, two-spin launches): same command list as gpu_r4_a.sh
+timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/r4c_pytest.txt 2>&1; echo "rc=$?" >> gpurun_out/r4c_pytest.txt
+SHA=$(python -c "from paper_1305_6861_b200.build import source_hash; print(source_hash())")
+M=smsp__inst_executed.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,sm__cycles_elapsed.avg.per_second,sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_issued.avg.pct_of_peak_sustained_active
+for c in 0 1 2 3 4; do
+  CMD="python bench.py --config $c --steps 1 --warmup 1 --no-cpu-baseline --no-per-config --no-projection --e2e-steps 1 --quiet"
+  BLOCH_NO_GRAPH=1 timeout 300 $CMD > gpurun_out/r4c_plain_cfg$c.json 2>&1 && \
+  BLOCH_NO_GRAPH=1 timeout 600 ncu --metrics $M --clock-control none -k regex:integrate -s 1 -c 1 --csv --log-file gpurun_out/r4c_cfg$c.csv $CMD > /dev/null 2>&1
+  BLOCH_NO_GRAPH=1 timeout 600 ncu --metrics $M --clock-control none -k regex:contract_kernel -s 1 -c 1 --csv --log-file gpurun_out/r4c_contract_cfg$c.csv $CMD > /dev/null 2>&1
+done
+rm -f gpurun_out/ncu_counters.json
+python tools/ncu_counters.py gpurun_out/ncu_counters.json $SHA gpurun_out/r4c_cfg*.csv gpurun_out/r4c_contract_cfg*.csv > gpurun_out/r4c_counters.log 2>&1
+cp gpurun_out/ncu_counters.json profiles/ncu_counters.json
+CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-per-config --no-projection --e2e-steps 1 --quiet"
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r4c_launches_cfg2.csv $CMD > /dev/null 2>&1
+timeout 900 python bench.py > gpurun_out/r4c_bench.json 2> gpurun_out/r4c_bench.err; echo "rc=$?" >> gpurun_out/r4c_bench.err
+BLOCH_NO_GRAPH=1 timeout 600 ncu --set full --import-source on --clock-control none -k regex:resident -c 1 -o gpurun_out/r4c_res_cfg2 python tools/one_call.py 2 > gpurun_out/r4c_ncu2.log 2>&1
+BLOCH_NO_GRAPH=1 timeout 600 ncu --set full --import-source on --clock-control none -k regex:contract_kernel -c 1 -o gpurun_out/r4c_con_cfg2 python tools/one_call.py 2 > gpurun_out/r4c_ncu3.log 2>&1
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/r4c_reference.json 2> gpurun_out/r4c_reference.err
+for c in 1 2 3 4; do timeout 300 python tools/shard_probe.py $c 1 2 4 8; done > gpurun_out/r4c_shards.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r4c_smoke.txt 2>&1
