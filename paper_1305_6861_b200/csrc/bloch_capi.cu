@@ -907,11 +907,11 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
       if (res_threads > 0) threads = res_threads;
       const int64_t spc = threads * v.S;
       int64_t grid = (n + spc - 1) / spc;
-      int res_big = 0;
-      if (res_threads > 0) {  // whole warps dealt evenly over full waves of CTAs
-        int g = 0;
-        bloch::resident_grid(n, c->n_sm, res_threads, v.S, &g, &res_big);
-        grid = g;
+      bloch::ResidentShape rshape{};
+      if (res_threads > 0) {  // two-spin launches: spins dealt evenly over full waves of CTAs
+        bloch::resident_grid(n, c->n_sm, res_threads, v.S, &rshape);
+        grid = rshape.grid;
+        threads = rshape.block;
       }
       c->last_launch[0] = v.prec;
       c->last_launch[1] = v.S;
@@ -1038,7 +1038,9 @@ int bloch_compute_block(bloch_ctx* c, int64_t n, const double* pos, const double
           rp.uhi = kp.uhi;
           rp.ulo = kp.ulo;
           rp.urows = kp.urows;
-          rp.n_big = res_big;
+          rp.n_big = rshape.n_big;
+          rp.bd_big = rshape.bd_big;
+          rp.bd_small = rshape.bd_small;
           ck(bloch::launch_resident(rp, c->rplan, v.S, static_cast<int>(grid), static_cast<int>(threads), st),
              "resident integrate kernel");
         } else {

@@ -95,13 +95,15 @@ struct RParams {
   double* snaps;
   uint32_t *uhi, *ulo;
   int64_t urows;
-  int32_t n_big;                 // CTAs [0, n_big) run blockDim threads, the rest blockDim - 32 (one warp exits)
+  int32_t n_big, bd_big, bd_small;  // CTAs [0, n_big) run bd_big threads, the rest bd_small (ResidentShape)
 };
 
-// the launch of n spins at `threads` (a multiple of 32, from resident_threads) threads per CTA: the grid, and
-// how many of its CTAs keep every warp.  The spins are dealt in whole warps over n_sm x waves CTAs, so CTA
-// sizes differ by at most one warp and the last wave is as full as the others.
-void resident_grid(int64_t n, int n_sm, int threads, int spins_per_thread, int* grid, int* n_big);
+// the launch of n spins: `grid` CTAs of `block` threads, of which the first n_big use bd_big threads and the rest
+// bd_small (a CTA's spins: spins_per_thread x its threads, consecutive)
+struct ResidentShape {
+  int grid, block, n_big, bd_big, bd_small;
+};
+void resident_grid(int64_t n, int n_sm, int threads, int spins_per_thread, ResidentShape* out);
 
 // threads per CTA and spins per thread (1 or 2) for n spins on n_sm SMs (0: the tables of
 // kResidentMinThreads spins do not fit)

@@ -196,20 +196,50 @@ constexpr int kResidentFixedBytes = 2 * 64 * 32;  // the two staged record chunk
 // entries padded so that every matrix starts on a 16-byte boundary)
 static size_t resident_mats_bytes(const ResidentPlan& plan) { return plan.mats4.size() * 8 + plan.mats.size() / 9 * 80; }
 
+// BLOCH_RESIDENT_UNEVEN=1: equal CTAs of whole warps with a ragged last wave (the earlier launch, kept as the
+// A/B reference); =0 / unset: two-spin launches deal the spins in units over full waves (resident_grid)
+static int resident_uneven_mode() {
+  static const int mode = [] {
+    const char* e = getenv("BLOCH_RESIDENT_UNEVEN");
+    return e ? (atoi(e) ? 1 : 0) : -1;
+  }();
+  return mode;
+}
+
+constexpr int kDealThreads = 4;  // dealing unit of a two-spin launch: 4 threads = 8 spins (one 32-byte U sector)
+
 int resident_threads(const ResidentPlan& plan, int64_t n, int n_sm, int* spins_per_thread) {
   if (!plan.ok || n <= 0) return 0;
-  const int64_t room = kResidentSmemBytes - 1024 - kResidentFixedBytes - static_cast<int64_t>(resident_mats_bytes(plan));
-  int64_t cap = plan.bytes_per_spin > 0 ? room / plan.bytes_per_spin : kResidentMaxThreads;  // spins per CTA
+  const int64_t room = kResidentSmemBytes - kResidentFixedBytes - static_cast<int64_t>(resident_mats_bytes(plan));
+  const int64_t fit = plan.bytes_per_spin > 0 ? room / plan.bytes_per_spin : kResidentMaxThreads;  // spins per CTA
+  static const int force_s = [] {  // experiment hook: BLOCH_RESIDENT_SPINS=1|2
+    const char* e = getenv("BLOCH_RESIDENT_SPINS");
+    return e ? atoi(e) : 0;
+  }();
+  // two spins per thread, CTA sizes in units of 8 spins: the tables decide how many spins a CTA holds, not the
+  // warp rounding (config 2: 1016 of the 1019 that fit, so 5 waves instead of 6 at 896)
+  if (resident_uneven_mode() != 1 && force_s != 1) {
+    const int64_t u = 2 * kDealThreads;
+    const int64_t cap = std::min<int64_t>(kResidentMaxThreads, (fit / u) * u);
+    if (cap >= kResidentTwoSpinMin) {
+      const int64_t per_wave = static_cast<int64_t>(n_sm) * cap;
+      const int64_t waves = (n + per_wave - 1) / per_wave;
+      int64_t spins = (n + n_sm * waves - 1) / (n_sm * waves);  // per CTA
+      if (spins >= kResidentTwoSpinMin || force_s == 2) {
+        spins = std::max<int64_t>(u, std::min<int64_t>(cap, ((spins + u - 1) / u) * u));
+        if (spins_per_thread) *spins_per_thread = 2;
+        return static_cast<int>(spins / 2);
+      }
+    }
+  }
+  // whole warps, with 1 KB of the budget left free (as measured so far)
+  int64_t cap = plan.bytes_per_spin > 0 ? (room - 1024) / plan.bytes_per_spin : kResidentMaxThreads;
   cap = std::min<int64_t>(kResidentMaxThreads, (cap / 64) * 64);
   if (cap < kResidentMinThreads) return 0;
   // equal waves of one CTA per SM
   const int64_t per_wave = static_cast<int64_t>(n_sm) * cap;
   const int64_t waves = (n + per_wave - 1) / per_wave;
   int64_t spins = (n + n_sm * waves - 1) / (n_sm * waves);  // per CTA
-  static const int force_s = [] {  // experiment hook: BLOCH_RESIDENT_SPINS=1|2
-    const char* e = getenv("BLOCH_RESIDENT_SPINS");
-    return e ? atoi(e) : 0;
-  }();
   // two spins per thread amortise the record decode, the pulse loads and the branches; one spin per thread
   // keeps enough warps when a CTA has few spins (shards)
   int S = spins >= kResidentTwoSpinMin ? 2 : 1;
@@ -221,29 +251,31 @@ int resident_threads(const ResidentPlan& plan, int64_t n, int n_sm, int* spins_p
   return static_cast<int>(spins / S);
 }
 
-void resident_grid(int64_t n, int n_sm, int threads, int spins_per_thread, int* grid, int* n_big) {
-  // Measured (profiles/r4b_even_waves_ab.txt): integrator -1.9% on config 2, -0.4% on config 1 (two spins per
-  // thread); with one spin per thread a CTA's time hardly depends on its warp count (config 4 -1.6%, config 3
-  // +1.1%), so those launches keep equal CTAs.  BLOCH_RESIDENT_UNEVEN=1 / =0 forces equal / dealt CTAs.
-  static const int mode = [] {
-    const char* e = getenv("BLOCH_RESIDENT_UNEVEN");
-    return e ? (atoi(e) ? 1 : 0) : -1;
-  }();
-  const bool uneven = mode >= 0 ? mode == 1 : spins_per_thread != 2;
-  const int64_t spw = 32 * spins_per_thread;                  // spins per warp
-  const int64_t warps = (n + spw - 1) / spw, tw = threads / 32;
-  const int64_t uniform = (warps + tw - 1) / tw;              // CTAs of `threads` threads each
-  const int64_t waves = (uniform + n_sm - 1) / n_sm;
-  const int64_t ctas = waves * n_sm;
-  // ctas CTAs of tw - 1 warps, `extra` of them with one more
-  const int64_t extra = warps - ctas * (tw - 1);
-  if (uneven || tw < 2 || extra < 1 || extra > ctas) {
-    *grid = static_cast<int>(uniform);
-    *n_big = static_cast<int>(uniform);
-    return;
+void resident_grid(int64_t n, int n_sm, int threads, int spins_per_thread, ResidentShape* out) {
+  ResidentShape r{};
+  r.bd_big = r.bd_small = threads;
+  r.block = ((threads + 31) / 32) * 32;
+  const int64_t spc = static_cast<int64_t>(threads) * spins_per_thread;
+  r.grid = r.n_big = static_cast<int>((n + spc - 1) / spc);
+  // Two-spin launches: the spins are dealt in units of kDealThreads threads over n_sm x waves CTAs, so CTA sizes
+  // differ by one unit and the last wave is as full as the others.  One-spin launches keep equal CTAs: there a
+  // CTA's time hardly depends on its size (profiles/r4b_even_waves_ab.txt: config 4 -1.6%, config 3 +1.1%).
+  if (spins_per_thread == 2 && resident_uneven_mode() != 1 && threads % kDealThreads == 0) {
+    const int64_t us = static_cast<int64_t>(kDealThreads) * spins_per_thread;  // spins per unit
+    const int64_t units = (n + us - 1) / us, ub = threads / kDealThreads;
+    const int64_t waves = ((units + ub - 1) / ub + n_sm - 1) / n_sm;
+    const int64_t ctas = waves * n_sm;
+    const int64_t per = (units + ctas - 1) / ctas;       // units of a big CTA
+    const int64_t extra = units - ctas * (per - 1);      // how many CTAs are big
+    if (per >= 2 && extra >= 1 && extra <= ctas && per <= ub) {
+      r.grid = static_cast<int>(ctas);
+      r.n_big = static_cast<int>(extra);
+      r.bd_big = static_cast<int>(per * kDealThreads);
+      r.bd_small = static_cast<int>((per - 1) * kDealThreads);
+      r.block = ((r.bd_big + 31) / 32) * 32;
+    }
   }
-  *grid = static_cast<int>(ctas);
-  *n_big = static_cast<int>(extra);
+  *out = r;
 }
 
 // ---------------------------------------------------------------------------
@@ -334,14 +366,14 @@ __device__ __noinline__ double3 fly_interval(const ROp* rop, const DevOp* ops, c
 template <int S>
 __global__ void __launch_bounds__(kResidentMaxThreads / S, 1) resident_integrate_kernel(const RParams rp) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  // CTAs from n_big on run one warp fewer (resident_grid): that warp leaves before the first barrier
+  // CTAs [0, n_big) run bd_big threads, the rest bd_small (resident_grid); the launch's other threads leave
+  // before the first barrier
   const int tid = threadIdx.x, cta = blockIdx.x;
-  const int bd = cta < rp.n_big ? static_cast<int>(blockDim.x) : static_cast<int>(blockDim.x) - 32;
+  const int bd = cta < rp.n_big ? rp.bd_big : rp.bd_small;
   if (tid >= bd) return;
-  const int64_t cta0 = cta < rp.n_big
-                           ? static_cast<int64_t>(cta) * (S * static_cast<int>(blockDim.x))
-                           : static_cast<int64_t>(rp.n_big) * (S * static_cast<int>(blockDim.x)) +
-                                 static_cast<int64_t>(cta - rp.n_big) * (S * bd);
+  const int64_t cta0 = cta < rp.n_big ? static_cast<int64_t>(cta) * (S * rp.bd_big)
+                                      : static_cast<int64_t>(rp.n_big) * (S * rp.bd_big) +
+                                            static_cast<int64_t>(cta - rp.n_big) * (S * rp.bd_small);
   const int64_t base = cta0 + tid;  // spin of slot 0; slot s: + s bd
   const uint32_t s_base = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
   const uint32_t s_rec = s_base;                                    // [2][kRecChunk] staged records
@@ -595,8 +627,10 @@ static cudaError_t launch_resident_s(const RParams& rp, size_t smem, int grid, i
 
 cudaError_t launch_resident(const RParams& rp, const ResidentPlan& plan, int spins_per_thread, int grid, int threads,
                             cudaStream_t stream) {
+  // the tables are laid out for the big CTAs' bd_big threads; `threads` is bd_big rounded up to whole warps
   const size_t smem = kResidentFixedBytes + resident_mats_bytes(plan) +
-                      static_cast<size_t>(plan.bytes_per_spin) * threads * spins_per_thread;
+                      static_cast<size_t>(plan.bytes_per_spin) * rp.bd_big * spins_per_thread;
+  if (smem > static_cast<size_t>(kResidentSmemBytes) || rp.bd_big > threads) return cudaErrorInvalidValue;
   if (spins_per_thread == 2) return launch_resident_s<2>(rp, smem, grid, threads, stream);
   return launch_resident_s<1>(rp, smem, grid, threads, stream);
 }
